@@ -1,0 +1,290 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Log-Fourier SP decoder (arXiv:1008.4370) -- one JSON line on rank 0.
+
+A "step" is one nbldpc_decode of the whole batch: every frame of the workload runs
+the full hot path (channel spectrum, variable node, tentative decision, check node,
+syndrome, early termination) until it stops.  Workload at N=1: BASELINE.json
+configs[1] (C2: GF(64), (2,4)-regular, N=1024, 4096 all-zero-codeword frames,
+BPSK/AWGN Eb/N0 = 1.0 dB, 50 iterations with early stop), synthetic seeded inputs.
+
+metric = sum_f K_bits * iters_used_f / T  (decoded info bits per second per iteration),
+K_bits = N m (1 - 2/k).  Multi-GPU (torchrun): weak scaling, each rank decodes its own
+4096-frame shard (global frame indices rank*F ..), NCCL only for the final counter /
+timing reductions.  L2 is flushed (256 MiB write) before every timed step.
+
+--impl reference times the CPU oracle (oracle/, fp64, OpenMP over frames) on a bounded
+sample of the same workload; it is the base contract's reference arm for this tier.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "decoded info bits/s per iteration (1/2/4/8 B200) and % of roofline"
+UNIT = "info-bit-iterations/s"
+FFMA_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # FP32 FMA, 148 SMs x 128 lanes x 1.965 GHz
+
+
+def algorithmic_flops(cfg, iters_sum: int) -> float:
+    """2 x (E q^2 + N (m+1) q) FP32 FMAs per frame-iteration: the two variable-node
+    XOR-convolutions per variable and the m+1 decision points."""
+    N, q, m = cfg["N"], cfg["q"], cfg["m"]
+    return 2.0 * iters_sum * (2 * N * q * q + N * (m + 1) * q)
+
+
+def info_bits(cfg) -> float:
+    return cfg["N"] * cfg["m"] * cfg["rate"]
+
+
+def workload_name(cfg, point):
+    return (f"{cfg['name']}: GF({cfg['q']}) (2,{cfg['k']})-regular N={cfg['N']} rate {cfg['rate']:.4g}, "
+            f"Eb/N0={cfg['ebn0'][point]} dB, max {cfg['max_iters']} iters, early stop, "
+            f"{'random' if cfg['codeword'] == 'random' else 'all-zero'} codewords")
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=5)
+        sm, smax, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                smax = max(smax, float(p[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        loaded = [x for x in sm if x > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_oracle_run(cfg, point, frame0, nframes, threads=None):
+    """Times the oracle (as it stands) on frames frame0.. of the workload; returns (value, seconds, iters)."""
+    import oracle
+
+    M, rows, cols, coeffs = synth.config_code(cfg["name"])
+    code = oracle.Code(oracle.Field(cfg["m"], cfg["poly"]), M, cfg["N"], rows, cols, coeffs)
+    llr = synth.config_llr(cfg["name"], frame0, nframes, point=point)
+    nt = threads or os.cpu_count() or 1
+    t0 = time.perf_counter()
+    r = code.lf_decode_batch(llr, cfg["max_iters"], nthreads=nt)
+    dt = time.perf_counter() - t0
+    it = int(r["iters"].sum())
+    return info_bits(cfg) * it / dt, dt, it, nt
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    vals, dts = [], []
+    nframes = args.ref_frames
+    for i in range(args.warmup + args.steps):
+        v, dt, it, nt = cpu_oracle_run(cfg, args.point, i * nframes, nframes)
+        if i >= args.warmup:
+            vals.append(v)
+            dts.append(dt)
+    total_bits = sum(v * d for v, d in zip(vals, dts))
+    value = total_bits / sum(dts)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(dts) / len(dts),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(cfg, args.point), "frames_per_step": nframes,
+                   "sample": f"{nframes} frames per step (frames i*{nframes}.. of the seeded stream)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nt, "kind": "oracle",
+                         "sample": f"{nframes} frames per step x {args.steps} steps, fp64 C oracle, OpenMP"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--point", type=int, default=0)
+    ap.add_argument("--frames", type=int, default=0, help="frames per rank (default: the config's)")
+    ap.add_argument("--slots", type=int, default=0)
+    ap.add_argument("--graph", type=int, default=0)
+    ap.add_argument("--ref-frames", type=int, default=32)
+    ap.add_argument("--cpu-frames", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--traffic", default=os.path.join(ROOT, "profiles", "r01_pass_kernel_traffic.json"))
+    args = ap.parse_args()
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_1008_4370_b200 as nb
+
+    F = args.frames or cfg["frames"]
+    M, rows, cols, coeffs = synth.config_code(cfg["name"])
+    code = nb.Code(cfg["m"], cfg["poly"], M, cfg["N"], rows, cols, coeffs)
+    llr_np = synth.config_llr(cfg["name"], rank * F, F, point=args.point)
+    llr_host = torch.from_numpy(llr_np).pin_memory()
+    llr = llr_host.to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    kw = dict(slots=args.slots, use_graph=args.graph)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        out = code.decode(llr, cfg["max_iters"], **kw)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    step_ms, iters_sum, launches, ok_sum = [], 0, 0, 0
+    for _ in range(args.steps):
+        flush.fill_(1)  # L2 flush (untimed)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out = code.decode(llr, cfg["max_iters"], **kw)
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        iters_sum += int(out["iters"].sum().item())
+        ok_sum += int(out["ok"].sum().item())
+        launches += code.last_decode_launches()
+    barrier()
+    clk = clocks.stop()
+
+    # end to end through the host-buffer C-ABI entry (H2D + decode + D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        hout = None
+        code.decode_host(llr_host, cfg["max_iters"], **kw)
+        barrier()
+        e2e_ms, e2e_iters = [], 0
+        for _ in range(args.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            hout = code.decode_host(llr_host, cfg["max_iters"], **kw)
+            e2e_ms.append(1e3 * (time.perf_counter() - t0))
+            e2e_iters += int(hout["iters"].sum())
+        barrier()
+        e2e = {"total_ms": sum(e2e_ms), "iters": e2e_iters,
+               "h2d": llr_np.nbytes, "d2h": F * cfg["N"] + F + 4 * F}
+
+    total_ms = sum(step_ms)
+    stats = torch.tensor([total_ms, iters_sum, ok_sum, F * args.steps, launches,
+                          e2e["total_ms"] if e2e else 0.0, e2e["iters"] if e2e else 0], dtype=torch.float64,
+                         device=dev)
+    if dist is not None:
+        mx = stats.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(stats, op=dist.ReduceOp.SUM)
+        stats[0], stats[5] = mx[0], mx[5]
+    total_ms, iters_all, ok_all, frames_all, launches_all, e2e_ms_max, e2e_iters_all = stats.tolist()
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return 0
+
+    value = info_bits(cfg) * iters_all / (total_ms * 1e-3)
+    per_gpu_iters = iters_sum  # this rank's frame-iterations over the timed steps
+    achieved = algorithmic_flops(cfg, per_gpu_iters) / (sum(step_ms) * 1e-3) / 1e12
+    traffic = None
+    if os.path.exists(args.traffic):
+        try:
+            traffic = json.load(open(args.traffic)).get(cfg["name"])
+        except (OSError, ValueError):
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload_name(cfg, args.point), "frames_per_gpu": F, "global_frames": F * world,
+                   "N": cfg["N"], "q": cfg["q"], "k": cfg["k"], "max_iters": cfg["max_iters"],
+                   "parallelism": f"frames sharded over {world} GPU(s), no collective in the loop",
+                   "l2": "flushed (256 MiB write) before every timed step",
+                   "slots": args.slots or "default", "mean_iters": iters_all / frames_all,
+                   "frame_error_rate": 1.0 - ok_all / frames_all},
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": FFMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FFMA_PEAK_TFLOPS, "traffic": traffic,
+                     "kernel": "nb_pass_kernel (whole decode timed; DESIGN.md 9)"},
+        "gpu_launches": int(launches_all),
+        "clocks": clk,
+    }
+    if e2e:
+        line["e2e"] = {"value": info_bits(cfg) * e2e_iters_all / (e2e_ms_max * 1e-3), "unit": UNIT,
+                       "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]}
+    if not args.no_cpu_baseline and world == 1:
+        v, dt, it, nt = cpu_oracle_run(cfg, args.point, 0, args.cpu_frames)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": nt, "kind": "oracle",
+                                "sample": f"first {args.cpu_frames} frames of the workload, {it} frame-iterations, "
+                                          f"{dt:.1f} s, fp64 C oracle with OpenMP over frames"}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,146 @@
+/*
+ * nbldpc.h -- C-ABI of the B200-native (sm_100a) batched Log-Fourier SP decoder
+ * for (j=2,k)-regular non-binary LDPC codes over GF(2^m), arXiv:1008.4370.
+ *
+ * The decoder runs the paper's Log-Fourier sum-product iteration
+ * (section 3.2): messages are 2^m-point Walsh-Hadamard spectra
+ * held as (sign, log-magnitude); the check node is a leave-one-out sum of
+ * log-magnitudes with a sign XOR after the index permutation z -> H_cv z
+ * (Appendix A :672); the degree-2 variable node is the signed
+ * log-convolution with the channel spectrum; the tentative
+ * decision uses the paper's fast bit rule and the decoder
+ * stops on a zero syndrome.
+ *
+ * All functions are plain C; no C++ exception crosses the ABI.  Every entry
+ * point returns a status; on error nothing is written to any output buffer and
+ * no kernel has been launched (validation precedes all launches), except
+ * NBLDPC_ERR_CUDA which reports a failed CUDA call (sticky device errors
+ * included).  Symbols: bit r of a symbol is the coefficient of alpha^r
+ * (PAPER.md:105-108).  Edges are numbered in "canonical order": the nonzeros of
+ * H sorted by (row, col).
+ */
+#ifndef NBLDPC_H
+#define NBLDPC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nbldpc_code_s* nbldpc_code_t;
+
+typedef enum {
+  NBLDPC_OK = 0,
+  NBLDPC_ERR_INVALID_ARGUMENT = -1, /* NULL pointer, m not in [1,8], M/N/nnz <= 0, index out of range,
+                                       coefficient not in [1, 2^m-1], frames < 1, max_iters < 1,
+                                       host pointer where a device pointer is required (or vice versa) */
+  NBLDPC_ERR_NOT_PRIMITIVE = -2,    /* prim_poly not of degree m, or alpha's period != 2^m - 1 */
+  NBLDPC_ERR_UNSUPPORTED = -3,      /* a column weight != 2, duplicate (row, col), a row degree < 2,
+                                       or a row degree too large for one thread block */
+  NBLDPC_ERR_CUDA = -4,             /* a CUDA runtime call failed */
+  NBLDPC_ERR_OUT_OF_MEMORY = -5     /* device or pinned host allocation failed */
+} nbldpc_status_t;
+
+typedef enum {
+  NBLDPC_SYNDROME_EXACT = 0, /* s_c = sum_v h_cv xhat_v over GF(2^m); the default */
+  NBLDPC_SYNDROME_PAPER = 1  /* the paper's fast Fourier-domain syndrome */
+} nbldpc_syndrome_mode_t;
+
+/* Options of nbldpc_decode_ex / nbldpc_decode_host.  Zero-initialise, then set
+ * struct_size = sizeof(nbldpc_decode_opts_t).  NULL opts = all defaults. */
+typedef struct {
+  size_t struct_size;
+  int syndrome_mode; /* nbldpc_syndrome_mode_t, default EXACT */
+  int no_early_stop; /* 0 (default): stop a frame at its first zero syndrome;
+                        1: always run max_iters iterations (diagnostic timing only) */
+  float* soft_out;   /* device, [frames][N*m] or NULL: ln|M_v(alpha^i)/M_v(0)| at the stopping
+                        iteration (posterior bit log-magnitudes) */
+  int32_t* events_out; /* device, [frames] or NULL: numerical events (variable-node DC term <= 0) */
+  int slots;         /* frames resident on the device at once (0 = library default, sized to L2) */
+  int use_graph;     /* 0 = default (CUDA graph with a device-side WHILE loop), 1 = force graph,
+                        -1 = host-driven launch loop */
+} nbldpc_decode_opts_t;
+
+/* Builds a code from H given as nnz (row, col, coefficient) triplets in any order.
+ *   m         : field GF(2^m), 1 <= m <= 8
+ *   prim_poly : primitive polynomial as a full mask including x^m (e.g. 0x7, 0x13, 0x43, 0x11D)
+ *   M, N      : H is M x N
+ *   rows, cols, coeffs : HOST arrays of length nnz, 0-based indices, coefficients in [1, 2^m-1]
+ *   out       : receives the handle (caller owns it; release with nbldpc_destroy)
+ * Every column must have exactly two nonzeros in distinct rows (j = 2) and every
+ * row at least two.  The handle copies H, builds its device tables (GF tables, canonical edge list,
+ * Fourier permutation bases) on the CUDA device current at the call, and is
+ * immutable afterwards.  Decoding must happen on that device. */
+nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int nnz, const int32_t* rows,
+                                   const int32_t* cols, const uint16_t* coeffs, nbldpc_code_t* out);
+
+/* Releases the handle and everything it allocated.  NULL is a no-op.  The caller must make sure no
+ * decode using the handle is still running (synchronise the streams first). */
+void nbldpc_destroy(nbldpc_code_t code);
+
+/* Human-readable text of a status (static storage). */
+const char* nbldpc_status_string(nbldpc_status_t s);
+
+/* Name and text of the last CUDA error that made a call on this thread return NBLDPC_ERR_CUDA or
+ * NBLDPC_ERR_OUT_OF_MEMORY ("" if none).  Thread-local storage, valid until the next call. */
+const char* nbldpc_last_cuda_error(void);
+
+/* Code dimensions (any pointer may be NULL): field degree m, rows M, columns N, edges E = 2N,
+ * largest row degree k_max. */
+nbldpc_status_t nbldpc_code_info(nbldpc_code_t code, int* m, int* M, int* N, int* E, int* k_max);
+
+/* Device bytes the decoder keeps per resident frame slot (messages, channel terms, estimates). */
+size_t nbldpc_slot_bytes(nbldpc_code_t code);
+
+/* Number of kernels the most recent decode on this handle launched (setup, pass and control
+ * kernels).  Synchronises the stream of that decode.  0 before the first decode. */
+nbldpc_status_t nbldpc_last_decode_launches(nbldpc_code_t code, long long* launches);
+
+/* Decodes `frames` independent frames (the hot path).
+ *   llr          : DEVICE, float32 [frames][N*m]; LLR = ln Pr(b=0|y)/Pr(b=1|y) of bit i of symbol v at
+ *                  index v*m + i (binary image of the codeword)
+ *   max_iters    : >= 1, the iteration limit l_max of PAPER.md:144
+ *   hard_symbols : DEVICE, uint8 [frames][N]; the fast-rule estimate at the stopping iteration
+ *   syndrome_ok  : DEVICE, uint8 [frames]; 1 iff the syndrome of that estimate is zero
+ *   iters_used   : DEVICE, int32 [frames]; the stopping iteration, in [1, max_iters]
+ *   stream       : cudaStream_t (NULL = legacy default stream)
+ * Stream-ordered: returns after enqueueing; outputs are valid when `stream` reaches that point.
+ * Results depend only on (code, llr row, max_iters, options), not on frames, batching or slots.
+ * Calls sharing one handle must be ordered on one stream (they share the handle's workspace). */
+nbldpc_status_t nbldpc_decode(nbldpc_code_t code, const float* llr, int frames, int max_iters,
+                              uint8_t* hard_symbols, uint8_t* syndrome_ok, int32_t* iters_used, void* stream);
+
+/* nbldpc_decode with options (opts may be NULL). */
+nbldpc_status_t nbldpc_decode_ex(nbldpc_code_t code, const float* llr, int frames, int max_iters,
+                                 uint8_t* hard_symbols, uint8_t* syndrome_ok, int32_t* iters_used, void* stream,
+                                 const nbldpc_decode_opts_t* opts);
+
+/* End-to-end variant with HOST buffers: copies llr_host (float32 [frames][N*m], pinned memory
+ * recommended) to the device, decodes, copies the results back to the host arrays
+ * (hard_host [frames][N], ok_host [frames], iters_host [frames]) and synchronises `stream`
+ * before returning.  opts->soft_out / events_out are ignored here. */
+nbldpc_status_t nbldpc_decode_host(nbldpc_code_t code, const float* llr_host, int frames, int max_iters,
+                                   uint8_t* hard_host, uint8_t* ok_host, int32_t* iters_host, void* stream,
+                                   const nbldpc_decode_opts_t* opts);
+
+/* One Log-Fourier iteration from a given state (step-parity tests; not on the hot path).
+ * Requires every row of H to have the same degree k, a power of two >= 4 (else
+ * NBLDPC_ERR_UNSUPPORTED): then the decoder's internal edge slots coincide with canonical order.
+ * Message format (w_in, w_out, u_out): float32 [frames][E][2^m], edge e in canonical order; entry z
+ * holds |Gamma| as the non-negative value -log2|x| (0 = magnitude 1, >= 126 = zero) and the message
+ * sign in the IEEE sign bit.
+ *   iter == 0 : computes W^(1) = CHECK-TO-VARIABLE(Lambda^(0)); w_in, u_out,
+ *               hard, soft are not used.
+ *   iter >= 1 : given W^(iter) in w_in, computes U^(iter) = VARIABLE-TO-CHECK (u_out, optional),
+ *               the tentative decision (hard [frames][N], soft [frames][N*m] optional) and
+ *               W^(iter+1) = CHECK-TO-VARIABLE(U^(iter)) in w_out.
+ * All pointers are DEVICE pointers; llr as for nbldpc_decode.  Stream-ordered. */
+nbldpc_status_t nbldpc_step(nbldpc_code_t code, const float* llr, int frames, int iter, const float* w_in,
+                            float* w_out, float* u_out, uint8_t* hard, float* soft, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NBLDPC_H */

@@ -1,0 +1,706 @@
+// decoder.cuh -- device side of the B200 Log-Fourier SP decoder (arXiv:1008.4370).
+//
+// One kernel, nb_pass_kernel<m>, advances every resident frame slot by one
+// flooding iteration.  It is check-centric and fuses, per check c and edge
+// e = (c, v) with partner edge e' = (c', v):
+//   VARIABLE TO CHECK   U_e = normalise(P_v^0 (*) W_e')    [signed XOR-convolution]
+//   TENTATIVE DECISION  at the variable's first edge only: M_v at 0, alpha^i
+//   CHECK TO VARIABLE   W_e(next) = TOT_c(pi^-1 z) - U_e(z), TOT_c = sum_j U_j(pi_j .)
+// and, in the last CTA that finishes a slot, the syndrome (PAPER.md:427 or
+// :521-526), early termination and the refill of the slot
+// with the next pending frame.
+//
+// Work decomposition: CTA (g, y) owns check group g and the
+// frame slots y, y+Y, y+2Y, ...; it keeps its edge table in registers and walks
+// its slots one after another, prefetching the next slot's messages into a
+// second shared-memory buffer with cp.async while it computes the current one.
+//
+// Numerics: messages live in HBM/L2 as float32 whose
+// magnitude is -log2|x| (>= 0) and whose IEEE sign bit is the message sign
+// (the paper's Gamma, in base 2).  The signed log-convolution
+// Gamma(sum_y Gamma^-1(L1(y) + L2(z^y))) is evaluated through the exact identity
+// Gamma^-1(a + b) = Gamma^-1(a) Gamma^-1(b): ex2 on the inputs,
+// an FFMA2 XOR-convolution, lg2 on the outputs.  The channel spectrum is the
+// closed form P_v^0(z) = prod_{i in z} tanh(L_{v,i}/2) (= WHT of the factorised
+// prior).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nb {
+
+constexpr float kFloor = 200.0f;  // -log2 of a "zero" entry; ex2(-200) flushes to 0 in float32
+constexpr uint32_t kSign = 0x80000000u;
+constexpr int kMaxSlotsPerCta = 64;
+
+struct EdgeDev {      // 32 bytes, one per internal edge slot c*kpad + j (var < 0: padding)
+  int32_t partner;    // internal index of the variable's other edge
+  int32_t var;        // variable index v
+  uint8_t h, hinv;    // h_cv and its inverse
+  uint8_t is_a;       // 1 if e is v's first edge (owner of v's tentative decision)
+  uint8_t logh;       // log_alpha h_cv
+  uint8_t pib[8];     // pi_h(e_i)    = H_cv alpha^i     (i < m), bit j = bit i of h*alpha^j
+  uint8_t pinvb[8];   // pi_h^-1(e_i) = H_cv^-1 alpha^i  (= pi_{h^-1}(e_i))
+  uint8_t plogh;      // log_alpha of the partner edge's coefficient
+  uint8_t pad[3];
+};
+static_assert(sizeof(EdgeDev) == 32, "EdgeDev layout");
+
+struct CodeDev {
+  int m, M, N, E, k_max;      // E = M * kpad internal edge slots
+  int kpad;                   // edge-slot stride per check: next power of two >= max(4, k_max)
+  const EdgeDev* edges;       // [E]
+  const uint8_t* gf_exp;      // [2(q-1)+1] alpha^i
+  const uint8_t* gf_log;      // [q]
+};
+
+struct CallDev {            // per-call arguments, written on the stream before the pass loop
+  const float* llr;
+  uint8_t* hard;
+  uint8_t* ok;
+  int32_t* iters;
+  float* soft_out;
+  int32_t* events_out;
+  int frames, max_iters, mode, early_stop;
+  int want_soft;
+  int pad[3];
+};
+
+struct WorkDev {
+  int S;
+  float* W;              // [2][S][E][q] packed messages (ping-pong by iteration parity)
+  float* Tt;             // [S][N][m]  tanh(L/2)
+  uint8_t* xhat;         // [S][N]
+  float* soft;           // [S][N][m]
+  uint8_t* con;          // [S][con_stride] per-edge syndrome contribution h_cv xhat_v (or paper bits)
+  int con_stride;        // round_up(E, 16)
+  int32_t* slot_frame;   // [S] frame index or -1
+  int32_t* slot_iter;    // [S] CHECK-TO-VARIABLE steps completed (l)
+  int32_t* slot_events;  // [S]
+  int32_t* slot_counter; // [S] CTAs finished in the current pass
+  int32_t* glob;         // [0] next frame, [1] active slots, [2] WHILE-body iterations
+  CallDev* call;
+};
+
+struct PassParams {
+  CodeDev code;
+  WorkDev ws;
+  int groups;           // G: check groups (CTAs per slot)
+  int slot_lanes;       // Y: CTA (g, y) handles slots y, y+Y, ...
+  int checks_per_cta;
+  int tpc;              // threads per check: k_max*TT padded to a power of two <= 32 or a multiple of 32
+  int step_mode;        // 1: nbldpc_step (no syndrome / finish / refill)
+  float* u_out;         // step mode: optional U^(l) dump [S][E][q]
+};
+
+template <int MB>
+struct Cfg {
+  static constexpr int Q = 1 << MB;
+  static constexpr int LR = MB < 4 ? MB : 4;   // log2 of outputs per thread
+  static constexpr int R = 1 << LR;
+  static constexpr int TT = Q / R;             // threads per convolution team
+  static constexpr int PAD = (TT > 1 && TT < 8) ? 4 * TT : 0;
+  static constexpr int VEC = Q + PAD;          // floats per team vector in smem
+  // per team: A (P^0, then T_j) | B[2] (W_e') | D[2] (W_e) | TH[2][8]
+  static constexpr int TEAM_FLOATS = 5 * VEC + 16;
+};
+
+__device__ __forceinline__ float ex2a(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2a(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// packed (sign | -log2|x|) -> linear x
+__device__ __forceinline__ float to_lin(float p) {
+  float v = ex2a(-fabsf(p));
+  return __uint_as_float(__float_as_uint(v) | (__float_as_uint(p) & kSign));
+}
+__device__ __forceinline__ float pack(float mag, uint32_t sign) {
+  mag = fminf(fmaxf(mag, 0.0f), kFloor);
+  if (mag >= kFloor) sign = 0;  // a zero carries sign 0 (reading R6)
+  return __uint_as_float(__float_as_uint(mag) | (sign & kSign));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// chunk-major smem index of element y (block y/R, 16-byte chunk (y%R)/4): keeps the
+// XOR-permuted block reads of a team conflict-free
+template <int MB>
+__device__ __forceinline__ int cm_idx(int y) {
+  using C = Cfg<MB>;
+  constexpr int R = C::R, NB = C::TT;
+  if constexpr (C::TT > 1) {
+    return ((((y & (R - 1)) >> 2) * NB + (y >> C::LR)) << 2) | (y & 3);
+  } else {
+    return y;
+  }
+}
+
+// acc(2p, 2p+1) += sum_yl a[yl] (b[2p ^ yl], b[2p ^ yl ^ 1]): the thread's share of
+// raw[z] = sum_y a[y] b[z ^ y].  (b[w], b[w^1]) is a natural pair when yl is even and
+// the swapped natural pair when yl is odd -- both free operand forms of FFMA2, whose
+// scalar operand is broadcast.
+template <int R>
+__device__ __forceinline__ void conv_block(const float (&a)[R], const float (&b)[R], float2 (&acc)[R / 2]) {
+#pragma unroll
+  for (int p = 0; p < R / 2; ++p) {
+#pragma unroll
+    for (int yl = 0; yl < R; ++yl) {
+      const int w = (2 * p) ^ yl;
+      const float2 bp = (yl & 1) ? make_float2(b[w], b[w - 1]) : make_float2(b[w], b[w + 1]);
+      acc[p] = __ffma2_rn(make_float2(a[yl], a[yl]), bp, acc[p]);
+    }
+  }
+}
+
+// barrier over the threads of one check: the warp when a check fits in it, else a named barrier
+__device__ __forceinline__ void check_sync(int lc, int tpc) {
+  if (tpc <= 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(lc + 1), "r"(tpc) : "memory");
+  }
+}
+__device__ __forceinline__ int atom_add_release_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+template <int MB, int MAXB>
+__global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(PassParams P) {
+  using C = Cfg<MB>;
+  constexpr int Q = C::Q, R = C::R, TT = C::TT, LR = C::LR, NB = C::TT;
+  extern __shared__ __align__(16) float smem[];
+  __shared__ int sh_frame[kMaxSlotsPerCta], sh_iter[kMaxSlotsPerCta], sh_list[kMaxSlotsPerCta];
+  __shared__ int sh_nact;
+
+  const CodeDev& cd = P.code;
+  const WorkDev& ws = P.ws;
+  const int g = blockIdx.x % P.groups;
+  const int yl0 = blockIdx.x / P.groups;
+  const int Y = P.slot_lanes;
+  const int nmy = (ws.S - yl0 + Y - 1) / Y;  // my slots: s = yl0 + i*Y, i < nmy
+
+  // ---- my edge (the same for every slot I process)
+  const int TPC = P.tpc;
+  const int lc = threadIdx.x / TPC;
+  const int c = g * P.checks_per_cta + lc;
+  const int j = (threadIdx.x - lc * TPC) / TT;
+  const int t = threadIdx.x & (TT - 1);
+  const bool cvalid = (lc < P.checks_per_cta) && (c < cd.M) && (j < cd.k_max);
+  const int e = c * cd.kpad + j;  // internal edge slot
+  EdgeDev ed;
+  {
+    int4 w0 = make_int4(0, -1, 0, 0), w1 = make_int4(0, 0, 0, 0);
+    if (cvalid) {
+      const int4* ep = reinterpret_cast<const int4*>(cd.edges + e);
+      w0 = __ldg(ep);
+      w1 = __ldg(ep + 1);
+    }
+    *reinterpret_cast<int4*>(&ed) = w0;
+    *(reinterpret_cast<int4*>(&ed) + 1) = w1;
+  }
+  const bool active = cvalid && ed.var >= 0;
+  const bool is_a = active && ed.is_a;
+
+  // ---- my slots' states; list of the active ones
+  for (int i = threadIdx.x; i < nmy; i += blockDim.x) {
+    const int s = yl0 + i * Y;
+    sh_frame[i] = ws.slot_frame[s];
+    sh_iter[i] = ws.slot_iter[s];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int i = 0; i < nmy; ++i)
+      if (sh_frame[i] >= 0) sh_list[n++] = i;
+    sh_nact = n;
+  }
+  __syncthreads();
+  const int nact = sh_nact;
+  if (nact == 0) return;
+
+  const int lane = threadIdx.x & 31;
+  const int slot_target = P.groups * (int)(blockDim.x >> 5);  // warps that process every slot
+  const CallDev* call = ws.call;
+  const float* llr = call->llr;
+  const int max_iters = call->max_iters;
+  const int mode = call->mode;
+  const int want_soft = call->want_soft;
+  const size_t EQ = (size_t)cd.E * Q;
+
+  // team vectors (offsets computed arithmetically so the compiler keeps shared-space accesses)
+  const int team_off = (threadIdx.x / TT) * C::TEAM_FLOATS;
+  float* A = smem + team_off;
+#define NB_BV(b) (smem + team_off + (1 + (b)) * C::VEC)
+#define NB_DV(b) (smem + team_off + (3 + (b)) * C::VEC)
+#define NB_TH(b) (smem + team_off + 5 * C::VEC + 8 * (b))
+  float* TOT = smem + (blockDim.x / TT) * C::TEAM_FLOATS + lc * Q;
+
+  // issue the asynchronous loads of slot list entry kk into buffer buf
+  auto stage = [&](int kk, int buf) {
+    if (!active) return;
+    const int i = sh_list[kk];
+    const int s = yl0 + i * Y;
+    const int f = sh_frame[i], ell = sh_iter[i];
+    float* th = NB_TH(buf);
+    if (t == 0) {
+      const float* src = ell == 0 ? llr + ((size_t)f * cd.N + ed.var) * MB : ws.Tt + ((size_t)s * cd.N + ed.var) * MB;
+#pragma unroll
+      for (int b = 0; b < MB; ++b) cp_async4(th + b, src + b);
+    }
+    if (ell == 0) return;
+    const float* Wc = ws.W + ((size_t)(ell & 1) * ws.S + s) * EQ;
+    const float* sb = Wc + (size_t)ed.partner * Q + t * R;
+    const float* sd = Wc + (size_t)e * Q + t * R;
+    if constexpr (R >= 4) {
+#pragma unroll
+      for (int c4 = 0; c4 < R / 4; ++c4) cp_async16(NB_BV(buf) + cm_idx<MB>(t * R + 4 * c4), sb + 4 * c4);
+      if (is_a) {
+#pragma unroll
+        for (int c4 = 0; c4 < R / 4; ++c4) cp_async16(NB_DV(buf) + cm_idx<MB>(t * R + 4 * c4), sd + 4 * c4);
+      }
+    } else {
+      cp_async8(NB_BV(buf), sb);
+      if (is_a) cp_async8(NB_DV(buf), sd);
+    }
+  };
+
+  stage(0, 0);
+  cp_async_commit();
+#pragma unroll 1
+  for (int kk = 0; kk < nact; ++kk) {
+    const int buf = kk & 1;
+    if (kk + 1 < nact) stage(kk + 1, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+
+    const int si = sh_list[kk];
+    const int s = yl0 + si * Y;
+    const int f = sh_frame[si];
+    const int ell = sh_iter[si];
+    const bool do_dec = ell >= 1;
+    const bool do_cn = P.step_mode || ell < max_iters;
+    float* B = NB_BV(buf);
+    float* D = NB_DV(buf);
+
+    // ---- channel terms t_i = tanh(L_{v,i}/2): computed at l = 0, cached per slot after
+    float th[MB];
+#pragma unroll
+    for (int b = 0; b < MB; ++b) th[b] = active ? NB_TH(buf)[b] : 0.0f;
+    if (ell == 0 && active) {
+#pragma unroll
+      for (int b = 0; b < MB; ++b) th[b] = tanhf(0.5f * th[b]);
+      if (is_a && t == 0) {
+#pragma unroll
+        for (int b = 0; b < MB; ++b) ws.Tt[((size_t)s * cd.N + ed.var) * MB + b] = th[b];
+      }
+    }
+    // P_v^0(z) for the thread's block z = t*R + zl (closed form)
+    float p0[R];
+    {
+      float hi = 1.0f;
+#pragma unroll
+      for (int b = LR; b < MB; ++b)
+        if ((t >> (b - LR)) & 1) hi *= th[b];
+      p0[0] = hi;
+#pragma unroll
+      for (int b = 0; b < LR; ++b)
+#pragma unroll
+        for (int jj = 0; jj < (1 << b); ++jj) p0[(1 << b) + jj] = p0[jj] * th[b];
+    }
+
+    // ---- VARIABLE TO CHECK: raw = P^0 (*) W_e'  (at l = 0, U = Lambda^0: INITIALIZATION)
+    float raw[R];
+    float dreg[TT == 1 ? Q : 1];  // W_e linear for the decision (register path)
+    if (ell == 0) {
+#pragma unroll
+      for (int zl = 0; zl < R; ++zl) raw[zl] = p0[zl];
+    } else if constexpr (TT == 1) {
+      float b[Q];
+#pragma unroll
+      for (int y = 0; y < Q; ++y) b[y] = active ? to_lin(B[y]) : 0.0f;
+      if (is_a) {
+#pragma unroll
+        for (int y = 0; y < Q; ++y) {
+          dreg[y] = to_lin(D[y]);
+          D[y] = dreg[y];  // linear copy for the paper-mode points
+        }
+      }
+      float2 acc[R / 2];
+#pragma unroll
+      for (int p = 0; p < R / 2; ++p) acc[p] = make_float2(0.0f, 0.0f);
+      conv_block<R>(p0, b, acc);
+#pragma unroll
+      for (int p = 0; p < R / 2; ++p) { raw[2 * p] = acc[p].x; raw[2 * p + 1] = acc[p].y; }
+    } else {
+      if (active) {
+        // A <- P^0 (natural layout); B, D converted in place to linear (own chunks)
+#pragma unroll
+        for (int c4 = 0; c4 < R / 4; ++c4) {
+          *reinterpret_cast<float4*>(A + t * R + 4 * c4) =
+              make_float4(p0[4 * c4], p0[4 * c4 + 1], p0[4 * c4 + 2], p0[4 * c4 + 3]);
+          float4* pb = reinterpret_cast<float4*>(B + cm_idx<MB>(t * R + 4 * c4));
+          float4 v = *pb;
+          *pb = make_float4(to_lin(v.x), to_lin(v.y), to_lin(v.z), to_lin(v.w));
+        }
+        if (is_a) {
+#pragma unroll
+          for (int c4 = 0; c4 < R / 4; ++c4) {
+            float4* pd = reinterpret_cast<float4*>(D + cm_idx<MB>(t * R + 4 * c4));
+            float4 v = *pd;
+            *pd = make_float4(to_lin(v.x), to_lin(v.y), to_lin(v.z), to_lin(v.w));
+          }
+        }
+      }
+      __syncwarp();
+      float2 acc[R / 2];
+#pragma unroll
+      for (int p = 0; p < R / 2; ++p) acc[p] = make_float2(0.0f, 0.0f);
+      if (active) {
+#pragma unroll 1
+        for (int yh = 0; yh < NB; ++yh) {
+          float a[R], b[R];
+#pragma unroll
+          for (int c4 = 0; c4 < R / 4; ++c4) {
+            float4 va = *reinterpret_cast<const float4*>(A + yh * R + 4 * c4);
+            a[4 * c4] = va.x; a[4 * c4 + 1] = va.y; a[4 * c4 + 2] = va.z; a[4 * c4 + 3] = va.w;
+            float4 vb = *reinterpret_cast<const float4*>(B + cm_idx<MB>((t ^ yh) * R + 4 * c4));
+            b[4 * c4] = vb.x; b[4 * c4 + 1] = vb.y; b[4 * c4 + 2] = vb.z; b[4 * c4 + 3] = vb.w;
+          }
+          conv_block<R>(a, b, acc);
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < R / 2; ++p) { raw[2 * p] = acc[p].x; raw[2 * p + 1] = acc[p].y; }
+    }
+
+    // ---- normalise so that entry 0 is (0,0), Gamma in base 2, packed
+    float raw0 = raw[0];
+    if constexpr (TT > 1) raw0 = __shfl_sync(0xffffffffu, raw[0], lane & ~(TT - 1));
+    uint32_t up[R];
+    {
+      const bool neutral = !(raw0 > 0.0f);  // DC term <= 0: numerical event (reading R10)
+      const float lg0 = lg2a(raw0);
+#pragma unroll
+      for (int zl = 0; zl < R; ++zl) {
+        float pk = pack(lg0 - lg2a(fabsf(raw[zl])), __float_as_uint(raw[zl]));
+        if (neutral) pk = (t == 0 && zl == 0) ? 0.0f : kFloor;
+        up[zl] = __float_as_uint(pk);
+      }
+      if (neutral && active && t == 0) atomicAdd(&ws.slot_events[s], 1);
+    }
+    if (P.u_out != nullptr && active) {
+      float* dst = P.u_out + ((size_t)s * cd.E + e) * Q + t * R;
+#pragma unroll
+      for (int zl = 0; zl < R; ++zl) dst[zl] = __uint_as_float(up[zl]);
+    }
+
+    // ---- TENTATIVE DECISION at the variable's first edge:  M_v(z) = sum_y raw(y) W_e(z ^ y)
+    // (raw is the unnormalised VN output, so M_v is exact up to a positive factor; sums in
+    // fp64 because the alpha^i points cancel strongly)
+    if (do_dec) {
+      double mv[MB + 1];
+#pragma unroll
+      for (int b = 0; b <= MB; ++b) mv[b] = 0.0;
+      if (is_a) {
+        if constexpr (TT == 1) {
+#pragma unroll
+          for (int y = 0; y < Q; ++y) {
+            mv[0] = fma((double)raw[y], (double)dreg[y], mv[0]);
+#pragma unroll
+            for (int b = 0; b < MB; ++b) mv[b + 1] = fma((double)raw[y], (double)dreg[y ^ (1 << b)], mv[b + 1]);
+          }
+        } else {
+          float dv[R];
+#pragma unroll
+          for (int c4 = 0; c4 < R / 4; ++c4) {
+            float4 v = *reinterpret_cast<const float4*>(D + cm_idx<MB>(t * R + 4 * c4));
+            dv[4 * c4] = v.x; dv[4 * c4 + 1] = v.y; dv[4 * c4 + 2] = v.z; dv[4 * c4 + 3] = v.w;
+          }
+#pragma unroll
+          for (int zl = 0; zl < R; ++zl) {
+            mv[0] = fma((double)raw[zl], (double)dv[zl], mv[0]);
+#pragma unroll
+            for (int b = 0; b < LR; ++b) mv[b + 1] = fma((double)raw[zl], (double)dv[zl ^ (1 << b)], mv[b + 1]);
+          }
+#pragma unroll
+          for (int b = LR; b < MB; ++b) {
+            const int bb = t ^ (1 << (b - LR));
+#pragma unroll
+            for (int c4 = 0; c4 < R / 4; ++c4) {
+              float4 v = *reinterpret_cast<const float4*>(D + cm_idx<MB>(bb * R + 4 * c4));
+              mv[b + 1] = fma((double)raw[4 * c4], (double)v.x, mv[b + 1]);
+              mv[b + 1] = fma((double)raw[4 * c4 + 1], (double)v.y, mv[b + 1]);
+              mv[b + 1] = fma((double)raw[4 * c4 + 2], (double)v.z, mv[b + 1]);
+              mv[b + 1] = fma((double)raw[4 * c4 + 3], (double)v.w, mv[b + 1]);
+            }
+          }
+        }
+      }
+      if constexpr (TT > 1) {
+#pragma unroll
+        for (int off = TT / 2; off >= 1; off >>= 1)
+#pragma unroll
+          for (int b = 0; b <= MB; ++b) mv[b] += __shfl_xor_sync(0xffffffffu, mv[b], off);
+      }
+      const uint32_t s0z = mv[0] < 0.0 ? 1u : 0u;  // sgn_GF2 M(0); an exact zero has sign 0
+      if (is_a && t == 0) {
+        int x = 0;
+#pragma unroll
+        for (int b = 0; b < MB; ++b) x |= (int)(((mv[b + 1] < 0.0) ? 1u : 0u) ^ s0z) << b;
+        ws.xhat[(size_t)s * cd.N + ed.var] = (uint8_t)x;
+        if (mode == 0) {  // syndrome contributions h_cv xhat_v to both checks of v
+          int ca = 0, cb = 0;
+          if (x != 0) {
+            const int lx = __ldg(&cd.gf_log[x]);
+            ca = __ldg(&cd.gf_exp[ed.logh + lx]);
+            cb = __ldg(&cd.gf_exp[ed.plogh + lx]);
+          }
+          ws.con[(size_t)s * ws.con_stride + e] = (uint8_t)ca;
+          ws.con[(size_t)s * ws.con_stride + ed.partner] = (uint8_t)cb;
+        }
+        if (want_soft) {
+          const double l0 = log(fabs(mv[0]));
+#pragma unroll
+          for (int b = 0; b < MB; ++b)
+            ws.soft[((size_t)s * cd.N + ed.var) * MB + b] = (float)(log(fabs(mv[b + 1])) - l0);
+        }
+      }
+      if (mode == 1) {
+        // paper-mode fast syndrome: sign bits of M_v(H_cv alpha^i) for both checks
+        uint64_t pa = 0, pbv = 0;
+        if (is_a) {
+          const uint32_t* ea = reinterpret_cast<const uint32_t*>(cd.edges + e) + 3;
+          const uint32_t* eb = reinterpret_cast<const uint32_t*>(cd.edges + ed.partner) + 3;
+          pa = (uint64_t)__ldg(ea) | ((uint64_t)__ldg(ea + 1) << 32);
+          pbv = (uint64_t)__ldg(eb) | ((uint64_t)__ldg(eb + 1) << 32);
+        }
+        int ma = 0, mb = 0;
+#pragma unroll 1
+        for (int i = 0; i < 2 * MB; ++i) {
+          const int z = (int)(((i < MB ? pa : pbv) >> (8 * (i < MB ? i : i - MB))) & 0xFF);
+          double acc = 0.0;
+          if (is_a) {
+#pragma unroll
+            for (int zl = 0; zl < R; ++zl) {
+              const int yy = (t * R + zl) ^ z;
+              acc = fma((double)raw[zl], (double)D[cm_idx<MB>(yy)], acc);
+            }
+          }
+          if constexpr (TT > 1) {
+#pragma unroll
+            for (int off = TT / 2; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+          }
+          const int bit = (int)(((acc < 0.0) ? 1u : 0u) ^ s0z);
+          if (i < MB) ma |= bit << i; else mb |= bit << (i - MB);
+        }
+        if (is_a && t == 0) {
+          ws.con[(size_t)s * ws.con_stride + e] = (uint8_t)ma;
+          ws.con[(size_t)s * ws.con_stride + ed.partner] = (uint8_t)mb;
+        }
+      }
+    }
+
+    // ---- CHECK TO VARIABLE: T_j(w) = U_j(pi_j w);  W_j(z) = sum_{j' != j} T_j'(pi_j^-1 z)
+    if (do_cn) {
+      int pl[R];  // pi_h^-1 of the thread's outputs (linear map: XOR of basis images)
+      {
+        int base = 0;
+#pragma unroll
+        for (int b = LR; b < MB; ++b)
+          if ((t >> (b - LR)) & 1) base ^= ed.pinvb[b];
+        pl[0] = base;
+#pragma unroll
+        for (int b = 0; b < LR; ++b)
+#pragma unroll
+          for (int jj = 0; jj < (1 << b); ++jj) pl[(1 << b) + jj] = pl[jj] ^ ed.pinvb[b];
+      }
+      if constexpr (TT > 1) __syncwarp();  // team done reading A in the convolution
+      if (active) {
+#pragma unroll
+        for (int zl = 0; zl < R; ++zl) A[pl[zl]] = __uint_as_float(up[zl]);
+      } else if (cvalid) {
+#pragma unroll
+        for (int zl = 0; zl < R; ++zl) A[t * R + zl] = 0.0f;  // padding edge: neutral (0, 0)
+      }
+      check_sync(lc, TPC);
+      if (lc < P.checks_per_cta && c < cd.M) {
+        const float* Ab = smem + (size_t)(lc * (TPC / TT)) * C::TEAM_FLOATS;
+        for (int w = threadIdx.x - lc * TPC; w < Q; w += TPC) {
+          float mag = 0.0f;
+          uint32_t sg = 0;
+          for (int jj = 0; jj < cd.k_max; ++jj) {
+            const float x = Ab[(size_t)jj * C::TEAM_FLOATS + w];
+            mag += fabsf(x);
+            sg ^= __float_as_uint(x);
+          }
+          TOT[w] = __uint_as_float(__float_as_uint(mag) | (sg & kSign));
+        }
+      }
+      check_sync(lc, TPC);
+      if (active) {
+        float out[R];
+#pragma unroll
+        for (int zl = 0; zl < R; ++zl) {
+          const float x = TOT[pl[zl]];
+          const float u = __uint_as_float(up[zl]);
+          out[zl] = pack(fabsf(x) - fabsf(u), __float_as_uint(x) ^ up[zl]);
+        }
+        float* dst = ws.W + ((size_t)((ell + 1) & 1) * ws.S + s) * EQ + (size_t)e * Q + t * R;
+        if constexpr (R >= 4) {
+#pragma unroll
+          for (int c4 = 0; c4 < R / 4; ++c4)
+            reinterpret_cast<float4*>(dst)[c4] = make_float4(out[4 * c4], out[4 * c4 + 1], out[4 * c4 + 2], out[4 * c4 + 3]);
+        } else {
+#pragma unroll
+          for (int zl = 0; zl < R; ++zl) dst[zl] = out[zl];
+        }
+      }
+    }
+
+    // ---- slot bookkeeping, per warp: the warp that finishes the slot last (over all CTAs of
+    // the slot) runs the syndrome, the stopping rule and the refill.  The release add is
+    // cumulative over the warp's writes (ordered by __syncwarp); the finisher acquires.
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = atom_add_release_gpu(&ws.slot_counter[s], 1) == slot_target - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) continue;
+    fence_acquire_gpu();
+    if (lane == 0) ws.slot_counter[s] = 0;
+    if (P.step_mode) continue;
+    if (ell == 0) {
+      if (lane == 0) ws.slot_iter[s] = 1;
+      continue;
+    }
+    // syndrome: s_c = XOR of the contribution bytes on the check's kpad edge slots, read as
+    // 16-byte vectors; a check spans kpad/16 consecutive lanes when kpad > 16
+    int bad = 0;
+    {
+      const uint4* cs = reinterpret_cast<const uint4*>(ws.con + (size_t)s * ws.con_stride);
+      const int nvec = ws.con_stride >> 4;
+      const int kp = cd.kpad;
+#pragma unroll 4
+      for (int it = 0; it < (nvec + 31) / 32; ++it) {
+        const int v = lane + 32 * it;
+        const uint4 x = v < nvec ? __ldcg(cs + v) : make_uint4(0, 0, 0, 0);
+        uint32_t f0, f1 = 0, f2 = 0, f3 = 0;
+        if (kp == 4) {
+          f0 = x.x; f1 = x.y; f2 = x.z; f3 = x.w;
+        } else if (kp == 8) {
+          f0 = x.x ^ x.y; f1 = x.z ^ x.w;
+        } else {
+          f0 = x.x ^ x.y ^ x.z ^ x.w;
+          for (int off = 1; off < (kp >> 4); off <<= 1) f0 ^= __shfl_xor_sync(0xffffffffu, f0, off);
+        }
+        f0 ^= f0 >> 16; f1 ^= f1 >> 16; f2 ^= f2 >> 16; f3 ^= f3 >> 16;
+        f0 ^= f0 >> 8; f1 ^= f1 >> 8; f2 ^= f2 >> 8; f3 ^= f3 >> 8;
+        bad |= (int)((f0 | f1 | f2 | f3) & 0xFFu);
+      }
+    }
+    const int ok = !__any_sync(0xffffffffu, bad != 0);
+    const bool done = (call->early_stop && ok) || ell >= max_iters;
+    if (!done) {
+      if (lane == 0) ws.slot_iter[s] = ell + 1;
+      continue;
+    }
+    const int N = cd.N;
+    if ((N & 15) == 0) {  // 16-byte copies (the frame's rows are 16-byte aligned)
+      const uint4* src = reinterpret_cast<const uint4*>(ws.xhat + (size_t)s * N);
+      uint4* dst = reinterpret_cast<uint4*>(call->hard + (size_t)f * N);
+#pragma unroll 4
+      for (int v = lane; v < (N >> 4); v += 32) dst[v] = __ldcg(src + v);
+    } else {
+      for (int v = lane; v < N; v += 32) call->hard[(size_t)f * N + v] = __ldcg(&ws.xhat[(size_t)s * N + v]);
+    }
+    if (want_soft) {
+#pragma unroll 4
+      for (int i = lane; i < N * MB; i += 32)
+        call->soft_out[(size_t)f * N * MB + i] = __ldcg(&ws.soft[(size_t)s * N * MB + i]);
+    }
+    if (lane == 0) {
+      call->ok[f] = (uint8_t)ok;
+      call->iters[f] = ell;
+      if (call->events_out) call->events_out[f] = ws.slot_events[s];
+      ws.slot_events[s] = 0;
+      const int nf = atomicAdd(&ws.glob[0], 1);
+      if (nf < call->frames) {
+        ws.slot_frame[s] = nf;
+        ws.slot_iter[s] = 0;
+      } else {
+        ws.slot_frame[s] = -1;
+        atomicSub(&ws.glob[1], 1);
+      }
+    }
+  }
+  cp_async_wait<0>();
+#undef NB_BV
+#undef NB_DV
+#undef NB_TH
+}
+
+__global__ void nb_setup_kernel(WorkDev ws, CallDev call) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) {
+    *ws.call = call;
+    const int n = call.frames < ws.S ? call.frames : ws.S;
+    ws.glob[0] = n;
+    ws.glob[1] = n;
+    ws.glob[2] = 0;
+  }
+  if (i < ws.S) {
+    ws.slot_frame[i] = i < call.frames ? i : -1;
+    ws.slot_iter[i] = 0;
+    ws.slot_events[i] = 0;
+    ws.slot_counter[i] = 0;
+  }
+}
+
+// step mode: slots hold frames 0..frames-1 at iteration `iter`
+__global__ void nb_step_setup_kernel(WorkDev ws, CallDev call, int iter) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) *ws.call = call;
+  if (i < ws.S) {
+    ws.slot_frame[i] = i;
+    ws.slot_iter[i] = iter;
+    ws.slot_events[i] = 0;
+    ws.slot_counter[i] = 0;
+  }
+}
+
+__global__ void nb_tanh_kernel(const float* llr, float* Tt, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    Tt[i] = tanhf(0.5f * llr[i]);
+}
+
+__global__ void nb_control_kernel(int32_t* glob, cudaGraphConditionalHandle h) {
+  if (threadIdx.x == 0) {
+    glob[2] += 1;  // WHILE-body iterations (launch accounting)
+    if (*(volatile const int32_t*)&glob[1] == 0) cudaGraphSetConditional(h, 0);
+  }
+}
+
+}  // namespace nb

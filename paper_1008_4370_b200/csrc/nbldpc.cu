@@ -1,0 +1,715 @@
+// nbldpc.cu -- host side of the C-ABI declared in include/nbldpc.h.
+//
+// Builds the immutable code tables (GF(2^m) exp/log, the k_max-padded edge
+// table with the Fourier-domain permutation bases of PAPER.md Appendix A), owns
+// the per-handle workspace (frame slots resident in L2/HBM), and drives the
+// pass kernel either through a CUDA graph whose WHILE conditional node loops on
+// the device until every frame has stopped, or through a host launch loop.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "../../include/nbldpc.h"
+#include "decoder.cuh"
+
+using nb::CallDev;
+using nb::CodeDev;
+using nb::EdgeDev;
+using nb::PassParams;
+using nb::WorkDev;
+
+namespace {
+
+constexpr int kPassesPerGraphIter = 8;               // pass kernels per WHILE-body iteration
+constexpr size_t kDefaultSlotBudget = 64ull << 20;  // bytes of slot state kept L2-resident
+constexpr int kBigBlock = 512;                       // block-size variant for k_max * TT > 256
+
+struct Workspace {
+  int S = 0, Y = 1;
+  void* base = nullptr;
+  size_t bytes = 0;
+  WorkDev dev{};
+  int32_t* host_flag = nullptr;  // pinned, host loop
+  cudaGraphExec_t graph = nullptr;
+  float* llr_stage = nullptr;  // device staging for nbldpc_decode_host
+  size_t llr_stage_bytes = 0;
+  uint8_t* out_stage = nullptr;
+  size_t out_stage_bytes = 0;
+  // launch accounting of the most recent decode
+  cudaStream_t last_stream = nullptr;
+  int last_graph = 0;
+  long long last_host_launches = 0;
+};
+
+}  // namespace
+
+struct nbldpc_code_s {
+  int device = 0;
+  int m = 0, q = 0, M = 0, N = 0, E = 0, k_max = 0, kpad = 4, con_stride = 16;
+  bool row_regular = true;
+  uint32_t poly = 0;
+  EdgeDev* edges_d = nullptr;
+  uint8_t* gf_exp_d = nullptr;
+  uint8_t* gf_log_d = nullptr;
+  std::mutex mu;
+  Workspace ws;
+  // launch geometry
+  int TT = 1, TPC = 1, CPC = 1, groups = 1, block = 32, big = 0, blocks_per_sm = 1, sms = 148;  // TPC padded
+  size_t smem = 0;
+};
+
+namespace {
+
+thread_local char g_last_error[256] = "";
+
+nbldpc_status_t cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return NBLDPC_OK;
+  snprintf(g_last_error, sizeof(g_last_error), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+  if (e == cudaErrorMemoryAllocation) return NBLDPC_ERR_OUT_OF_MEMORY;
+  return NBLDPC_ERR_CUDA;
+}
+
+#define NB_TRY(expr)                               \
+  do {                                             \
+    cudaError_t e_ = (expr);                       \
+    if (e_ != cudaSuccess) return cuda_status(e_); \
+  } while (0)
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int team_threads(int m) { return m <= 4 ? 1 : (1 << m) / 16; }
+
+int team_floats(int m) {
+  const int q = 1 << m;
+  const int tt = team_threads(m);
+  const int pad = (tt > 1 && tt < 8) ? 4 * tt : 0;
+  return 5 * (q + pad) + 16;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+size_t slot_bytes_of(const nbldpc_code_s* c) {
+  const size_t q = c->q;
+  size_t b = 0;
+  b += 2 * (size_t)c->E * q * sizeof(float);  // W ping-pong
+  b += (size_t)c->N * c->m * sizeof(float);   // tanh
+  b += (size_t)c->N;                          // xhat
+  b += (size_t)c->N * c->m * sizeof(float);   // soft
+  b += (size_t)c->con_stride;                 // syndrome contributions
+  b += 4 * sizeof(int32_t);
+  return b;
+}
+
+void free_workspace(Workspace& w) {
+  if (w.graph) cudaGraphExecDestroy(w.graph);
+  if (w.base) cudaFree(w.base);
+  if (w.host_flag) cudaFreeHost(w.host_flag);
+  if (w.llr_stage) cudaFree(w.llr_stage);
+  if (w.out_stage) cudaFree(w.out_stage);
+  w = Workspace{};
+}
+
+template <int MB, int MAXB>
+void* pass_fn() { return reinterpret_cast<void*>(&nb::nb_pass_kernel<MB, MAXB>); }
+
+void* pass_kernel_ptr(int m, int big) {
+  switch (m * 2 + (big ? 1 : 0)) {
+    case 2: return pass_fn<1, 256>();
+    case 3: return pass_fn<1, kBigBlock>();
+    case 4: return pass_fn<2, 256>();
+    case 5: return pass_fn<2, kBigBlock>();
+    case 6: return pass_fn<3, 256>();
+    case 7: return pass_fn<3, kBigBlock>();
+    case 8: return pass_fn<4, 256>();
+    case 9: return pass_fn<4, kBigBlock>();
+    case 10: return pass_fn<5, 256>();
+    case 11: return pass_fn<5, kBigBlock>();
+    case 12: return pass_fn<6, 256>();
+    case 13: return pass_fn<6, kBigBlock>();
+    case 14: return pass_fn<7, 256>();
+    case 15: return pass_fn<7, kBigBlock>();
+    case 16: return pass_fn<8, 256>();
+    case 17: return pass_fn<8, kBigBlock>();
+  }
+  return nullptr;
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a property of the kernel (one instantiation per
+// (m, block variant)) shared by every code on the device: only ever raise it.
+std::mutex g_attr_mu;
+size_t g_attr_smem[64][18] = {};
+
+cudaError_t ensure_smem_attr(const nbldpc_code_s* c) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  const int d = c->device & 63, k = c->m * 2 + c->big;
+  if (g_attr_smem[d][k] >= c->smem) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(pass_kernel_ptr(c->m, c->big), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)c->smem);
+  if (e == cudaSuccess) g_attr_smem[d][k] = c->smem;
+  return e;
+}
+
+// Slot lanes Y: CTA (g, y) processes slots y, y+Y, ... .  Minimise the makespan
+// ceil(G*Y / resident CTAs) * ceil(S / Y) (waves x slots per CTA).
+int choose_lanes(const nbldpc_code_s* c, int S) {
+  const long target = (long)c->blocks_per_sm * c->sms;
+  int best = 1;
+  long best_cost = -1;
+  for (int Y = 1; Y <= S; ++Y) {
+    const long per = (S + Y - 1) / Y;
+    if (per > nb::kMaxSlotsPerCta) continue;
+    const long waves = ((long)c->groups * Y + target - 1) / target;
+    const long cost = waves * per;
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = Y;
+    }
+  }
+  return best;
+}
+
+nbldpc_status_t ensure_workspace(nbldpc_code_s* c, int S) {
+  Workspace& w = c->ws;
+  if (w.base && w.S == S) return NBLDPC_OK;
+  if (w.base) {
+    cudaDeviceSynchronize();
+    if (w.graph) cudaGraphExecDestroy(w.graph);
+    w.graph = nullptr;
+    cudaFree(w.base);
+    w.base = nullptr;
+    cudaGetLastError();
+  }
+  const size_t q = c->q;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  const size_t oW = take(2 * (size_t)S * c->E * q * sizeof(float));
+  const size_t oT = take((size_t)S * c->N * c->m * sizeof(float));
+  const size_t oX = take((size_t)S * c->N);
+  const size_t oS = take((size_t)S * c->N * c->m * sizeof(float));
+  const size_t oP = take((size_t)S * c->con_stride);
+  const size_t oF = take((size_t)S * sizeof(int32_t));
+  const size_t oI = take((size_t)S * sizeof(int32_t));
+  const size_t oV = take((size_t)S * sizeof(int32_t));
+  const size_t oC = take((size_t)S * sizeof(int32_t));
+  const size_t oG = take(16 * sizeof(int32_t));
+  const size_t oK = take(sizeof(CallDev));
+  void* base = nullptr;
+  NB_TRY(cudaMalloc(&base, off));
+  NB_TRY(cudaMemset(base, 0, off));  // padding edge slots of `con` must stay zero
+  char* b = static_cast<char*>(base);
+  w.base = base;
+  w.bytes = off;
+  w.S = S;
+  w.Y = choose_lanes(c, S);
+  w.dev.S = S;
+  w.dev.W = reinterpret_cast<float*>(b + oW);
+  w.dev.Tt = reinterpret_cast<float*>(b + oT);
+  w.dev.xhat = reinterpret_cast<uint8_t*>(b + oX);
+  w.dev.soft = reinterpret_cast<float*>(b + oS);
+  w.dev.con = reinterpret_cast<uint8_t*>(b + oP);
+  w.dev.con_stride = c->con_stride;
+  w.dev.slot_frame = reinterpret_cast<int32_t*>(b + oF);
+  w.dev.slot_iter = reinterpret_cast<int32_t*>(b + oI);
+  w.dev.slot_events = reinterpret_cast<int32_t*>(b + oV);
+  w.dev.slot_counter = reinterpret_cast<int32_t*>(b + oC);
+  w.dev.glob = reinterpret_cast<int32_t*>(b + oG);
+  w.dev.call = reinterpret_cast<CallDev*>(b + oK);
+  if (!w.host_flag) NB_TRY(cudaMallocHost(&w.host_flag, 64));
+  return NBLDPC_OK;
+}
+
+PassParams make_params(const nbldpc_code_s* c, int step_mode, float* u_out) {
+  PassParams P{};
+  P.code.m = c->m;
+  P.code.M = c->M;
+  P.code.N = c->N;
+  P.code.E = c->E;
+  P.code.k_max = c->k_max;
+  P.code.kpad = c->kpad;
+  P.code.edges = c->edges_d;
+  P.code.gf_exp = c->gf_exp_d;
+  P.code.gf_log = c->gf_log_d;
+  P.ws = c->ws.dev;
+  P.groups = c->groups;
+  P.slot_lanes = c->ws.Y;
+  P.checks_per_cta = c->CPC;
+  P.tpc = c->TPC;
+  P.step_mode = step_mode;
+  P.u_out = u_out;
+  return P;
+}
+
+dim3 pass_grid(const nbldpc_code_s* c) { return dim3((unsigned)(c->groups * c->ws.Y)); }
+
+cudaError_t launch_pass(const nbldpc_code_s* c, const PassParams& P, cudaStream_t st) {
+  void* args[] = {const_cast<PassParams*>(&P)};
+  return cudaLaunchKernel(pass_kernel_ptr(c->m, c->big), pass_grid(c), dim3(c->block), args, c->smem, st);
+}
+
+nbldpc_status_t build_graph(nbldpc_code_s* c) {
+  Workspace& w = c->ws;
+  if (w.graph) return NBLDPC_OK;
+  cudaGraph_t g = nullptr;
+  NB_TRY(cudaGraphCreate(&g, 0));
+  auto fail = [&](cudaError_t e) {
+    cudaGraphDestroy(g);
+    return cuda_status(e);
+  };
+  cudaGraphConditionalHandle h;
+  if (cudaError_t e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault)) return fail(e);
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cn;
+  if (cudaError_t e = cudaGraphAddNode(&cn, g, nullptr, 0, &cp)) return fail(e);
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  PassParams P = make_params(c, 0, nullptr);  // node parameters are copied at creation
+  cudaGraphNode_t prev = nullptr;
+  for (int i = 0; i < kPassesPerGraphIter; ++i) {
+    cudaGraphNodeParams kp = {};
+    kp.type = cudaGraphNodeTypeKernel;
+    kp.kernel.func = pass_kernel_ptr(c->m, c->big);
+    kp.kernel.gridDim = pass_grid(c);
+    kp.kernel.blockDim = dim3(c->block);
+    kp.kernel.sharedMemBytes = (unsigned)c->smem;
+    void* args[] = {&P};
+    kp.kernel.kernelParams = args;
+    cudaGraphNode_t kn;
+    if (cudaError_t e = cudaGraphAddNode(&kn, body, prev ? &prev : nullptr, prev ? 1 : 0, &kp)) return fail(e);
+    prev = kn;
+  }
+  {
+    cudaGraphNodeParams kp = {};
+    kp.type = cudaGraphNodeTypeKernel;
+    kp.kernel.func = reinterpret_cast<void*>(&nb::nb_control_kernel);
+    kp.kernel.gridDim = dim3(1);
+    kp.kernel.blockDim = dim3(32);
+    int32_t* glob = w.dev.glob;
+    void* args[] = {&glob, &h};
+    kp.kernel.kernelParams = args;
+    cudaGraphNode_t kn;
+    if (cudaError_t e = cudaGraphAddNode(&kn, body, &prev, 1, &kp)) return fail(e);
+  }
+  cudaError_t e = cudaGraphInstantiate(&w.graph, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    w.graph = nullptr;
+    return cuda_status(e);
+  }
+  return NBLDPC_OK;
+}
+
+int default_slots(const nbldpc_code_s* c, int frames) {
+  const size_t sb = slot_bytes_of(c);
+  long S = (long)(kDefaultSlotBudget / sb);
+  if (S < 1) S = 1;
+  if (S > frames) S = frames;
+  return (int)S;
+}
+
+nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int max_iters, uint8_t* hard,
+                            uint8_t* ok, int32_t* iters, cudaStream_t st, const nbldpc_decode_opts_t* opts) {
+  int mode = 0, early = 1, slots = 0, use_graph = 0;
+  float* soft = nullptr;
+  int32_t* events = nullptr;
+  if (opts) {
+    if (opts->struct_size < sizeof(nbldpc_decode_opts_t)) return NBLDPC_ERR_INVALID_ARGUMENT;
+    mode = opts->syndrome_mode;
+    early = opts->no_early_stop ? 0 : 1;
+    soft = opts->soft_out;
+    events = opts->events_out;
+    slots = opts->slots;
+    use_graph = opts->use_graph;
+  }
+  if (mode != 0 && mode != 1) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (slots < 0) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if ((soft && !is_device_ptr(soft)) || (events && !is_device_ptr(events))) return NBLDPC_ERR_INVALID_ARGUMENT;
+  const int S = slots > 0 ? std::min(slots, frames) : default_slots(c, frames);
+  NB_TRY(cudaSetDevice(c->device));
+  nbldpc_status_t rs = ensure_workspace(c, S);
+  if (rs != NBLDPC_OK) return rs;
+  Workspace& w = c->ws;
+  CallDev call{};
+  call.llr = llr;
+  call.hard = hard;
+  call.ok = ok;
+  call.iters = iters;
+  call.soft_out = soft;
+  call.events_out = events;
+  call.frames = frames;
+  call.max_iters = max_iters;
+  call.mode = mode;
+  call.early_stop = early;
+  call.want_soft = soft != nullptr;
+  nb::nb_setup_kernel<<<(S + 255) / 256, 256, 0, st>>>(w.dev, call);
+  NB_TRY(cudaGetLastError());
+  w.last_stream = st;
+  w.last_graph = use_graph >= 0;
+  w.last_host_launches = 1;
+  if (use_graph >= 0) {
+    rs = build_graph(c);
+    if (rs != NBLDPC_OK) return rs;
+    NB_TRY(cudaGraphLaunch(w.graph, st));
+    return NBLDPC_OK;
+  }
+  // host-driven loop: launch passes, poll the active-slot counter every few passes
+  PassParams P = make_params(c, 0, nullptr);
+  for (;;) {
+    for (int i = 0; i < kPassesPerGraphIter; ++i) {
+      NB_TRY(launch_pass(c, P, st));
+      w.last_host_launches++;
+    }
+    NB_TRY(cudaMemcpyAsync(w.host_flag, w.dev.glob + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    NB_TRY(cudaStreamSynchronize(st));
+    if (*w.host_flag == 0) break;
+  }
+  return NBLDPC_OK;
+}
+
+bool gf_tables(int m, uint32_t poly, std::vector<int>& ex, std::vector<int>& lg) {
+  const int q = 1 << m;
+  if ((poly >> m) != 1u) return false;
+  ex.assign(2 * (q - 1) + 1, 0);
+  lg.assign(q, -1);
+  int a = 1;
+  for (int i = 0; i < q - 1; ++i) {
+    if (lg[a] != -1) return false;
+    ex[i] = a;
+    lg[a] = i;
+    a <<= 1;
+    if (a & q) a ^= (int)poly;
+  }
+  if (a != 1) return false;
+  for (int i = q - 1; i < 2 * (q - 1); ++i) ex[i] = ex[i - (q - 1)];
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nbldpc_last_cuda_error(void) { return g_last_error; }
+
+const char* nbldpc_status_string(nbldpc_status_t s) {
+  switch (s) {
+    case NBLDPC_OK: return "ok";
+    case NBLDPC_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case NBLDPC_ERR_NOT_PRIMITIVE: return "polynomial is not primitive of degree m";
+    case NBLDPC_ERR_UNSUPPORTED: return "unsupported parity-check matrix (column weight must be 2, rows >= 2)";
+    case NBLDPC_ERR_CUDA: return "CUDA error";
+    case NBLDPC_ERR_OUT_OF_MEMORY: return "out of memory";
+  }
+  return "unknown status";
+}
+
+nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int nnz, const int32_t* rows,
+                                   const int32_t* cols, const uint16_t* coeffs, nbldpc_code_t* out) {
+  if (!out || !rows || !cols || !coeffs) return NBLDPC_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (m < 1 || m > 8 || M <= 0 || N <= 0 || nnz <= 0) return NBLDPC_ERR_INVALID_ARGUMENT;
+  const int q = 1 << m;
+  for (int i = 0; i < nnz; ++i) {
+    if (rows[i] < 0 || rows[i] >= M || cols[i] < 0 || cols[i] >= N) return NBLDPC_ERR_INVALID_ARGUMENT;
+    if (coeffs[i] < 1 || coeffs[i] >= q) return NBLDPC_ERR_INVALID_ARGUMENT;
+  }
+  std::vector<int> ex, lg;
+  if (!gf_tables(m, prim_poly, ex, lg)) return NBLDPC_ERR_NOT_PRIMITIVE;
+  auto gmul = [&](int a, int b) { return (a && b) ? ex[lg[a] + lg[b]] : 0; };
+  auto ginv = [&](int a) { return ex[(q - 1 - lg[a]) % (q - 1)]; };
+
+  // canonical order: sorted by (row, col)
+  std::vector<int> order(nnz);
+  for (int i = 0; i < nnz; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(),
+            [&](int a, int b) { return rows[a] != rows[b] ? rows[a] < rows[b] : cols[a] < cols[b]; });
+  for (int i = 1; i < nnz; ++i)
+    if (rows[order[i]] == rows[order[i - 1]] && cols[order[i]] == cols[order[i - 1]]) return NBLDPC_ERR_UNSUPPORTED;
+  std::vector<int> colw(N, 0), roww(M, 0);
+  for (int i = 0; i < nnz; ++i) {
+    colw[cols[i]]++;
+    roww[rows[i]]++;
+  }
+  for (int v = 0; v < N; ++v)
+    if (colw[v] != 2) return NBLDPC_ERR_UNSUPPORTED;
+  int k_max = 0, k_min = 1 << 30;
+  for (int r = 0; r < M; ++r) {
+    if (roww[r] < 2) return NBLDPC_ERR_UNSUPPORTED;
+    k_max = std::max(k_max, roww[r]);
+    k_min = std::min(k_min, roww[r]);
+  }
+  const int tt = team_threads(m);
+  if (k_max * tt > kBigBlock) return NBLDPC_ERR_UNSUPPORTED;
+
+  // internal edge slots: e = c * kpad + j (j-th nonzero of row c in canonical order), kpad the
+  // next power of two >= max(4, k_max); the padding slots have var = -1
+  int kpad = 4;
+  while (kpad < k_max) kpad <<= 1;
+  const int E = M * kpad;
+  std::vector<EdgeDev> edges(E);
+  for (auto& ed : edges) {
+    std::memset(&ed, 0, sizeof(ed));
+    ed.var = -1;
+  }
+  std::vector<int> first(N, -1), fill(M, 0);
+  for (int n = 0; n < nnz; ++n) {
+    const int i = order[n];
+    const int r = rows[i];
+    const int e = r * kpad + fill[r]++;
+    EdgeDev& ed = edges[e];
+    ed.var = cols[i];
+    ed.h = (uint8_t)coeffs[i];
+    ed.hinv = (uint8_t)ginv(coeffs[i]);
+    ed.logh = (uint8_t)lg[ed.h];
+    // pi_h(e_i): bit j = bit i of h * alpha^j  (M_h^T e_i)
+    for (int bi = 0; bi < m; ++bi) {
+      int img = 0, imginv = 0;
+      for (int bj = 0; bj < m; ++bj) {
+        img |= ((gmul(ed.h, 1 << bj) >> bi) & 1) << bj;
+        imginv |= ((gmul(ed.hinv, 1 << bj) >> bi) & 1) << bj;
+      }
+      ed.pib[bi] = (uint8_t)img;
+      ed.pinvb[bi] = (uint8_t)imginv;
+    }
+    const int v = cols[i];
+    if (first[v] < 0) {
+      first[v] = e;
+      ed.is_a = 1;
+    } else {
+      EdgeDev& ea = edges[first[v]];
+      ed.partner = first[v];
+      ed.plogh = ea.logh;
+      ea.partner = e;
+      ea.plogh = ed.logh;
+    }
+  }
+  std::vector<uint8_t> gexp(2 * (q - 1) + 1), glog(q, 0);
+  for (size_t i = 0; i < gexp.size(); ++i) gexp[i] = (uint8_t)ex[i];
+  for (int x = 1; x < q; ++x) glog[x] = (uint8_t)lg[x];
+
+  nbldpc_code_s* c = new (std::nothrow) nbldpc_code_s();
+  if (!c) return NBLDPC_ERR_OUT_OF_MEMORY;
+  cudaGetDevice(&c->device);
+  c->m = m;
+  c->q = q;
+  c->M = M;
+  c->N = N;
+  c->E = E;
+  c->k_max = k_max;
+  c->kpad = kpad;
+  c->con_stride = (int)align_up((size_t)E, 16);
+  c->row_regular = k_min == k_max && kpad == k_max;
+  c->poly = prim_poly;
+  auto bail = [&](cudaError_t e) {
+    cudaGetLastError();
+    nbldpc_destroy(c);
+    return cuda_status(e);
+  };
+  if (cudaError_t e = cudaMalloc(&c->edges_d, sizeof(EdgeDev) * E)) return bail(e);
+  if (cudaError_t e = cudaMalloc(&c->gf_exp_d, gexp.size())) return bail(e);
+  if (cudaError_t e = cudaMalloc(&c->gf_log_d, q)) return bail(e);
+  if (cudaError_t e = cudaMemcpy(c->edges_d, edges.data(), sizeof(EdgeDev) * E, cudaMemcpyHostToDevice)) return bail(e);
+  if (cudaError_t e = cudaMemcpy(c->gf_exp_d, gexp.data(), gexp.size(), cudaMemcpyHostToDevice)) return bail(e);
+  if (cudaError_t e = cudaMemcpy(c->gf_log_d, glog.data(), q, cudaMemcpyHostToDevice)) return bail(e);
+  // launch geometry: teams of TT threads per edge, k_max teams per check, <= 256 threads per CTA
+  c->TT = tt;
+  {
+    // threads per check, padded so that a check never straddles a warp (<= 32: a power of two)
+    // or fills whole warps (> 32: a multiple of 32, synchronised by a named barrier)
+    int tpc = k_max * tt;
+    if (tpc <= 32) {
+      int p2 = 1;
+      while (p2 < tpc) p2 <<= 1;
+      tpc = p2;
+    } else {
+      tpc = (int)align_up((size_t)tpc, 32);
+    }
+    c->TPC = tpc;
+  }
+  if (c->TPC > kBigBlock) {
+    nbldpc_destroy(c);
+    return NBLDPC_ERR_UNSUPPORTED;
+  }
+  c->big = c->TPC > 256 ? 1 : 0;
+  c->CPC = std::min(std::max(1, 256 / c->TPC), M);
+  c->groups = (M + c->CPC - 1) / c->CPC;
+  c->block = (int)align_up((size_t)c->CPC * c->TPC, 32);
+  c->smem = ((size_t)(c->block / tt) * team_floats(m) + (size_t)c->CPC * q) * sizeof(float);
+  if (cudaError_t e = ensure_smem_attr(c)) return bail(e);
+  int bps = 0;
+  if (cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pass_kernel_ptr(m, c->big), c->block, c->smem))
+    return bail(e);
+  if (bps < 1) {
+    nbldpc_destroy(c);
+    return NBLDPC_ERR_UNSUPPORTED;
+  }
+  c->blocks_per_sm = bps;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device);
+  *out = c;
+  return NBLDPC_OK;
+}
+
+void nbldpc_destroy(nbldpc_code_t c) {
+  if (!c) return;
+  free_workspace(c->ws);
+  cudaFree(c->edges_d);
+  cudaFree(c->gf_exp_d);
+  cudaFree(c->gf_log_d);
+  delete c;
+}
+
+nbldpc_status_t nbldpc_code_info(nbldpc_code_t c, int* m, int* M, int* N, int* E, int* k_max) {
+  if (!c) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (m) *m = c->m;
+  if (M) *M = c->M;
+  if (N) *N = c->N;
+  if (E) *E = 2 * c->N;
+  if (k_max) *k_max = c->k_max;
+  return NBLDPC_OK;
+}
+
+size_t nbldpc_slot_bytes(nbldpc_code_t c) { return c ? slot_bytes_of(c) : 0; }
+
+nbldpc_status_t nbldpc_last_decode_launches(nbldpc_code_t c, long long* launches) {
+  if (!c || !launches) return NBLDPC_ERR_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lk(c->mu);
+  Workspace& w = c->ws;
+  if (!w.base) {
+    *launches = 0;
+    return NBLDPC_OK;
+  }
+  if (!w.last_graph) {
+    *launches = w.last_host_launches;
+    return NBLDPC_OK;
+  }
+  NB_TRY(cudaStreamSynchronize(w.last_stream));
+  int32_t it = 0;
+  NB_TRY(cudaMemcpy(&it, w.dev.glob + 2, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  *launches = 1 + (long long)it * (kPassesPerGraphIter + 1);
+  return NBLDPC_OK;
+}
+
+nbldpc_status_t nbldpc_decode_ex(nbldpc_code_t c, const float* llr, int frames, int max_iters, uint8_t* hard,
+                                 uint8_t* ok, int32_t* iters, void* stream, const nbldpc_decode_opts_t* opts) {
+  if (!c || frames < 1 || max_iters < 1) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (!is_device_ptr(llr) || !is_device_ptr(hard) || !is_device_ptr(ok) || !is_device_ptr(iters))
+    return NBLDPC_ERR_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lk(c->mu);
+  return decode_impl(c, llr, frames, max_iters, hard, ok, iters, static_cast<cudaStream_t>(stream), opts);
+}
+
+nbldpc_status_t nbldpc_decode(nbldpc_code_t c, const float* llr, int frames, int max_iters, uint8_t* hard,
+                              uint8_t* ok, int32_t* iters, void* stream) {
+  return nbldpc_decode_ex(c, llr, frames, max_iters, hard, ok, iters, stream, nullptr);
+}
+
+nbldpc_status_t nbldpc_decode_host(nbldpc_code_t c, const float* llr_host, int frames, int max_iters,
+                                   uint8_t* hard_host, uint8_t* ok_host, int32_t* iters_host, void* stream,
+                                   const nbldpc_decode_opts_t* opts) {
+  if (!c || frames < 1 || max_iters < 1 || !llr_host || !hard_host || !ok_host || !iters_host)
+    return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (is_device_ptr(llr_host) || is_device_ptr(hard_host)) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (opts && opts->struct_size < sizeof(nbldpc_decode_opts_t)) return NBLDPC_ERR_INVALID_ARGUMENT;
+  std::lock_guard<std::mutex> lk(c->mu);
+  NB_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Workspace& w = c->ws;
+  const size_t llr_bytes = (size_t)frames * c->N * c->m * sizeof(float);
+  const size_t out_bytes = align_up((size_t)frames * c->N, 256) + align_up(frames, 256) + (size_t)frames * 4;
+  if (w.llr_stage_bytes < llr_bytes) {
+    cudaStreamSynchronize(st);
+    cudaFree(w.llr_stage);
+    w.llr_stage = nullptr;
+    w.llr_stage_bytes = 0;
+    NB_TRY(cudaMalloc(&w.llr_stage, llr_bytes));
+    w.llr_stage_bytes = llr_bytes;
+  }
+  if (w.out_stage_bytes < out_bytes) {
+    cudaStreamSynchronize(st);
+    cudaFree(w.out_stage);
+    w.out_stage = nullptr;
+    w.out_stage_bytes = 0;
+    NB_TRY(cudaMalloc(&w.out_stage, out_bytes));
+    w.out_stage_bytes = out_bytes;
+  }
+  uint8_t* hard_d = w.out_stage;
+  uint8_t* ok_d = hard_d + align_up((size_t)frames * c->N, 256);
+  int32_t* it_d = reinterpret_cast<int32_t*>(ok_d + align_up(frames, 256));
+  nbldpc_decode_opts_t o{};
+  o.struct_size = sizeof(o);
+  if (opts) {
+    o = *opts;
+    o.struct_size = sizeof(o);
+    o.soft_out = nullptr;
+    o.events_out = nullptr;
+  }
+  NB_TRY(cudaMemcpyAsync(w.llr_stage, llr_host, llr_bytes, cudaMemcpyHostToDevice, st));
+  nbldpc_status_t rs = decode_impl(c, w.llr_stage, frames, max_iters, hard_d, ok_d, it_d, st, &o);
+  if (rs != NBLDPC_OK) return rs;
+  NB_TRY(cudaMemcpyAsync(hard_host, hard_d, (size_t)frames * c->N, cudaMemcpyDeviceToHost, st));
+  NB_TRY(cudaMemcpyAsync(ok_host, ok_d, frames, cudaMemcpyDeviceToHost, st));
+  NB_TRY(cudaMemcpyAsync(iters_host, it_d, (size_t)frames * 4, cudaMemcpyDeviceToHost, st));
+  NB_TRY(cudaStreamSynchronize(st));
+  return NBLDPC_OK;
+}
+
+nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int iter, const float* w_in, float* w_out,
+                            float* u_out, uint8_t* hard, float* soft, void* stream) {
+  if (!c || frames < 1 || iter < 0 || !is_device_ptr(llr) || !is_device_ptr(w_out)) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (iter >= 1 && (!is_device_ptr(w_in) || !is_device_ptr(hard))) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if ((u_out && !is_device_ptr(u_out)) || (soft && !is_device_ptr(soft))) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (!c->row_regular) return NBLDPC_ERR_UNSUPPORTED;  // internal edge slots == canonical order only then
+  std::lock_guard<std::mutex> lk(c->mu);
+  NB_TRY(cudaSetDevice(c->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  nbldpc_status_t rs = ensure_workspace(c, frames);
+  if (rs != NBLDPC_OK) return rs;
+  Workspace& w = c->ws;
+  const size_t msg = (size_t)frames * c->E * c->q * sizeof(float);
+  CallDev call{};
+  call.llr = llr;
+  call.frames = frames;
+  call.max_iters = 1 << 30;
+  call.mode = 0;
+  call.early_stop = 1;
+  call.want_soft = soft != nullptr;
+  nb::nb_step_setup_kernel<<<(frames + 255) / 256, 256, 0, st>>>(w.dev, call, iter);
+  NB_TRY(cudaGetLastError());
+  if (iter >= 1) {
+    nb::nb_tanh_kernel<<<256, 256, 0, st>>>(llr, w.dev.Tt, (size_t)frames * c->N * c->m);
+    NB_TRY(cudaGetLastError());
+    float* wcur = w.dev.W + (size_t)(iter & 1) * frames * c->E * c->q;
+    NB_TRY(cudaMemcpyAsync(wcur, w_in, msg, cudaMemcpyDeviceToDevice, st));
+  }
+  PassParams P = make_params(c, 1, u_out);
+  NB_TRY(launch_pass(c, P, st));
+  float* wnxt = w.dev.W + (size_t)((iter + 1) & 1) * frames * c->E * c->q;
+  NB_TRY(cudaMemcpyAsync(w_out, wnxt, msg, cudaMemcpyDeviceToDevice, st));
+  if (iter >= 1) {
+    NB_TRY(cudaMemcpyAsync(hard, w.dev.xhat, (size_t)frames * c->N, cudaMemcpyDeviceToDevice, st));
+    if (soft)
+      NB_TRY(cudaMemcpyAsync(soft, w.dev.soft, (size_t)frames * c->N * c->m * sizeof(float), cudaMemcpyDeviceToDevice,
+                             st));
+  }
+  return NBLDPC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,87 @@
+"""Shared helpers for the GPU parity tests (tests/ only; imports the oracle).
+
+Message formats:
+  GPU  : packed float32, magnitude = -log2|x| (>= 0, 200 = zero), IEEE sign bit = sign
+  oracle: (sign uint8, ln|x| float64 with floor -745)
+"""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+import synth
+
+LN2 = np.log(2.0)
+ZERO_LN = -87.0  # entries at or below e^-87 are "zero" for comparisons (reading R7)
+
+
+def oracle_code(name_or_cfg, M=None, rows=None, cols=None, coeffs=None):
+    if isinstance(name_or_cfg, str):
+        c = synth.CONFIGS[name_or_cfg]
+        M, rows, cols, coeffs = synth.config_code(name_or_cfg)
+    else:
+        c = name_or_cfg
+    return oracle.Code(oracle.Field(c["m"], c["poly"]), M, c["N"], rows, cols, coeffs)
+
+
+def config_inputs(name, frame0, nframes, point=0, ebn0=None):
+    """(code tuple, llr float32 [F, N*m], sent symbols [F, N]) for a BASELINE config."""
+    c = synth.CONFIGS[name]
+    M, rows, cols, coeffs = synth.config_code(name)
+    if c["codeword"] == "random":
+        ocode = oracle_code(name)
+        xs = np.stack([ocode.encode(synth.random_symbols(c["N"], c["q"], c["seed_codeword"], f))[0]
+                       for f in range(frame0, frame0 + nframes)])
+        bits = synth.symbols_to_bits(xs, c["m"])
+    else:
+        xs = np.zeros((nframes, c["N"]), np.int32)
+        bits = None
+    llr = synth.config_llr(name, frame0, nframes, ebn0_db=ebn0, bits=bits, point=point)
+    return (M, rows, cols, coeffs), llr, xs
+
+
+def packed_to_oracle(p):
+    """GPU packed float32 -> (sign uint8, ln float64) with the oracle's floor."""
+    p = np.asarray(p, np.float32)
+    mag = np.abs(p).astype(np.float64)
+    s = (np.signbit(p)).astype(np.uint8)
+    l = -mag * LN2
+    zero = mag >= 200.0
+    l[zero] = oracle.FLOOR
+    s[zero] = 0
+    return s, l
+
+
+def oracle_to_packed(s, l):
+    mag = np.minimum(-np.asarray(l, np.float64) / LN2, 200.0)
+    mag = np.maximum(mag, 0.0).astype(np.float32)
+    out = mag.copy()
+    neg = (np.asarray(s) == 1) & (mag < 200.0)
+    out[neg] = -mag[neg]
+    out[neg & (mag == 0)] = np.float32(-0.0)
+    return out
+
+
+def message_mismatch(gs, gl, os_, ol, ln_tol=1e-3, lin_tol=1e-4):
+    """Boolean mask of entries that fail the combined tolerance:
+    pass if |d ln| <= ln_tol, or |d linear| <= lin_tol; a sign mismatch passes only where the
+    oracle's |linear| <= lin_tol; entries that are zero on both sides pass."""
+    gl = np.where(gl <= ZERO_LN, -np.inf, gl)
+    ol = np.where(ol <= ZERO_LN, -np.inf, ol)
+    glin = np.where(gs == 1, -1.0, 1.0) * np.exp(gl)
+    olin = np.where(os_ == 1, -1.0, 1.0) * np.exp(ol)
+    with np.errstate(invalid="ignore"):
+        dln = np.abs(gl - ol)
+    dln = np.where(np.isinf(gl) & np.isinf(ol), 0.0, dln)
+    dlin = np.abs(glin - olin)
+    ok_val = (dln <= ln_tol) | (dlin <= lin_tol)
+    sign_ok = (gs == os_) | (np.abs(olin) <= lin_tol) | (np.isinf(gl) & np.isinf(ol))
+    return ~(ok_val & sign_ok)
+
+
+def stable_frames(ocode, llr, max_iters, mode=0):
+    """Oracle f64 results plus the stable-frame mask (f64 and f32 twins agree; reading R20)."""
+    a = ocode.lf_decode_batch(llr, max_iters, mode=mode)
+    b = ocode.lf_decode_batch(llr, max_iters, mode=mode, f32=True)
+    stable = (a["hard"] == b["hard"]).all(1) & (a["ok"] == b["ok"]) & (a["iters"] == b["iters"])
+    return a, stable

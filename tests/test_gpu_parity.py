@@ -1,0 +1,244 @@
+"""GPU parity: the sm_100a decoder (through the C-ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star):
+  * hard decisions, syndrome flags and iteration counts bit-exact with the fp64
+    oracle on every stable frame (a frame whose fp64 and fp32 oracle trajectories
+    agree; unstable frames are counted and must be rare);
+  * per-step message / posterior log-magnitudes within 1e-3 (ln) or 1e-4 linear.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle
+import synth
+from parity import (config_inputs, message_mismatch, oracle_code, oracle_to_packed, packed_to_oracle)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch.device("cuda:0")
+
+
+_codes = {}
+
+
+def gpu_code(name):
+    import paper_1008_4370_b200 as nb
+
+    if name not in _codes:
+        c = synth.CONFIGS[name]
+        M, rows, cols, coeffs = synth.config_code(name)
+        _codes[name] = nb.Code(c["m"], c["poly"], M, c["N"], rows, cols, coeffs)
+    return _codes[name]
+
+
+def compare_decode(name, gpu_out, llr_np, idx, max_iters, mode=0):
+    """Oracle on frames idx; bit-exact on stable frames.  Returns (n_checked, n_unstable)."""
+    ocode = oracle_code(name)
+    sub = llr_np[idx]
+    ref = ocode.lf_decode_batch(sub, max_iters, mode=mode)
+    hard = gpu_out["hard"].cpu().numpy()[idx]
+    ok = gpu_out["ok"].cpu().numpy()[idx]
+    it = gpu_out["iters"].cpu().numpy()[idx]
+    same = (hard == ref["hard"]).all(1) & (ok == ref["ok"]) & (it == ref["iters"])
+    unstable = 0
+    if not same.all():
+        bad = np.where(~same)[0]
+        twin = ocode.lf_decode_batch(sub[bad], max_iters, mode=mode, f32=True)
+        for n, b in enumerate(bad):
+            oracle_stable = (np.array_equal(twin["hard"][n], ref["hard"][b]) and twin["ok"][n] == ref["ok"][b]
+                             and twin["iters"][n] == ref["iters"][b])
+            assert not oracle_stable, (
+                f"{name}: stable frame {idx[b]} differs: gpu iters {it[b]} ok {ok[b]} vs oracle "
+                f"{ref['iters'][b]} {ref['ok'][b]}, {int((hard[b] != ref['hard'][b]).sum())} symbols")
+            unstable += 1
+    return len(idx), unstable
+
+
+DECODE_CASES = [
+    # name, point, gpu frames, oracle sample size
+    ("C1", 0, 64, 64),
+    ("C2", 0, 4096, 24),
+    ("C3", 0, 512, 8),
+    ("C4", 0, 64, 3),
+    ("C5", 0, 256, 8),   # 3.0 dB: every frame runs all 50 iterations
+    ("C5", 3, 256, 16),  # 4.5 dB
+    ("C5", 4, 256, 16),  # 5.0 dB
+]
+
+
+@pytest.mark.parametrize("name,point,F,nsample", DECODE_CASES)
+def test_decode_parity(dev, name, point, F, nsample):
+    c = synth.CONFIGS[name]
+    _, llr, xs = config_inputs(name, 0, F, point=point)
+    code = gpu_code(name)
+    out = code.decode(torch.from_numpy(llr).to(dev), c["max_iters"])
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(1)
+    idx = np.arange(F) if nsample >= F else np.sort(rng.choice(F, nsample, replace=False))
+    n, unstable = compare_decode(name, out, llr, idx, c["max_iters"])
+    assert unstable <= max(1, n // 10)
+    # every GPU frame: iterations within [1, max], ok consistent with the exact syndrome
+    it = out["iters"].cpu().numpy()
+    assert it.min() >= 1 and it.max() <= c["max_iters"]
+    ocode = oracle_code(name)
+    hard = out["hard"].cpu().numpy()
+    okg = out["ok"].cpu().numpy()
+    for f in rng.choice(F, min(F, 64), replace=False):
+        assert bool(okg[f]) == ocode.syndrome(hard[f])[0]
+
+
+@pytest.mark.parametrize("name", ["C1", "C5"])
+def test_paper_syndrome_mode_parity(dev, name):
+    c = synth.CONFIGS[name]
+    point = 4 if name == "C5" else 0
+    _, llr, _ = config_inputs(name, 0, 64, point=point)
+    out = gpu_code(name).decode(torch.from_numpy(llr).to(dev), c["max_iters"], syndrome_mode=1)
+    torch.cuda.synchronize()
+    idx = np.arange(64) if name == "C1" else np.arange(0, 64, 4)
+    n, unstable = compare_decode(name, out, llr, idx, c["max_iters"], mode=1)
+    assert unstable <= max(1, n // 10)
+
+
+def _oracle_state(ocode, llr_row, iters):
+    """Oracle trajectory up to W^(iters) (f64) for one frame."""
+    S0, L0 = ocode.lf_init(llr_row.astype(np.float64))
+    ecol = ocode.edges()[1]
+    Us, Ul = S0[ecol].copy(), L0[ecol].copy()
+    for _ in range(iters):
+        Ws, Wl = ocode.lf_check_to_variable(Us, Ul)
+        Us, Ul, _ = ocode.lf_variable_to_check(S0, L0, Ws, Wl)
+    return S0, L0, Ws, Wl
+
+
+@pytest.mark.parametrize("name,point", [("C1", 0), ("C5", 3), ("C2", 0), ("C3", 0)])
+@pytest.mark.parametrize("ell", [1, 2, 3])
+def test_step_parity(dev, name, point, ell):
+    c = synth.CONFIGS[name]
+    F = 2
+    _, llr, _ = config_inputs(name, 0, F, point=point)
+    ocode = oracle_code(name)
+    code = gpu_code(name)
+    w_in = []
+    refs = []
+    for f in range(F):
+        S0, L0, Ws, Wl = _oracle_state(ocode, llr[f], ell)
+        packed = oracle_to_packed(Ws, Wl)
+        w_in.append(packed)
+        # the oracle continues from the same f32-rounded state
+        Ws32, Wl32 = packed_to_oracle(packed)
+        Us, Ul, _ = ocode.lf_variable_to_check(S0, L0, Ws32, Wl32)
+        x, soft, _ = ocode.lf_decision(S0, L0, Ws32, Wl32)
+        Wn_s, Wn_l = ocode.lf_check_to_variable(Us, Ul)
+        refs.append((Us, Ul, x, soft, Wn_s, Wn_l))
+    w_in = torch.from_numpy(np.stack(w_in)).to(dev)
+    res = code.step(torch.from_numpy(llr).to(dev), ell, w_in, want_u=True, want_soft=True)
+    torch.cuda.synchronize()
+    for f in range(F):
+        Us, Ul, x, soft, Wn_s, Wn_l = refs[f]
+        gs, gl = packed_to_oracle(res["u"][f].cpu().numpy())
+        bad_u = message_mismatch(gs, gl, Us, Ul)
+        assert bad_u.sum() == 0, f"U: {bad_u.sum()} of {bad_u.size} entries off"
+        gs, gl = packed_to_oracle(res["w"][f].cpu().numpy())
+        bad_w = message_mismatch(gs, gl, Wn_s, Wn_l, ln_tol=2e-3 * (c["k"] - 1), lin_tol=1e-4)
+        assert bad_w.sum() == 0, f"W: {bad_w.sum()} of {bad_w.size} entries off"
+        gsoft = res["soft"][f].cpu().numpy().reshape(c["N"], c["m"])
+        big = soft > -5.0  # posterior bit log-magnitudes (ln|q_i(0)-q_i(1)|) away from ties
+        assert np.abs(gsoft[big] - soft[big]).max(initial=0) <= 1e-3
+        hard = res["hard"][f].cpu().numpy()
+        sure = (soft > -12.0).all(1)
+        assert np.array_equal(hard[sure], x[sure])
+
+
+def test_invariance_slots_graph_batch(dev):
+    name = "C2"
+    c = synth.CONFIGS[name]
+    _, llr, _ = config_inputs(name, 0, 160)
+    code = gpu_code(name)
+    x = torch.from_numpy(llr).to(dev)
+    base = code.decode(x, c["max_iters"])
+    variants = [dict(slots=1), dict(slots=7), dict(slots=160), dict(use_graph=-1, slots=13)]
+    for kw in variants:
+        o = code.decode(x, c["max_iters"], **kw)
+        torch.cuda.synchronize()
+        for k in ("hard", "ok", "iters"):
+            assert torch.equal(o[k], base[k]), (kw, k)
+    sub = torch.arange(17, 160, 9)
+    o = code.decode(x[sub].contiguous(), c["max_iters"])
+    for k in ("hard", "ok", "iters"):
+        assert torch.equal(o[k], base[k][sub.to(dev)]), k
+    again = code.decode(x, c["max_iters"])
+    for k in ("hard", "ok", "iters"):
+        assert torch.equal(again[k], base[k])
+
+
+def test_decode_host_matches_device(dev):
+    name = "C5"
+    c = synth.CONFIGS[name]
+    _, llr, _ = config_inputs(name, 0, 96, point=4)
+    code = gpu_code(name)
+    d = code.decode(torch.from_numpy(llr).to(dev), c["max_iters"])
+    h = code.decode_host(torch.from_numpy(llr).pin_memory(), c["max_iters"])
+    for k in ("hard", "ok", "iters"):
+        assert torch.equal(d[k].cpu(), h[k])
+
+
+def test_soft_and_events_outputs(dev):
+    name = "C1"
+    c = synth.CONFIGS[name]
+    _, llr, _ = config_inputs(name, 0, 64)
+    code = gpu_code(name)
+    out = code.decode(torch.from_numpy(llr).to(dev), 1, early_stop=False, want_soft=True, want_events=True)
+    ref = oracle_code(name).lf_decode_batch(llr, 1, early_stop=False, want_soft=True)
+    soft = out["soft"].cpu().numpy()
+    big = ref["soft"] > -5.0
+    assert np.abs(soft[big] - ref["soft"][big]).max() <= 1e-3
+    assert int(out["events"].sum()) == 0
+    assert (out["iters"].cpu().numpy() == 1).all()
+
+
+def test_binary_code_and_small_fields(dev):
+    import paper_1008_4370_b200 as nb
+
+    for m, poly, N, k in [(1, 0x3, 48, 4), (3, 0xB, 24, 6), (5, 0x25, 40, 4), (7, 0x89, 16, 4)]:
+        M, rows, cols, coeffs = synth.make_regular_code(N, k, m, 50 + m)
+        code = nb.Code(m, poly, M, N, rows, cols, coeffs)
+        ocode = oracle.Code(oracle.Field(m, poly), M, N, rows, cols, coeffs)
+        llr = synth.awgn_llr(N * m, 0, 48, synth.sigma2_for(2.0, 1 - 2 / k), 77 + m)
+        out = code.decode(torch.from_numpy(llr).to(dev), 20)
+        ref = ocode.lf_decode_batch(llr, 20)
+        same = ((out["hard"].cpu().numpy() == ref["hard"]).all(1) & (out["ok"].cpu().numpy() == ref["ok"])
+                & (out["iters"].cpu().numpy() == ref["iters"]))
+        assert same.mean() >= 0.95, (m, same.mean())
+
+
+def test_edge_cases_and_errors(dev):
+    import paper_1008_4370_b200 as nb
+
+    name = "C1"
+    c = synth.CONFIGS[name]
+    code = gpu_code(name)
+    _, llr, _ = config_inputs(name, 0, 1)
+    x = torch.from_numpy(llr).to(dev)
+    o = code.decode(x, 1)
+    ref = oracle_code(name).lf_decode_batch(llr, 1)
+    assert o["iters"].item() == 1 and np.array_equal(o["hard"].cpu().numpy(), ref["hard"])
+    with pytest.raises(nb.NbldpcError):
+        code.decode(x, 0)
+    M, rows, cols, coeffs = synth.config_code(name)
+    with pytest.raises(nb.NbldpcError) as ei:
+        nb.Code(2, 0x5, M, c["N"], rows, cols, coeffs)  # x^2+1 not primitive
+    assert ei.value.status == -2
+    with pytest.raises(nb.NbldpcError) as ei:
+        nb.Code(2, 0x7, M, c["N"], rows[:-1], cols[:-1], coeffs[:-1])  # a column of weight 1
+    assert ei.value.status == -3
+    bad = coeffs.copy()
+    bad[0] = 4
+    with pytest.raises(nb.NbldpcError) as ei:
+        nb.Code(2, 0x7, M, c["N"], rows, cols, bad)
+    assert ei.value.status == -1
