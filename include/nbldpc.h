@@ -48,6 +48,16 @@ typedef enum {
   NBLDPC_SYNDROME_PAPER = 1  /* the paper's fast Fourier-domain syndrome */
 } nbldpc_syndrome_mode_t;
 
+/* How the variable node evaluates the signed log-convolution U = Lambda^0 [+] W.
+ * Both compute the same result up to rounding. */
+typedef enum {
+  NBLDPC_VN_SEPARABLE = 0, /* default: the binary-image channel spectrum is the tensor product
+                              P^0 = (x)_i (1, tanh(L_i/2)), so the XOR-
+                              convolution factors into m butterfly stages x(z) += t_i x(z ^ alpha^i):
+                              m 2^m FMAs per edge */
+  NBLDPC_VN_DIRECT = 1     /* the paper's CONV (Table 1): 2^{2m} FMAs per edge */
+} nbldpc_vn_algorithm_t;
+
 /* Options of nbldpc_decode_ex / nbldpc_decode_host.  Zero-initialise, then set
  * struct_size = sizeof(nbldpc_decode_opts_t).  NULL opts = all defaults. */
 typedef struct {
@@ -61,6 +71,7 @@ typedef struct {
   int slots;         /* frames resident on the device at once (0 = library default, sized to L2) */
   int use_graph;     /* 0 = default (CUDA graph with a device-side WHILE loop), 1 = force graph,
                         -1 = host-driven launch loop */
+  int vn_algorithm;  /* nbldpc_vn_algorithm_t, default NBLDPC_VN_SEPARABLE */
 } nbldpc_decode_opts_t;
 
 /* Builds a code from H given as nnz (row, col, coefficient) triplets in any order.
@@ -136,9 +147,10 @@ nbldpc_status_t nbldpc_decode_host(nbldpc_code_t code, const float* llr_host, in
  *   iter >= 1 : given W^(iter) in w_in, computes U^(iter) = VARIABLE-TO-CHECK (u_out, optional),
  *               the tentative decision (hard [frames][N], soft [frames][N*m] optional) and
  *               W^(iter+1) = CHECK-TO-VARIABLE(U^(iter)) in w_out.
- * All pointers are DEVICE pointers; llr as for nbldpc_decode.  Stream-ordered. */
+ * vn_algorithm: nbldpc_vn_algorithm_t.  All pointers are DEVICE pointers; llr as for
+ * nbldpc_decode.  Stream-ordered. */
 nbldpc_status_t nbldpc_step(nbldpc_code_t code, const float* llr, int frames, int iter, const float* w_in,
-                            float* w_out, float* u_out, uint8_t* hard, float* soft, void* stream);
+                            float* w_out, float* u_out, uint8_t* hard, float* soft, int vn_algorithm, void* stream);
 
 #ifdef __cplusplus
 }

@@ -38,7 +38,7 @@ class NbldpcError(RuntimeError):
 class _Opts(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_size_t), ("syndrome_mode", ctypes.c_int), ("no_early_stop", ctypes.c_int),
                 ("soft_out", ctypes.c_void_p), ("events_out", ctypes.c_void_p), ("slots", ctypes.c_int),
-                ("use_graph", ctypes.c_int)]
+                ("use_graph", ctypes.c_int), ("vn_algorithm", ctypes.c_int)]
 
 
 def header_symbols() -> list[str]:
@@ -70,7 +70,7 @@ def lib():
         "nbldpc_decode": (i32, [vp, vp, i32, i32, vp, vp, vp, vp]),
         "nbldpc_decode_ex": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, ctypes.POINTER(_Opts)]),
         "nbldpc_decode_host": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, ctypes.POINTER(_Opts)]),
-        "nbldpc_step": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp]),
+        "nbldpc_step": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -141,7 +141,7 @@ class Code:
     def slot_bytes(self) -> int:
         return int(self._L.nbldpc_slot_bytes(self._h))
 
-    def _opts(self, syndrome_mode=0, early_stop=True, soft=None, events=None, slots=0, use_graph=0):
+    def _opts(self, syndrome_mode=0, early_stop=True, soft=None, events=None, slots=0, use_graph=0, vn_algorithm=0):
         o = _Opts()
         o.struct_size = ctypes.sizeof(_Opts)
         o.syndrome_mode = int(syndrome_mode)
@@ -150,10 +150,11 @@ class Code:
         o.events_out = _ptr(events)
         o.slots = int(slots)
         o.use_graph = int(use_graph)
+        o.vn_algorithm = int(vn_algorithm)
         return o
 
     def decode(self, llr, max_iters: int, *, syndrome_mode: int = 0, early_stop: bool = True, want_soft=False,
-               want_events=False, slots: int = 0, use_graph: int = 0, out=None, stream=None):
+               want_events=False, slots: int = 0, use_graph: int = 0, vn_algorithm: int = 0, out=None, stream=None):
         """Decode frames. ``llr``: CUDA float32 tensor [F, N*m].  Returns a dict of CUDA tensors
         (hard uint8 [F,N], ok uint8 [F], iters int32 [F], optional soft float32 [F,N*m], events int32 [F])."""
         import torch
@@ -172,7 +173,7 @@ class Code:
                 out["soft"] = torch.empty((F, self.N * self.m), dtype=torch.float32, device=dev)
             if want_events:
                 out["events"] = torch.empty(F, dtype=torch.int32, device=dev)
-        o = self._opts(syndrome_mode, early_stop, out.get("soft"), out.get("events"), slots, use_graph)
+        o = self._opts(syndrome_mode, early_stop, out.get("soft"), out.get("events"), slots, use_graph, vn_algorithm)
         st = self._L.nbldpc_decode_ex(self._h, llr.data_ptr(), F, int(max_iters), out["hard"].data_ptr(),
                                       out["ok"].data_ptr(), out["iters"].data_ptr(), _stream(stream),
                                       ctypes.byref(o))
@@ -180,7 +181,7 @@ class Code:
         return out
 
     def decode_host(self, llr_host, max_iters: int, *, syndrome_mode: int = 0, slots: int = 0, use_graph: int = 0,
-                    out=None, stream=None):
+                    vn_algorithm: int = 0, out=None, stream=None):
         """End-to-end decode from HOST memory (pinned torch tensor or numpy array) to host outputs."""
         import torch
 
@@ -194,14 +195,14 @@ class Code:
             out = {"hard": torch.empty((F, self.N), dtype=torch.uint8, pin_memory=pin),
                    "ok": torch.empty(F, dtype=torch.uint8, pin_memory=pin),
                    "iters": torch.empty(F, dtype=torch.int32, pin_memory=pin)}
-        o = self._opts(syndrome_mode, True, None, None, slots, use_graph)
+        o = self._opts(syndrome_mode, True, None, None, slots, use_graph, vn_algorithm)
         st = self._L.nbldpc_decode_host(self._h, llr_host.data_ptr(), F, int(max_iters), out["hard"].data_ptr(),
                                         out["ok"].data_ptr(), out["iters"].data_ptr(), _stream(stream),
                                         ctypes.byref(o))
         _check(st, "nbldpc_decode_host")
         return out
 
-    def step(self, llr, iter_: int, w_in=None, want_u=False, want_soft=False, stream=None):
+    def step(self, llr, iter_: int, w_in=None, want_u=False, want_soft=False, vn_algorithm: int = 0, stream=None):
         """One Log-Fourier iteration from state W^(iter) (parity tests).  Tensors in the packed
         -log2|x| + sign-bit format, [F, E, q]."""
         import torch
@@ -213,6 +214,6 @@ class Code:
         hard = torch.empty((F, self.N), dtype=torch.uint8, device=dev)
         soft = torch.empty((F, self.N * self.m), dtype=torch.float32, device=dev) if want_soft else None
         st = self._L.nbldpc_step(self._h, llr.data_ptr(), F, int(iter_), _ptr(w_in), w_out.data_ptr(), _ptr(u_out),
-                                 hard.data_ptr(), _ptr(soft), _stream(stream))
+                                 hard.data_ptr(), _ptr(soft), int(vn_algorithm), _stream(stream))
         _check(st, "nbldpc_step")
         return {"w": w_out, "u": u_out, "hard": hard, "soft": soft}

@@ -172,6 +172,41 @@ __device__ __forceinline__ void conv_block(const float (&a)[R], const float (&b)
   }
 }
 
+// One stage of the separable XOR-convolution with P^0 = (x)_i (1, t_i):
+// x(z) <- x(z) + t_i x(z ^ e_i) on the bit i of the thread's register index (i < LR), as
+// FFMA2 with the broadcast t_i and a natural or swapped pair.
+template <int R, int I>
+__device__ __forceinline__ void bfly_reg(float (&x)[R], float ti) {
+  constexpr int S = 1 << I;
+  if constexpr (I == 0) {
+#pragma unroll
+    for (int p = 0; p < R / 2; ++p) {
+      const float2 v = make_float2(x[2 * p], x[2 * p + 1]);
+      const float2 r = __ffma2_rn(make_float2(ti, ti), make_float2(v.y, v.x), v);
+      x[2 * p] = r.x;
+      x[2 * p + 1] = r.y;
+    }
+  } else {
+    float y[R];
+#pragma unroll
+    for (int p = 0; p < R / 2; ++p) {
+      const int lo = 2 * p, pa = lo ^ S;
+      const float2 r = __ffma2_rn(make_float2(ti, ti), make_float2(x[pa], x[pa + 1]), make_float2(x[lo], x[lo + 1]));
+      y[lo] = r.x;
+      y[lo + 1] = r.y;
+    }
+#pragma unroll
+    for (int z = 0; z < R; ++z) x[z] = y[z];
+  }
+}
+template <int R, int I, int LR>
+__device__ __forceinline__ void bfly_regs(float (&x)[R], const float* th) {
+  if constexpr (I < LR) {
+    bfly_reg<R, I>(x, th[I]);
+    bfly_regs<R, I + 1, LR>(x, th);
+  }
+}
+
 // barrier over the threads of one check: the warp when a check fits in it, else a named barrier
 __device__ __forceinline__ void check_sync(int lc, int tpc) {
   if (tpc <= 32) {
@@ -187,7 +222,7 @@ __device__ __forceinline__ int atom_add_release_gpu(int* p, int v) {
 }
 __device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
-template <int MB, int MAXB>
+template <int MB, int MAXB, bool DIRECT>
 __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(PassParams P) {
   using C = Cfg<MB>;
   constexpr int Q = C::Q, R = C::R, TT = C::TT, LR = C::LR, NB = C::TT;
@@ -349,12 +384,45 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
           D[y] = dreg[y];  // linear copy for the paper-mode points
         }
       }
-      float2 acc[R / 2];
+      if constexpr (DIRECT) {
+        float2 acc[R / 2];
 #pragma unroll
-      for (int p = 0; p < R / 2; ++p) acc[p] = make_float2(0.0f, 0.0f);
-      conv_block<R>(p0, b, acc);
+        for (int p = 0; p < R / 2; ++p) acc[p] = make_float2(0.0f, 0.0f);
+        conv_block<R>(p0, b, acc);
 #pragma unroll
-      for (int p = 0; p < R / 2; ++p) { raw[2 * p] = acc[p].x; raw[2 * p + 1] = acc[p].y; }
+        for (int p = 0; p < R / 2; ++p) { raw[2 * p] = acc[p].x; raw[2 * p + 1] = acc[p].y; }
+      } else {
+        bfly_regs<R, 0, LR>(b, th);  // raw = P^0 (*) W_e' through the m separable stages
+#pragma unroll
+        for (int zl = 0; zl < R; ++zl) raw[zl] = b[zl];
+      }
+    } else if constexpr (!DIRECT) {
+      // separable path: own block of W_e' to linear; the m - LR high stages pair threads of
+      // the team (lane ^ 2^(i-LR)), the LR low stages stay in registers
+      float b[R];
+#pragma unroll
+      for (int c4 = 0; c4 < R / 4; ++c4) {
+        float4 v = *reinterpret_cast<const float4*>(B + cm_idx<MB>(t * R + 4 * c4));
+        b[4 * c4] = to_lin(v.x); b[4 * c4 + 1] = to_lin(v.y); b[4 * c4 + 2] = to_lin(v.z); b[4 * c4 + 3] = to_lin(v.w);
+      }
+      if (is_a) {
+#pragma unroll
+        for (int c4 = 0; c4 < R / 4; ++c4) {
+          float4* pd = reinterpret_cast<float4*>(D + cm_idx<MB>(t * R + 4 * c4));
+          float4 v = *pd;
+          *pd = make_float4(to_lin(v.x), to_lin(v.y), to_lin(v.z), to_lin(v.w));
+        }
+      }
+      bfly_regs<R, 0, LR>(b, th);
+#pragma unroll
+      for (int i = LR; i < MB; ++i) {
+        const int off = 1 << (i - LR);
+#pragma unroll
+        for (int zl = 0; zl < R; ++zl) b[zl] = fmaf(th[i], __shfl_xor_sync(0xffffffffu, b[zl], off), b[zl]);
+      }
+#pragma unroll
+      for (int zl = 0; zl < R; ++zl) raw[zl] = b[zl];
+      __syncwarp();  // D conversions visible to the team
     } else {
       if (active) {
         // A <- P^0 (natural layout); B, D converted in place to linear (own chunks)
@@ -419,19 +487,19 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
     }
 
     // ---- TENTATIVE DECISION at the variable's first edge:  M_v(z) = sum_y raw(y) W_e(z ^ y)
-    // (raw is the unnormalised VN output, so M_v is exact up to a positive factor; sums in
-    // fp64 because the alpha^i points cancel strongly)
+    // (raw is the unnormalised VN output, so M_v is exact up to a positive factor; per-thread
+    // partial sums in fp32, the cross-thread reduction in fp64)
     if (do_dec) {
-      double mv[MB + 1];
+      float mf[MB + 1];  // the thread's partial sums (<= 16 terms) in fp32, reduced across the team in fp64
 #pragma unroll
-      for (int b = 0; b <= MB; ++b) mv[b] = 0.0;
+      for (int b = 0; b <= MB; ++b) mf[b] = 0.0f;
       if (is_a) {
         if constexpr (TT == 1) {
 #pragma unroll
           for (int y = 0; y < Q; ++y) {
-            mv[0] = fma((double)raw[y], (double)dreg[y], mv[0]);
+            mf[0] = fmaf(raw[y], dreg[y], mf[0]);
 #pragma unroll
-            for (int b = 0; b < MB; ++b) mv[b + 1] = fma((double)raw[y], (double)dreg[y ^ (1 << b)], mv[b + 1]);
+            for (int b = 0; b < MB; ++b) mf[b + 1] = fmaf(raw[y], dreg[y ^ (1 << b)], mf[b + 1]);
           }
         } else {
           float dv[R];
@@ -442,9 +510,9 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
           }
 #pragma unroll
           for (int zl = 0; zl < R; ++zl) {
-            mv[0] = fma((double)raw[zl], (double)dv[zl], mv[0]);
+            mf[0] = fmaf(raw[zl], dv[zl], mf[0]);
 #pragma unroll
-            for (int b = 0; b < LR; ++b) mv[b + 1] = fma((double)raw[zl], (double)dv[zl ^ (1 << b)], mv[b + 1]);
+            for (int b = 0; b < LR; ++b) mf[b + 1] = fmaf(raw[zl], dv[zl ^ (1 << b)], mf[b + 1]);
           }
 #pragma unroll
           for (int b = LR; b < MB; ++b) {
@@ -452,14 +520,17 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
 #pragma unroll
             for (int c4 = 0; c4 < R / 4; ++c4) {
               float4 v = *reinterpret_cast<const float4*>(D + cm_idx<MB>(bb * R + 4 * c4));
-              mv[b + 1] = fma((double)raw[4 * c4], (double)v.x, mv[b + 1]);
-              mv[b + 1] = fma((double)raw[4 * c4 + 1], (double)v.y, mv[b + 1]);
-              mv[b + 1] = fma((double)raw[4 * c4 + 2], (double)v.z, mv[b + 1]);
-              mv[b + 1] = fma((double)raw[4 * c4 + 3], (double)v.w, mv[b + 1]);
+              mf[b + 1] = fmaf(raw[4 * c4], v.x, mf[b + 1]);
+              mf[b + 1] = fmaf(raw[4 * c4 + 1], v.y, mf[b + 1]);
+              mf[b + 1] = fmaf(raw[4 * c4 + 2], v.z, mf[b + 1]);
+              mf[b + 1] = fmaf(raw[4 * c4 + 3], v.w, mf[b + 1]);
             }
           }
         }
       }
+      double mv[MB + 1];
+#pragma unroll
+      for (int b = 0; b <= MB; ++b) mv[b] = (double)mf[b];
       if constexpr (TT > 1) {
 #pragma unroll
         for (int off = TT / 2; off >= 1; off >>= 1)
@@ -502,14 +573,15 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
 #pragma unroll 1
         for (int i = 0; i < 2 * MB; ++i) {
           const int z = (int)(((i < MB ? pa : pbv) >> (8 * (i < MB ? i : i - MB))) & 0xFF);
-          double acc = 0.0;
+          float accf = 0.0f;
           if (is_a) {
 #pragma unroll
             for (int zl = 0; zl < R; ++zl) {
               const int yy = (t * R + zl) ^ z;
-              acc = fma((double)raw[zl], (double)D[cm_idx<MB>(yy)], acc);
+              accf = fmaf(raw[zl], D[cm_idx<MB>(yy)], accf);
             }
           }
+          double acc = (double)accf;
           if constexpr (TT > 1) {
 #pragma unroll
             for (int off = TT / 2; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);

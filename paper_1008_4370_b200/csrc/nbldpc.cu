@@ -36,6 +36,7 @@ struct Workspace {
   WorkDev dev{};
   int32_t* host_flag = nullptr;  // pinned, host loop
   cudaGraphExec_t graph = nullptr;
+  int graph_direct = 0;           // VN algorithm the graph was built with
   float* llr_stage = nullptr;  // device staging for nbldpc_decode_host
   size_t llr_stage_bytes = 0;
   uint8_t* out_stage = nullptr;
@@ -122,44 +123,52 @@ void free_workspace(Workspace& w) {
   w = Workspace{};
 }
 
-template <int MB, int MAXB>
-void* pass_fn() { return reinterpret_cast<void*>(&nb::nb_pass_kernel<MB, MAXB>); }
+template <int MB, int MAXB, bool DIRECT>
+void* pass_fn() { return reinterpret_cast<void*>(&nb::nb_pass_kernel<MB, MAXB, DIRECT>); }
 
-void* pass_kernel_ptr(int m, int big) {
+template <bool DIRECT>
+void* pass_kernel_ptr_t(int m, int big) {
   switch (m * 2 + (big ? 1 : 0)) {
-    case 2: return pass_fn<1, 256>();
-    case 3: return pass_fn<1, kBigBlock>();
-    case 4: return pass_fn<2, 256>();
-    case 5: return pass_fn<2, kBigBlock>();
-    case 6: return pass_fn<3, 256>();
-    case 7: return pass_fn<3, kBigBlock>();
-    case 8: return pass_fn<4, 256>();
-    case 9: return pass_fn<4, kBigBlock>();
-    case 10: return pass_fn<5, 256>();
-    case 11: return pass_fn<5, kBigBlock>();
-    case 12: return pass_fn<6, 256>();
-    case 13: return pass_fn<6, kBigBlock>();
-    case 14: return pass_fn<7, 256>();
-    case 15: return pass_fn<7, kBigBlock>();
-    case 16: return pass_fn<8, 256>();
-    case 17: return pass_fn<8, kBigBlock>();
+    case 2: return pass_fn<1, 256, DIRECT>();
+    case 3: return pass_fn<1, kBigBlock, DIRECT>();
+    case 4: return pass_fn<2, 256, DIRECT>();
+    case 5: return pass_fn<2, kBigBlock, DIRECT>();
+    case 6: return pass_fn<3, 256, DIRECT>();
+    case 7: return pass_fn<3, kBigBlock, DIRECT>();
+    case 8: return pass_fn<4, 256, DIRECT>();
+    case 9: return pass_fn<4, kBigBlock, DIRECT>();
+    case 10: return pass_fn<5, 256, DIRECT>();
+    case 11: return pass_fn<5, kBigBlock, DIRECT>();
+    case 12: return pass_fn<6, 256, DIRECT>();
+    case 13: return pass_fn<6, kBigBlock, DIRECT>();
+    case 14: return pass_fn<7, 256, DIRECT>();
+    case 15: return pass_fn<7, kBigBlock, DIRECT>();
+    case 16: return pass_fn<8, 256, DIRECT>();
+    case 17: return pass_fn<8, kBigBlock, DIRECT>();
   }
   return nullptr;
+}
+// direct = 1: the paper's q^2-term convolution; 0: separable butterflies
+void* pass_kernel_ptr(int m, int big, int direct) {
+  return direct ? pass_kernel_ptr_t<true>(m, big) : pass_kernel_ptr_t<false>(m, big);
 }
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a property of the kernel (one instantiation per
 // (m, block variant)) shared by every code on the device: only ever raise it.
 std::mutex g_attr_mu;
-size_t g_attr_smem[64][18] = {};
+size_t g_attr_smem[64][36] = {};
 
 cudaError_t ensure_smem_attr(const nbldpc_code_s* c) {
   std::lock_guard<std::mutex> lk(g_attr_mu);
-  const int d = c->device & 63, k = c->m * 2 + c->big;
-  if (g_attr_smem[d][k] >= c->smem) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(pass_kernel_ptr(c->m, c->big), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)c->smem);
-  if (e == cudaSuccess) g_attr_smem[d][k] = c->smem;
-  return e;
+  for (int direct = 0; direct < 2; ++direct) {
+    const int d = c->device & 63, k = (c->m * 2 + c->big) * 2 + direct;
+    if (g_attr_smem[d][k] >= c->smem) continue;
+    cudaError_t e = cudaFuncSetAttribute(pass_kernel_ptr(c->m, c->big, direct),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
+    if (e != cudaSuccess) return e;
+    g_attr_smem[d][k] = c->smem;
+  }
+  return cudaSuccess;
 }
 
 // Slot lanes Y: CTA (g, y) processes slots y, y+Y, ... .  Minimise the makespan
@@ -235,7 +244,7 @@ nbldpc_status_t ensure_workspace(nbldpc_code_s* c, int S) {
   return NBLDPC_OK;
 }
 
-PassParams make_params(const nbldpc_code_s* c, int step_mode, float* u_out) {
+PassParams make_params(const nbldpc_code_s* c, int step_mode, float* u_out) {  // NOLINT
   PassParams P{};
   P.code.m = c->m;
   P.code.M = c->M;
@@ -258,14 +267,18 @@ PassParams make_params(const nbldpc_code_s* c, int step_mode, float* u_out) {
 
 dim3 pass_grid(const nbldpc_code_s* c) { return dim3((unsigned)(c->groups * c->ws.Y)); }
 
-cudaError_t launch_pass(const nbldpc_code_s* c, const PassParams& P, cudaStream_t st) {
+cudaError_t launch_pass(const nbldpc_code_s* c, const PassParams& P, int direct, cudaStream_t st) {
   void* args[] = {const_cast<PassParams*>(&P)};
-  return cudaLaunchKernel(pass_kernel_ptr(c->m, c->big), pass_grid(c), dim3(c->block), args, c->smem, st);
+  return cudaLaunchKernel(pass_kernel_ptr(c->m, c->big, direct), pass_grid(c), dim3(c->block), args, c->smem, st);
 }
 
-nbldpc_status_t build_graph(nbldpc_code_s* c) {
+nbldpc_status_t build_graph(nbldpc_code_s* c, int direct) {
   Workspace& w = c->ws;
-  if (w.graph) return NBLDPC_OK;
+  if (w.graph && w.graph_direct == direct) return NBLDPC_OK;
+  if (w.graph) {
+    cudaGraphExecDestroy(w.graph);
+    w.graph = nullptr;
+  }
   cudaGraph_t g = nullptr;
   NB_TRY(cudaGraphCreate(&g, 0));
   auto fail = [&](cudaError_t e) {
@@ -287,7 +300,7 @@ nbldpc_status_t build_graph(nbldpc_code_s* c) {
   for (int i = 0; i < kPassesPerGraphIter; ++i) {
     cudaGraphNodeParams kp = {};
     kp.type = cudaGraphNodeTypeKernel;
-    kp.kernel.func = pass_kernel_ptr(c->m, c->big);
+    kp.kernel.func = pass_kernel_ptr(c->m, c->big, direct);
     kp.kernel.gridDim = pass_grid(c);
     kp.kernel.blockDim = dim3(c->block);
     kp.kernel.sharedMemBytes = (unsigned)c->smem;
@@ -315,6 +328,7 @@ nbldpc_status_t build_graph(nbldpc_code_s* c) {
     w.graph = nullptr;
     return cuda_status(e);
   }
+  w.graph_direct = direct;
   return NBLDPC_OK;
 }
 
@@ -328,7 +342,7 @@ int default_slots(const nbldpc_code_s* c, int frames) {
 
 nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int max_iters, uint8_t* hard,
                             uint8_t* ok, int32_t* iters, cudaStream_t st, const nbldpc_decode_opts_t* opts) {
-  int mode = 0, early = 1, slots = 0, use_graph = 0;
+  int mode = 0, early = 1, slots = 0, use_graph = 0, direct = 0;
   float* soft = nullptr;
   int32_t* events = nullptr;
   if (opts) {
@@ -339,8 +353,10 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
     events = opts->events_out;
     slots = opts->slots;
     use_graph = opts->use_graph;
+    direct = opts->vn_algorithm;
   }
   if (mode != 0 && mode != 1) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (direct != 0 && direct != 1) return NBLDPC_ERR_INVALID_ARGUMENT;
   if (slots < 0) return NBLDPC_ERR_INVALID_ARGUMENT;
   if ((soft && !is_device_ptr(soft)) || (events && !is_device_ptr(events))) return NBLDPC_ERR_INVALID_ARGUMENT;
   const int S = slots > 0 ? std::min(slots, frames) : default_slots(c, frames);
@@ -366,7 +382,7 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   w.last_graph = use_graph >= 0;
   w.last_host_launches = 1;
   if (use_graph >= 0) {
-    rs = build_graph(c);
+    rs = build_graph(c, direct);
     if (rs != NBLDPC_OK) return rs;
     NB_TRY(cudaGraphLaunch(w.graph, st));
     return NBLDPC_OK;
@@ -375,7 +391,7 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   PassParams P = make_params(c, 0, nullptr);
   for (;;) {
     for (int i = 0; i < kPassesPerGraphIter; ++i) {
-      NB_TRY(launch_pass(c, P, st));
+      NB_TRY(launch_pass(c, P, direct, st));
       w.last_host_launches++;
     }
     NB_TRY(cudaMemcpyAsync(w.host_flag, w.dev.glob + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -555,7 +571,7 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
   c->smem = ((size_t)(c->block / tt) * team_floats(m) + (size_t)c->CPC * q) * sizeof(float);
   if (cudaError_t e = ensure_smem_attr(c)) return bail(e);
   int bps = 0;
-  if (cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pass_kernel_ptr(m, c->big), c->block, c->smem))
+  if (cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pass_kernel_ptr(m, c->big, 0), c->block, c->smem))
     return bail(e);
   if (bps < 1) {
     nbldpc_destroy(c);
@@ -672,10 +688,11 @@ nbldpc_status_t nbldpc_decode_host(nbldpc_code_t c, const float* llr_host, int f
 }
 
 nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int iter, const float* w_in, float* w_out,
-                            float* u_out, uint8_t* hard, float* soft, void* stream) {
+                            float* u_out, uint8_t* hard, float* soft, int vn_algorithm, void* stream) {
   if (!c || frames < 1 || iter < 0 || !is_device_ptr(llr) || !is_device_ptr(w_out)) return NBLDPC_ERR_INVALID_ARGUMENT;
   if (iter >= 1 && (!is_device_ptr(w_in) || !is_device_ptr(hard))) return NBLDPC_ERR_INVALID_ARGUMENT;
   if ((u_out && !is_device_ptr(u_out)) || (soft && !is_device_ptr(soft))) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (vn_algorithm != 0 && vn_algorithm != 1) return NBLDPC_ERR_INVALID_ARGUMENT;
   if (!c->row_regular) return NBLDPC_ERR_UNSUPPORTED;  // internal edge slots == canonical order only then
   std::lock_guard<std::mutex> lk(c->mu);
   NB_TRY(cudaSetDevice(c->device));
@@ -700,7 +717,7 @@ nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int i
     NB_TRY(cudaMemcpyAsync(wcur, w_in, msg, cudaMemcpyDeviceToDevice, st));
   }
   PassParams P = make_params(c, 1, u_out);
-  NB_TRY(launch_pass(c, P, st));
+  NB_TRY(launch_pass(c, P, vn_algorithm, st));
   float* wnxt = w.dev.W + (size_t)((iter + 1) & 1) * frames * c->E * c->q;
   NB_TRY(cudaMemcpyAsync(w_out, wnxt, msg, cudaMemcpyDeviceToDevice, st));
   if (iter >= 1) {

@@ -1,0 +1,163 @@
+"""Host-side tests that need no GPU: the C-ABI library loads and exports every symbol the
+header declares, argument validation (which precedes any CUDA call, include/nbldpc.h), and
+the multi-process sharding / counter reduction of the N>1 path over gloo (world size 2)."""
+import ctypes
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def L():
+    import paper_1008_4370_b200 as nb
+
+    return nb.lib()
+
+
+def test_library_exports_every_header_symbol(L):
+    import paper_1008_4370_b200 as nb
+
+    syms = nb.header_symbols()
+    for must in ("nbldpc_code_create", "nbldpc_decode", "nbldpc_destroy"):
+        assert must in syms
+    missing = [s for s in syms if not hasattr(L, s)]
+    assert not missing, missing
+    # the library's device code is an sm_100a cubin
+    import shutil
+    import subprocess
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if os.path.exists(tool):
+        out = subprocess.run([tool, "--list-elf", nb._build.LIB], capture_output=True, text=True).stdout
+        assert "sm_100a" in out, out
+
+
+def _create(L, m, poly, M, N, rows, cols, coeffs):
+    r = np.ascontiguousarray(rows, np.int32)
+    c = np.ascontiguousarray(cols, np.int32)
+    h = np.ascontiguousarray(coeffs, np.uint16)
+    out = ctypes.c_void_p()
+    st = L.nbldpc_code_create(m, poly, M, N, r.size, r.ctypes.data, c.ctypes.data, h.ctypes.data, ctypes.byref(out))
+    return st, out
+
+
+def test_status_strings(L):
+    for s, txt in [(0, b"ok"), (-1, b"invalid argument"), (-2, b"polynomial"), (-3, b"unsupported"),
+                   (-4, b"CUDA"), (-5, b"memory")]:
+        assert txt in L.nbldpc_status_string(s)
+
+
+def test_code_create_validation_without_gpu(L):
+    """Every validation error is reported before the library touches the device."""
+    M, rows, cols, coeffs = synth.config_code("C1")
+    N = 16
+    assert _create(L, 2, 0x5, M, N, rows, cols, coeffs)[0] == -2  # x^2+1 not primitive
+    assert _create(L, 2, 0x13, M, N, rows, cols, coeffs)[0] == -2  # wrong degree
+    assert _create(L, 0, 0x3, M, N, rows, cols, coeffs)[0] == -1  # m out of range
+    assert _create(L, 9, 0x211, M, N, rows, cols, coeffs)[0] == -1
+    bad = coeffs.copy()
+    bad[3] = 4
+    assert _create(L, 2, 0x7, M, N, rows, cols, bad)[0] == -1  # coefficient outside GF(4)*
+    bad[3] = 0
+    assert _create(L, 2, 0x7, M, N, rows, cols, bad)[0] == -1
+    badr = rows.copy()
+    badr[0] = M
+    assert _create(L, 2, 0x7, M, N, badr, cols, coeffs)[0] == -1  # row out of range
+    assert _create(L, 2, 0x7, M, N, rows[:-1], cols[:-1], coeffs[:-1])[0] == -3  # a weight-1 column
+    dup_r = np.concatenate([rows, rows[:1]])
+    dup_c = np.concatenate([cols, cols[:1]])
+    dup_h = np.concatenate([coeffs, coeffs[:1]])
+    assert _create(L, 2, 0x7, M, N, dup_r, dup_c, dup_h)[0] == -3  # duplicate (row, col)
+    # a row of degree 1: column 0 moved entirely into its own extra row
+    M2, r2, c2, h2 = M + 1, rows.copy(), cols.copy(), coeffs.copy()
+    r2[np.where(c2 == 0)[0][0]] = M
+    assert _create(L, 2, 0x7, M2, N, r2, c2, h2)[0] == -3
+    out = ctypes.c_void_p()
+    assert L.nbldpc_code_create(2, 0x7, M, N, len(rows), None, None, None, ctypes.byref(out)) == -1
+
+
+def test_null_handles_are_rejected(L):
+    L.nbldpc_destroy(None)  # no-op
+    assert L.nbldpc_decode(None, None, 1, 1, None, None, None, None) == -1
+    assert L.nbldpc_code_info(None, None, None, None, None, None) == -1
+    assert L.nbldpc_slot_bytes(None) == 0
+    n = ctypes.c_longlong()
+    assert L.nbldpc_last_decode_launches(None, ctypes.byref(n)) == -1
+
+
+def test_frame_range_partitions_frames():
+    from paper_1008_4370_b200 import shard
+
+    seen = []
+    for r in range(8):
+        a, b = shard.frame_range(r, 8, 2048)
+        seen.extend(range(a, b))
+    assert seen == list(range(8 * 2048))
+    with pytest.raises(ValueError):
+        shard.frame_range(2, 2, 16)
+
+
+def test_llr_shards_do_not_depend_on_sharding():
+    """A frame's LLRs depend only on its global index (chunk-keyed Philox), so a rank's shard
+    equals the same rows of a single-process batch."""
+    whole = synth.config_llr("C5", 0, 600, point=3)
+    for world in (2, 3):
+        per = 600 // world
+        parts = [synth.config_llr("C5", r * per, per, point=3) for r in range(world)]
+        assert np.array_equal(np.concatenate(parts), whole[: per * world])
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_1008_4370_b200 import shard
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a, b = shard.frame_range(rank, world, 40)
+        llr = synth.config_llr("C2", a, b - a)
+        # stand-in for a rank's decode: per-frame "iterations" derived from its own inputs only
+        iters = (np.abs(llr).sum(1) % 7).astype(np.int64) + 1
+        c, t = shard.reduce_stats({"frame_iters": int(iters.sum()), "frames": b - a, "ok": rank},
+                                  {"ms": 10.0 + rank}, dist)
+        q.put((rank, c, t, iters.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_sharding_and_reduction():
+    import torch.multiprocessing as mp
+
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    # the single-process computation over all 80 frames
+    llr = synth.config_llr("C2", 0, 80)
+    iters = (np.abs(llr).sum(1) % 7).astype(np.int64) + 1
+    assert res[0][3] + res[1][3] == iters.tolist()
+    for _, c, t, _ in res:
+        assert c == {"frame_iters": float(iters.sum()), "frames": 80.0, "ok": 1.0}
+        assert t == {"ms": 11.0}
