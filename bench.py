@@ -35,14 +35,61 @@ import synth  # noqa: E402
 
 METRIC = "decoded info bits/s per iteration (1/2/4/8 B200) and % of roofline"
 UNIT = "info-bit-iterations/s"
-FFMA_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # FP32 FMA, 148 SMs x 128 lanes x 1.965 GHz
+# Peaks.  HBM: MEASURED_PEAKS.json (driver-measured copy bandwidth).  SFU (MUFU ex2/lg2)
+# and FP32 FMA: 148 SMs x 16 (MUFU) / 128 (FMA) lanes per clock x 1.965 GHz, the guide's unit counts at
+# clocks.max.sm; profiles/r01_microbench.log measured 15.85 MUFU and 127.6 FMA per SM-clock.
+SMS, CLK = 148, 1.965e9
+MUFU_PEAK = SMS * 16 * CLK          # ops/s
+FMA_PEAK = SMS * 128 * CLK          # FMA/s
+HBM_PEAK_FALLBACK = 6.65e12         # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
 
 
-def algorithmic_flops(cfg, iters_sum: int) -> float:
-    """2 x (E q^2 + N (m+1) q) FP32 FMAs per frame-iteration: the two variable-node
-    XOR-convolutions per variable and the m+1 decision points."""
+def hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]) * 1e9, "measured"
+    except (OSError, ValueError, KeyError):
+        return HBM_PEAK_FALLBACK, "fallback"
+
+
+def per_frame_iter(cfg, vn):
+    """Algorithmic work of one frame-iteration: SFU ops, FP32 FMAs, message bytes."""
     N, q, m = cfg["N"], cfg["q"], cfg["m"]
-    return 2.0 * iters_sum * (2 * N * q * q + N * (m + 1) * q)
+    E = 2 * N
+    mufu = 2 * E * q + N * q                        # ex2 of every VN input entry, lg2 of every output, ex2 of W_a
+    fma = (E * m * q if vn == 0 else E * q * q) + N * (m + 1) * q  # VN (separable / direct) + decision points
+    bytes_ = 2 * E * q * 4 + 4 * N * m + N           # one message set read + written, channel terms, symbols
+    return mufu, fma, bytes_
+
+
+def roofline(cfg, vn, frame_iters, seconds, traffic):
+    """The slower of the SFU, FP32 and HBM-message-byte bounds (BASELINE.json north_star) for the
+    work done; achieved / peak of that resource over the measured kernel time."""
+    mufu, fma, byts = per_frame_iter(cfg, vn)
+    hbm, hbm_src = hbm_peak()
+    t = {"alu": max(mufu / MUFU_PEAK, fma / FMA_PEAK), "hbm": byts / hbm}
+    bound = max(t, key=t.get)
+    n = frame_iters
+    comps = {
+        "sfu": {"achieved_Tops": mufu * n / seconds / 1e12, "peak_Tops": MUFU_PEAK / 1e12,
+                "frac": mufu * n / seconds / MUFU_PEAK},
+        "fp32_fma": {"achieved_TFLOPs": 2 * fma * n / seconds / 1e12, "peak_TFLOPs": 2 * FMA_PEAK / 1e12,
+                     "frac": fma * n / seconds / FMA_PEAK},
+        "hbm_message_bytes": {"achieved_GBs": byts * n / seconds / 1e9, "peak_GBs": hbm / 1e9, "peak_source": hbm_src,
+                              "frac": byts * n / seconds / hbm},
+    }
+    if bound == "hbm":
+        r = {"bound": "hbm", "achieved": byts * n / seconds / 1e9, "peak": hbm / 1e9, "unit": "GB/s"}
+    elif mufu / MUFU_PEAK >= fma / FMA_PEAK:
+        r = {"bound": "alu", "achieved": mufu * n / seconds / 1e12, "peak": MUFU_PEAK / 1e12,
+             "unit": "TFLOP/s", "pipe": "SFU (MUFU ex2/lg2 ops, not FLOPs)"}
+    else:
+        r = {"bound": "alu", "achieved": 2 * fma * n / seconds / 1e12, "peak": 2 * FMA_PEAK / 1e12,
+             "unit": "TFLOP/s", "pipe": "FP32 FMA"}
+    r["frac"] = r["achieved"] / r["peak"]
+    r["traffic"] = traffic
+    r["components"] = comps
+    r["roofline_info_bits_iter_per_s"] = info_bits(cfg) / max(t.values())
+    return r
 
 
 def info_bits(cfg) -> float:
@@ -151,18 +198,21 @@ def main():
     ap.add_argument("--point", type=int, default=0)
     ap.add_argument("--frames", type=int, default=0, help="frames per rank (default: the config's)")
     ap.add_argument("--slots", type=int, default=0)
-    ap.add_argument("--graph", type=int, default=0)
+    ap.add_argument("--graph", type=int, default=0, help="direct path only: 0 graph, -1 host loop")
+    ap.add_argument("--vn", type=int, default=0, help="0 separable (default), 1 direct q^2 convolution")
     ap.add_argument("--ref-frames", type=int, default=32)
     ap.add_argument("--cpu-frames", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--traffic", default=os.path.join(ROOT, "profiles", "r01_pass_kernel_traffic.json"))
+    ap.add_argument("--traffic", default=os.path.join(ROOT, "profiles", "traffic.json"))
     args = ap.parse_args()
     cfg = synth.CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
 
     import torch
+
+    from paper_1008_4370_b200 import shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -178,21 +228,23 @@ def main():
     import paper_1008_4370_b200 as nb
 
     F = args.frames or cfg["frames"]
+    f0, f1 = shard.frame_range(rank, world, F)
     M, rows, cols, coeffs = synth.config_code(cfg["name"])
     code = nb.Code(cfg["m"], cfg["poly"], M, cfg["N"], rows, cols, coeffs)
-    llr_np = synth.config_llr(cfg["name"], rank * F, F, point=args.point)
+    llr_np = synth.config_llr(cfg["name"], f0, f1 - f0, point=args.point)
     llr_host = torch.from_numpy(llr_np).pin_memory()
     llr = llr_host.to(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
-    kw = dict(slots=args.slots, use_graph=args.graph)
+    kw = dict(slots=args.slots, use_graph=args.graph, vn_algorithm=args.vn)
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(max(3, args.warmup)):
+    warm = max(3, args.warmup)
+    for _ in range(warm):
         out = code.decode(llr, cfg["max_iters"], **kw)
     torch.cuda.synchronize()
 
@@ -215,66 +267,58 @@ def main():
     clk = clocks.stop()
 
     # end to end through the host-buffer C-ABI entry (H2D + decode + D2H inside the timed region)
-    e2e = None
+    e2e_ms, e2e_iters = 0.0, 0
     if not args.no_e2e:
-        hout = None
         code.decode_host(llr_host, cfg["max_iters"], **kw)
         barrier()
-        e2e_ms, e2e_iters = [], 0
         for _ in range(args.steps):
             flush.fill_(1)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             hout = code.decode_host(llr_host, cfg["max_iters"], **kw)
-            e2e_ms.append(1e3 * (time.perf_counter() - t0))
+            e2e_ms += 1e3 * (time.perf_counter() - t0)
             e2e_iters += int(hout["iters"].sum())
         barrier()
-        e2e = {"total_ms": sum(e2e_ms), "iters": e2e_iters,
-               "h2d": llr_np.nbytes, "d2h": F * cfg["N"] + F + 4 * F}
 
-    total_ms = sum(step_ms)
-    stats = torch.tensor([total_ms, iters_sum, ok_sum, F * args.steps, launches,
-                          e2e["total_ms"] if e2e else 0.0, e2e["iters"] if e2e else 0], dtype=torch.float64,
-                         device=dev)
-    if dist is not None:
-        mx = stats.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(stats, op=dist.ReduceOp.SUM)
-        stats[0], stats[5] = mx[0], mx[5]
-    total_ms, iters_all, ok_all, frames_all, launches_all, e2e_ms_max, e2e_iters_all = stats.tolist()
+    cnt, tim = shard.reduce_stats(
+        {"frame_iters": iters_sum, "ok": ok_sum, "frames": F * args.steps, "launches": launches,
+         "e2e_frame_iters": e2e_iters},
+        {"ms": sum(step_ms), "e2e_ms": e2e_ms}, dist, device=dev)
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return 0
 
-    value = info_bits(cfg) * iters_all / (total_ms * 1e-3)
-    per_gpu_iters = iters_sum  # this rank's frame-iterations over the timed steps
-    achieved = algorithmic_flops(cfg, per_gpu_iters) / (sum(step_ms) * 1e-3) / 1e12
+    value = info_bits(cfg) * cnt["frame_iters"] / (tim["ms"] * 1e-3)
     traffic = None
     if os.path.exists(args.traffic):
         try:
-            traffic = json.load(open(args.traffic)).get(cfg["name"])
+            traffic = json.load(open(args.traffic)).get(f"{cfg['name']}:vn{args.vn}")
         except (OSError, ValueError):
             traffic = None
+    # this rank's kernel: its frame-iterations over its own device time
+    roof = roofline(cfg, args.vn, iters_sum, sum(step_ms) * 1e-3, traffic)
+    roof["kernel"] = ("lf_cluster_kernel (one launch per step + a 1-block setup kernel; "
+                      "CUDA events around the step)") if args.vn == 0 else "nb_pass_kernel (direct q^2 convolution)"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "warmup": warm, "ms_per_step": tim["ms"] / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_name(cfg, args.point), "frames_per_gpu": F, "global_frames": F * world,
                    "N": cfg["N"], "q": cfg["q"], "k": cfg["k"], "max_iters": cfg["max_iters"],
+                   "vn_algorithm": ["separable", "direct"][args.vn],
                    "parallelism": f"frames sharded over {world} GPU(s), no collective in the loop",
                    "l2": "flushed (256 MiB write) before every timed step",
-                   "slots": args.slots or "default", "mean_iters": iters_all / frames_all,
-                   "frame_error_rate": 1.0 - ok_all / frames_all},
-        "roofline": {"bound": "alu", "achieved": achieved, "peak": FFMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": achieved / FFMA_PEAK_TFLOPS, "traffic": traffic,
-                     "kernel": "nb_pass_kernel (whole decode timed; DESIGN.md 9)"},
-        "gpu_launches": int(launches_all),
+                   "slots": args.slots or "default", "mean_iters": cnt["frame_iters"] / cnt["frames"],
+                   "frame_error_rate": 1.0 - cnt["ok"] / cnt["frames"]},
+        "roofline": roof,
+        "gpu_launches": int(cnt["launches"]),
         "clocks": clk,
     }
-    if e2e:
-        line["e2e"] = {"value": info_bits(cfg) * e2e_iters_all / (e2e_ms_max * 1e-3), "unit": UNIT,
-                       "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]}
+    if not args.no_e2e:
+        line["e2e"] = {"value": info_bits(cfg) * cnt["e2e_frame_iters"] / (tim["e2e_ms"] * 1e-3), "unit": UNIT,
+                       "h2d_bytes_per_step": int(llr_np.nbytes),
+                       "d2h_bytes_per_step": int(F * cfg["N"] + F + 4 * F)}
     if not args.no_cpu_baseline and world == 1:
         v, dt, it, nt = cpu_oracle_run(cfg, args.point, 0, args.cpu_frames)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": nt, "kind": "oracle",

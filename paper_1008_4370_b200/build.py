@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
-LIB = os.path.join(LIBDIR, "libnbldpc.so")
+LIB = os.environ.get("NBLDPC_LIB", os.path.join(LIBDIR, "libnbldpc.so"))  # override: tuning builds
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -25,9 +25,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     newest = max(os.path.getmtime(s) for s in sources())
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+    defs = os.environ.get("NBLDPC_DEFS", "").split()  # e.g. "-DNB_CLUSTER_MINB=2" (tuning builds)
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", *defs,
            "-Xptxas", "-v" if verbose else "-O3", "-o", tmp, os.path.join(CSRC, "nbldpc.cu")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

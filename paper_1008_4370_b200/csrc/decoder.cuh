@@ -69,7 +69,7 @@ struct CallDev {            // per-call arguments, written on the stream before 
 struct WorkDev {
   int S;
   float* W;              // [2][S][E][q] packed messages (ping-pong by iteration parity)
-  float* Tt;             // [S][N][m]  tanh(L/2)
+  float* Tt;             // [S][N][8]  tanh(L/2) (m used)
   uint8_t* xhat;         // [S][N]
   float* soft;           // [S][N][m]
   uint8_t* con;          // [S][con_stride] per-edge syndrome contribution h_cv xhat_v (or paper bits)
@@ -78,6 +78,7 @@ struct WorkDev {
   int32_t* slot_iter;    // [S] CHECK-TO-VARIABLE steps completed (l)
   int32_t* slot_events;  // [S]
   int32_t* slot_counter; // [S] CTAs finished in the current pass
+  int32_t* slot_epoch;   // [S] passes completed (persistent kernel)
   int32_t* glob;         // [0] next frame, [1] active slots, [2] WHILE-body iterations
   CallDev* call;
 };
@@ -301,7 +302,7 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
     const int f = sh_frame[i], ell = sh_iter[i];
     float* th = NB_TH(buf);
     if (t == 0) {
-      const float* src = ell == 0 ? llr + ((size_t)f * cd.N + ed.var) * MB : ws.Tt + ((size_t)s * cd.N + ed.var) * MB;
+      const float* src = ell == 0 ? llr + ((size_t)f * cd.N + ed.var) * MB : ws.Tt + ((size_t)s * cd.N + ed.var) * 8;
 #pragma unroll
       for (int b = 0; b < MB; ++b) cp_async4(th + b, src + b);
     }
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
       for (int b = 0; b < MB; ++b) th[b] = tanhf(0.5f * th[b]);
       if (is_a && t == 0) {
 #pragma unroll
-        for (int b = 0; b < MB; ++b) ws.Tt[((size_t)s * cd.N + ed.var) * MB + b] = th[b];
+        for (int b = 0; b < MB; ++b) ws.Tt[((size_t)s * cd.N + ed.var) * 8 + b] = th[b];
       }
     }
     // P_v^0(z) for the thread's block z = t*R + zl (closed form)
@@ -748,7 +749,20 @@ __global__ void nb_setup_kernel(WorkDev ws, CallDev call) {
     ws.slot_iter[i] = 0;
     ws.slot_events[i] = 0;
     ws.slot_counter[i] = 0;
+    ws.slot_epoch[i] = 0;
   }
+}
+
+// cluster kernel: frames are taken from glob[0] starting at 0; slot = cluster
+__global__ void nb_cluster_setup_kernel(WorkDev ws, CallDev call) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) {
+    *ws.call = call;
+    ws.glob[0] = 0;
+    ws.glob[1] = 0;
+    ws.glob[2] = 0;
+  }
+  if (i < ws.S) ws.slot_events[i] = 0;
 }
 
 // step mode: slots hold frames 0..frames-1 at iteration `iter`
@@ -760,12 +774,14 @@ __global__ void nb_step_setup_kernel(WorkDev ws, CallDev call, int iter) {
     ws.slot_iter[i] = iter;
     ws.slot_events[i] = 0;
     ws.slot_counter[i] = 0;
+    ws.slot_epoch[i] = 0;
   }
 }
 
-__global__ void nb_tanh_kernel(const float* llr, float* Tt, size_t n) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-    Tt[i] = tanhf(0.5f * llr[i]);
+// Tt[fv][b] = tanh(L_{fv,b} / 2), rows of 8 floats (m used)
+__global__ void nb_tanh_kernel(const float* llr, float* Tt, size_t nvar, int m) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nvar * m; i += (size_t)gridDim.x * blockDim.x)
+    Tt[(i / m) * 8 + i % m] = tanhf(0.5f * llr[i]);
 }
 
 __global__ void nb_control_kernel(int32_t* glob, cudaGraphConditionalHandle h) {

@@ -1,0 +1,682 @@
+// lf_cluster.cuh -- cluster-per-frame kernel of the B200 Log-Fourier SP decoder (arXiv:1008.4370),
+// separable variable node (NBLDPC_VN_SEPARABLE).
+//
+// One launch decodes the whole batch.  The grid is the number of thread-block clusters that fit on
+// the GPU at once (persistent); each cluster of CS CTAs decodes one frame at a time, start to finish,
+// then takes the next frame from a global counter.  CTA rank r of the cluster owns the check chunks
+// r, r + CS, ... (checks_per_cta checks each, CPC * TPC threads).  One flooding iteration is one
+// pass of every CTA over its chunks (the next chunk's messages prefetched with cp.async while the
+// current one computes) followed by a hardware cluster barrier; the frame's two message buffers
+// stay L2-resident (clusters x 2 E 2^m x 4 bytes).  After the barrier each CTA folds its checks'
+// syndrome bytes, ORs a "not a codeword" flag into rank 0's shared memory (DSMEM), and a second
+// barrier makes the stopping decision cluster-uniform.
+//
+// Per check c and edge e = (c, v) with partner edge e' = (c', v) one pass computes
+//   VARIABLE TO CHECK  raw = P_v^0 (*) Gamma^-1(W_e'), U_e = normalise(Gamma(raw)),
+//       with P^0 = (x)_i (1, tanh(L_i/2)): the XOR-convolution is m butterfly stages
+//       x(z) <- x(z) + t_i x(z ^ alpha^i)
+//   TENTATIVE DECISION at v's first edge: M_v(z) = sum_y raw(y) W_e(z ^ y) at
+//       z = 0, alpha^i (and H_cv alpha^i in paper mode)
+//   CHECK TO VARIABLE X_e(pi_e^-1 z) = U_e(z) (scatter), TOT(w) = sum_j X_j(w),
+//       W_e(next)(z) = TOT(pi_e^-1 z) - U_e(z) (log-magnitudes add, signs XOR).
+//
+// Thread layout: an edge is owned by a team of TT = max(1, q/16) threads holding R = min(q, 16)
+// entries each.  Phase A: thread t holds z = 16t + r (register bits = z bits 0..3); phase B (after
+// one shared-memory transposition): z = jl | t << (8-m) | h << 4 with r = jl + 2^(8-m) h.
+#pragma once
+#include "decoder.cuh"
+
+namespace nb {
+
+struct ClusterParams {
+  CodeDev code;
+  WorkDev ws;          // slots = clusters (decode) or frames (step mode)
+  int chunks;          // G = ceil(M / checks_per_cta)
+  int checks_per_cta;  // CPC
+  int tpc;             // threads per check (power of two)
+  int step_mode;       // 1: nbldpc_step (frames 0..F-1 at iteration step_iter, one pass each)
+  int step_iter;
+  int rec_per_cta;     // compact edge records per CTA in shared memory (max over ranks)
+  float* u_out;        // step mode: optional U dump [F][E][q]
+};
+
+// compact per-edge record kept in shared memory for the CTA's chunks (16 bytes)
+struct EdgeRec {
+  int32_t partner_a;  // partner edge << 1 | is_a ; -1: padding slot
+  int32_t var;
+  uint64_t pinv;      // byte i: pi_h^-1(alpha^i), i < 8
+};
+
+template <int MB>
+struct CCfg {
+  static constexpr int Q = 1 << MB;
+  static constexpr int LR = MB < 4 ? MB : 4;
+  static constexpr int R = 1 << LR;                 // entries per thread
+  static constexpr int TT = Q / R;                  // threads per edge team
+  static constexpr int LJ = MB >= 4 ? 8 - MB : 0;   // phase-B low register bits (TT > 1)
+  static constexpr int V = 1 << LJ;                 // phase-B contiguous run (floats)
+  static constexpr int CH = R >= 4 ? R / 4 : 1;     // 16-byte chunks per thread
+  // per-team shared memory (floats): stage buffers [2] x (Wp q | th 8), X (transposition / scatter)
+  static constexpr int QS = Q < 4 ? 4 : Q;          // th at a 16-byte boundary
+  static constexpr int STG = QS + 8;
+  static constexpr int XS = TT > 1 ? Q + Q / 4 : Q;
+  static constexpr int TEAM0 = 2 * STG + XS;
+  static constexpr int TEAM = TEAM0 + ((4 - TEAM0 % 32) + 32) % 32;  // team stride = 4 mod 32 words
+};
+
+__host__ __device__ constexpr int ctz_c(int r) { return (r & 1) ? 0 : 1 + ctz_c(r >> 1); }
+
+template <int CH>
+__device__ __forceinline__ int cswz(int c, int key) { return c ^ (key & (CH - 1)); }
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_nrank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_count() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `p` (a shared variable of this CTA) in CTA `rank`
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, uint32_t rank) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void dsmem_st(uint32_t addr, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ int dsmem_ld(uint32_t addr) {
+  int v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void dsmem_or(uint32_t addr, int v) {
+  asm volatile("red.shared::cluster.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// TOT(w) = sum_j X_j(w) over the thread's WPT w's (stride TT*JPT) and JPT teams (stride TEAM words)
+template <int R, int JPT, int TT, int TEAM>
+__device__ __forceinline__ void tot_sum(const float* smem, int gbase, float* TOT, int wgrp, int split, int pck,
+                                        bool cvalid) {
+  constexpr int WPT = R / JPT;
+  const float* g = smem + gbase;
+#pragma unroll
+  for (int i = 0; i < WPT; ++i) {
+    float mag = 0.0f;
+    uint32_t sg = 0;
+#pragma unroll
+    for (int jj = 0; jj < JPT; ++jj) {
+      const float v = g[jj * TEAM + i * TT * JPT];
+      mag += fabsf(v);
+      sg ^= __float_as_uint(v);
+    }
+    if constexpr (WPT == 1) {
+      for (int off = 1; off < split; off <<= 1) {
+        mag += __shfl_xor_sync(0xffffffffu, mag, off);
+        sg ^= __shfl_xor_sync(0xffffffffu, sg, off);
+      }
+    }
+    if (cvalid && (WPT > 1 || (pck & (split - 1)) == 0))
+      TOT[wgrp + TT * JPT * i] = __uint_as_float(__float_as_uint(mag) | (sg & kSign));
+  }
+}
+
+template <int MB, int NTHR>
+#ifndef NB_CLUSTER_MINB
+#define NB_CLUSTER_MINB 2
+#endif
+__global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_cluster_kernel(ClusterParams P) {
+  using C = CCfg<MB>;
+  constexpr int Q = C::Q, R = C::R, TT = C::TT, LR = C::LR, LJ = C::LJ, CH = C::CH;
+  extern __shared__ __align__(16) float smem[];
+  __shared__ int sh_frame, sh_flag[2], sh_bad;
+
+  const CodeDev& cd = P.code;
+  const WorkDev& ws = P.ws;
+  const int tid = threadIdx.x;
+  const int nthr = blockDim.x;
+  const int lane = tid & 31;
+  const uint32_t rank = cluster_rank();
+  const uint32_t csz = cluster_nrank();
+  const int clid = (int)cluster_id();
+  const int ncl = (int)cluster_count();
+  const int TPC = P.tpc;
+  const int CPC = P.checks_per_cta;
+  const int KT = TPC / TT;                       // teams per check (incl. padding teams)
+  const int nch = ((int)P.chunks - (int)rank + (int)csz - 1) / (int)csz;  // my chunks: rank + k*csz
+
+  // ---- my position in a chunk (fixed)
+  const int lc = tid / TPC;
+  const int pck = tid - lc * TPC;
+  const int j = pck / TT;
+  const int t = pck & (TT - 1);
+  const bool in_check = lc < CPC;
+  const int team = tid / TT;
+  const int nteams = nthr / TT;
+  float* const TB = smem + team * C::TEAM;  // STG[0] | STG[1] | X
+  float* const X = TB + 2 * C::STG;
+  float* const TOT = smem + nteams * C::TEAM + lc * Q;
+  EdgeRec* const recs = reinterpret_cast<EdgeRec*>(smem + nteams * C::TEAM + CPC * Q);
+
+  // TOT(w) gather offsets: thread pck owns WPT w's x JPT teams of its check (R terms, natural X)
+  const int SPLIT = KT > R ? KT / R : 1;
+  const int JPT = KT / SPLIT;
+  const int wgrp = pck / SPLIT;
+  const int jbase = (pck % SPLIT) * JPT;
+  const int gbase = in_check ? (lc * KT + jbase) * C::TEAM + 2 * C::STG + wgrp : 0;
+  // my phase-B z's
+  int zr[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) zr[r] = TT > 1 ? ((r & ((1 << LJ) - 1)) | (t << LJ) | ((r >> LJ) << 4)) : r;
+
+  // ---- compact edge records of my chunks -> shared memory (once)
+  for (int i = tid; i < nch * CPC * KT; i += nthr) {
+    const int kc = i / (CPC * KT), rem = i - kc * CPC * KT;
+    const int l = rem / KT, jj = rem - l * KT;
+    const int c = ((int)rank + kc * (int)csz) * CPC + l;
+    EdgeRec rr{-1, 0, 0};
+    if (c < cd.M && jj < cd.k_max) {
+      const EdgeDev* ep = cd.edges + (size_t)c * cd.kpad + jj;
+      if (ep->var >= 0) {
+        rr.partner_a = (ep->partner << 1) | (ep->is_a ? 1 : 0);
+        rr.var = ep->var;
+        uint64_t pv = 0;
+        for (int b = 0; b < 8; ++b) pv |= (uint64_t)ep->pinvb[b] << (8 * b);
+        rr.pinv = pv;
+      }
+    }
+    recs[i] = rr;
+  }
+  if (tid == 0) {
+    sh_flag[0] = 0;
+    sh_flag[1] = 0;
+  }
+  __syncthreads();
+  cluster_sync_all();  // every CTA of the cluster has started before any DSMEM access
+
+  const CallDev* call = ws.call;
+  const int max_iters = call->max_iters;
+  const int mode = call->mode;
+  const int want_soft = call->want_soft;
+  const int step = P.step_mode;
+  const size_t EQ = (size_t)cd.E * Q;
+  const uint32_t flag0 = dsmem_addr(&sh_flag[0], 0), flag1 = dsmem_addr(&sh_flag[1], 0);
+
+  int round = 0;
+#pragma unroll 1
+  for (;;) {
+    // ---- next frame for the cluster
+    int f, slot;
+    if (step) {
+      f = clid + round * ncl;
+      slot = f;
+      if (f >= call->frames) break;
+    } else {
+      if (rank == 0 && tid == 0) {
+        const int nf = atomicAdd(&ws.glob[0], 1);
+        for (uint32_t r = 0; r < csz; ++r) dsmem_st(dsmem_addr(&sh_frame, r), nf);
+      }
+      cluster_sync_all();
+      f = sh_frame;
+      slot = clid;
+      if (f >= call->frames) break;
+      if (rank == 0 && tid == 0) {
+        sh_flag[0] = 0;
+        sh_flag[1] = 0;
+      }
+    }
+    ++round;
+    uint8_t* const xout = step ? ws.xhat + (size_t)f * cd.N : call->hard + (size_t)f * cd.N;
+    float* const sout = step ? ws.soft + (size_t)f * cd.N * MB : call->soft_out + (size_t)f * cd.N * MB;
+    float* const Tt = ws.Tt + (size_t)slot * cd.N * 8;
+    uint8_t* const con = ws.con + (size_t)slot * ws.con_stride;
+
+#pragma unroll 1
+    for (int ell = step ? P.step_iter : 0;; ++ell) {
+      const int rb_ = step ? 0 : (ell & 1);
+      const float* const Win = ws.W + ((size_t)rb_ * ws.S + slot) * EQ;
+      float* const Wout = ws.W + ((size_t)(rb_ ^ 1) * ws.S + slot) * EQ;
+      const bool do_dec = ell >= 1;
+      const bool do_cn = step || ell < max_iters;
+
+      // stage chunk kc into buffer b: partner message, own message (v's first edge), channel terms
+      auto stage = [&](int kc, int b) {
+        if (!in_check) return;
+        const EdgeRec rr = recs[(kc * CPC + lc) * KT + j];
+        if (rr.partner_a < 0) return;
+        float* st = TB + b * C::STG;
+        const int var = rr.var;
+        if (t == 0) {
+          if (ell == 0) {
+            const float* src = call->llr + ((size_t)f * cd.N + var) * MB;
+#pragma unroll
+            for (int bb = 0; bb < MB; ++bb) cp_async4(st + C::QS + bb, src + bb);
+          } else {
+            const float* src = Tt + (size_t)var * 8;
+            cp_async16(st + C::QS, src);
+            cp_async16(st + C::QS + 4, src + 4);
+          }
+        }
+        if (ell == 0) return;
+        const float* sp = Win + (size_t)(rr.partner_a >> 1) * Q + t * R;
+        if constexpr (R >= 4) {
+          const int key = TT > 1 ? t : j;
+#pragma unroll
+          for (int ch = 0; ch < CH; ++ch) cp_async16(st + t * R + 4 * cswz<CH>(ch, key), sp + 4 * ch);
+        } else {
+          cp_async8(st, sp);
+        }
+      };
+
+      int buf = 0;
+      if (nch > 0) stage(0, 0);
+      cp_async_commit();
+#pragma unroll 1
+      for (int kc = 0; kc < nch; ++kc) {
+        if (kc + 1 < nch) stage(kc + 1, buf ^ 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+
+        const int c = ((int)rank + kc * (int)csz) * CPC + lc;
+        const bool cvalid = in_check && c < cd.M;
+        EdgeRec rr{-1, 0, 0};
+        if (in_check) rr = recs[(kc * CPC + lc) * KT + j];
+        const bool active = cvalid && rr.partner_a >= 0;
+        const bool is_a = active && (rr.partner_a & 1);
+        const int e = c * cd.kpad + j;
+        const int var = rr.var;
+        float* st = TB + buf * C::STG;
+
+        // ---- channel terms t_i = tanh(L_i / 2)
+        float th[MB];
+#pragma unroll
+        for (int b = 0; b < MB; ++b) th[b] = active ? st[C::QS + b] : 0.0f;
+        // W_e (own message, for v's decision at its first edge) straight from L2 into registers;
+        // consumed after the variable node
+        float4 wo4[CH];
+        if (is_a && do_dec) {
+          if constexpr (R >= 4) {
+            const float4* so = reinterpret_cast<const float4*>(Win + (size_t)e * Q + t * R);
+#pragma unroll
+            for (int ch = 0; ch < CH; ++ch) wo4[ch] = __ldcg(so + ch);
+          } else {
+            const float2 v2 = __ldcg(reinterpret_cast<const float2*>(Win + (size_t)e * Q));
+            wo4[0] = make_float4(v2.x, v2.y, 0.f, 0.f);
+          }
+        }
+        if (ell == 0 && active) {
+#pragma unroll
+          for (int b = 0; b < MB; ++b) th[b] = tanhf(0.5f * th[b]);
+          if (is_a && t == 0 && !step) {
+#pragma unroll
+            for (int b = 0; b < MB; ++b) Tt[(size_t)var * 8 + b] = th[b];
+          }
+        }
+
+        // ---- VARIABLE TO CHECK: x (phase B) = P^0 (*) Gamma^-1(W_e'); at l = 0, x = P^0
+        float x[R];
+        if (ell == 0) {
+          float base = 1.0f;
+          if constexpr (TT > 1) {
+#pragma unroll
+            for (int b = 0; b < MB - 4; ++b)
+              if ((t >> b) & 1) base *= th[LJ + b];
+          }
+          x[0] = base;
+#pragma unroll
+          for (int rb = 0; rb < LR; ++rb) {
+            const int zb = (TT > 1) ? (rb < LJ ? rb : 4 + rb - LJ) : rb;
+#pragma unroll
+            for (int jj = 0; jj < (1 << rb); ++jj) x[(1 << rb) + jj] = x[jj] * th[zb];
+          }
+        } else {
+          if constexpr (R >= 4) {
+            const int key = TT > 1 ? t : j;
+#pragma unroll
+            for (int ch = 0; ch < CH; ++ch) {
+              const float4 v = *reinterpret_cast<const float4*>(st + t * R + 4 * cswz<CH>(ch, key));
+              x[4 * ch] = to_lin(v.x); x[4 * ch + 1] = to_lin(v.y); x[4 * ch + 2] = to_lin(v.z); x[4 * ch + 3] = to_lin(v.w);
+            }
+          } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) x[r] = to_lin(st[r]);
+          }
+          bfly_regs<R, 0, LR>(x, th);  // z bits 0..LR-1
+          if constexpr (TT > 1) {
+            // transposition through X (padded layout idx(z) = z + 4 (z >> 4))
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch)
+              *reinterpret_cast<float4*>(X + 20 * t + 4 * ch) = make_float4(x[4 * ch], x[4 * ch + 1], x[4 * ch + 2], x[4 * ch + 3]);
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < TT; ++h) {
+              const float* src = X + ((t << LJ) | (h << 4)) + 4 * h;
+              if constexpr (LJ == 0) {
+                x[h] = src[0];
+              } else if constexpr (LJ == 1) {
+                const float2 v = *reinterpret_cast<const float2*>(src);
+                x[2 * h] = v.x; x[2 * h + 1] = v.y;
+              } else {
+#pragma unroll
+                for (int q4 = 0; q4 < (1 << LJ) / 4; ++q4) {
+                  const float4 v = *reinterpret_cast<const float4*>(src + 4 * q4);
+                  x[(h << LJ) + 4 * q4] = v.x; x[(h << LJ) + 4 * q4 + 1] = v.y;
+                  x[(h << LJ) + 4 * q4 + 2] = v.z; x[(h << LJ) + 4 * q4 + 3] = v.w;
+                }
+              }
+            }
+            // z bits 4..MB-1 = register bits LJ..3
+            if constexpr (LJ <= 0) bfly_reg<R, 0>(x, th[4 - LJ]);
+            if constexpr (LJ <= 1) bfly_reg<R, 1>(x, th[(5 - LJ) < MB ? 5 - LJ : 0]);
+            if constexpr (LJ <= 2) bfly_reg<R, 2>(x, th[(6 - LJ) < MB ? 6 - LJ : 0]);
+            if constexpr (LJ <= 3) bfly_reg<R, 3>(x, th[(7 - LJ) < MB ? 7 - LJ : 0]);
+          }
+        }
+
+        // ---- normalise so that entry 0 is (0, 0), Gamma in base 2, packed
+        float raw0 = x[0];
+        if constexpr (TT > 1) raw0 = __shfl_sync(0xffffffffu, x[0], lane & ~(TT - 1));
+        uint32_t up[R];
+        {
+          const float lg0 = lg2a(raw0);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            // |x| >= 2^-120 keeps the magnitude finite (<= lg0 + 120); a rounding-negative magnitude
+            // loses its sign bit to the message sign in the same LOP3
+            const float mag = lg0 - lg2a(fmaxf(fabsf(x[r]), 7.52316385e-37f));
+            up[r] = (__float_as_uint(mag) & ~kSign) | (__float_as_uint(x[r]) & kSign);
+          }
+          if (!(raw0 > 0.0f)) {  // DC term <= 0: neutral message + numerical event (reading R10)
+#pragma unroll
+            for (int r = 0; r < R; ++r) up[r] = __float_as_uint(zr[r] == 0 ? 0.0f : kFloor);
+            if (active && t == 0) atomicAdd(&ws.slot_events[step ? 0 : slot], 1);
+          }
+        }
+        if (P.u_out != nullptr && active) {
+          float* dst = P.u_out + ((size_t)f * cd.E + e) * Q;
+#pragma unroll
+          for (int r = 0; r < R; ++r) dst[zr[r]] = __uint_as_float(up[r]);
+        }
+
+        // ---- TENTATIVE DECISION at v's first edge: M_v(z) = sum_y raw(y) W_e(z ^ y)
+        if (do_dec) {
+          // D = Gamma^-1(W_e) in the row layout word(z) = 16 tB(z) + rB(z), over the consumed Wp
+          float* DB = st;
+          if (is_a) {
+            if constexpr (TT > 1) {
+#pragma unroll
+              for (int ch = 0; ch < 4; ++ch) {
+                const float4 v = wo4[ch];
+                const float d4[4] = {to_lin(v.x), to_lin(v.y), to_lin(v.z), to_lin(v.w)};
+#pragma unroll
+                for (int k4 = 0; k4 < 4; ++k4) {
+                  const int w = 4 * ch + k4;  // z = 16 t + w: tB = w >> LJ, rB = (w & (2^LJ - 1)) | t << LJ
+                  DB[16 * (w >> LJ) + (w & ((1 << LJ) - 1)) + (t << LJ)] = d4[k4];
+                }
+              }
+            } else if constexpr (R >= 4) {
+#pragma unroll
+              for (int ch = 0; ch < CH; ++ch) {
+                const float4 v = wo4[ch];
+                DB[4 * ch] = to_lin(v.x); DB[4 * ch + 1] = to_lin(v.y); DB[4 * ch + 2] = to_lin(v.z); DB[4 * ch + 3] = to_lin(v.w);
+              }
+            } else {
+#pragma unroll
+              DB[0] = to_lin(wo4[0].x);
+              if constexpr (R > 1) DB[1] = to_lin(wo4[0].y);
+            }
+          }
+          if constexpr (TT > 1) __syncwarp();
+          float mf[MB + 1];
+#pragma unroll
+          for (int b = 0; b <= MB; ++b) mf[b] = 0.0f;
+          if (is_a) {
+            // pairwise FFMA2 dot products: M(0) and the register-bit points in-thread, the
+            // thread-bit points against the partner thread's row
+            float d[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) d[r] = DB[16 * t + r];
+            if constexpr (R >= 2) {
+              float2 acc[MB + 1];
+#pragma unroll
+              for (int b = 0; b <= MB; ++b) acc[b] = make_float2(0.0f, 0.0f);
+#pragma unroll
+              for (int p = 0; p < R / 2; ++p) {
+                const float2 xp = make_float2(x[2 * p], x[2 * p + 1]);
+                acc[0] = __ffma2_rn(xp, make_float2(d[2 * p], d[2 * p + 1]), acc[0]);
+#pragma unroll
+                for (int rb = 0; rb < LR; ++rb) {
+                  const int zb = (TT > 1) ? (rb < LJ ? rb : 4 + rb - LJ) : rb;
+                  const int w = (2 * p) ^ (1 << rb);
+                  const float2 dp = rb == 0 ? make_float2(d[w], d[w - 1]) : make_float2(d[w], d[w + 1]);
+                  acc[zb + 1] = __ffma2_rn(xp, dp, acc[zb + 1]);
+                }
+              }
+              if constexpr (TT > 1) {
+#pragma unroll
+                for (int b = 0; b < MB - 4; ++b) {
+                  const float* row = DB + 16 * (t ^ (1 << b));
+#pragma unroll
+                  for (int p = 0; p < R / 2; ++p)
+                    acc[LJ + b + 1] = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]),
+                                                 make_float2(row[2 * p], row[2 * p + 1]), acc[LJ + b + 1]);
+                }
+              }
+#pragma unroll
+              for (int b = 0; b <= MB; ++b) mf[b] = acc[b].x + acc[b].y;
+            } else {
+              mf[0] = x[0] * d[0];
+            }
+          }
+          if constexpr (TT > 1) {
+#pragma unroll
+            for (int off = TT / 2; off >= 1; off >>= 1)
+#pragma unroll
+              for (int b = 0; b <= MB; ++b) mf[b] += __shfl_xor_sync(0xffffffffu, mf[b], off);
+          }
+          const uint32_t s0z = mf[0] < 0.0f ? 1u : 0u;  // sgn_GF2 M(0); an exact zero has sign 0
+          if (is_a && t == 0) {
+            int xv = 0;
+#pragma unroll
+            for (int b = 0; b < MB; ++b) xv |= (int)(((mf[b + 1] < 0.0f) ? 1u : 0u) ^ s0z) << b;
+            xout[var] = (uint8_t)xv;
+            if (mode == 0) {  // syndrome contributions h_cv xhat_v to both checks of v
+              const EdgeDev* ep = cd.edges + e;
+              int ca = 0, cbv = 0;
+              if (xv != 0) {
+                const int lx = __ldg(&cd.gf_log[xv]);
+                ca = __ldg(&cd.gf_exp[ep->logh + lx]);
+                cbv = __ldg(&cd.gf_exp[ep->plogh + lx]);
+              }
+              con[e] = (uint8_t)ca;
+              con[rr.partner_a >> 1] = (uint8_t)cbv;
+            }
+            if (want_soft) {
+              const float l0 = __logf(fabsf(mf[0]));
+#pragma unroll
+              for (int b = 0; b < MB; ++b) sout[(size_t)var * MB + b] = __logf(fabsf(mf[b + 1])) - l0;
+            }
+          }
+          if (mode == 1) {
+            // paper-mode fast syndrome: sign bits of M_v(H_cv alpha^i), both checks
+            uint64_t pa = 0, pbv = 0;
+            if (is_a) {
+              const uint32_t* ea = reinterpret_cast<const uint32_t*>(cd.edges + e) + 3;
+              const uint32_t* eb = reinterpret_cast<const uint32_t*>(cd.edges + (rr.partner_a >> 1)) + 3;
+              pa = (uint64_t)__ldg(ea) | ((uint64_t)__ldg(ea + 1) << 32);
+              pbv = (uint64_t)__ldg(eb) | ((uint64_t)__ldg(eb + 1) << 32);
+            }
+            int ma = 0, mbb = 0;
+#pragma unroll 1
+            for (int i = 0; i < 2 * MB; ++i) {
+              const int z = (int)(((i < MB ? pa : pbv) >> (8 * (i < MB ? i : i - MB))) & 0xFF);
+              float acc = 0.0f;
+              if (is_a) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                  const int yy = zr[r] ^ z;
+                  int w;
+                  if constexpr (TT > 1) {
+                    w = 16 * ((yy >> LJ) & (TT - 1)) + ((yy & ((1 << LJ) - 1)) | ((yy >> 4) << LJ));
+                  } else {
+                    w = yy;
+                  }
+                  acc = fmaf(x[r], DB[w], acc);
+                }
+              }
+              if constexpr (TT > 1) {
+#pragma unroll
+                for (int off = TT / 2; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+              }
+              const int bit = (int)(((acc < 0.0f) ? 1u : 0u) ^ s0z);
+              if (i < MB) ma |= bit << i; else mbb |= bit << (i - MB);
+            }
+            if (is_a && t == 0) {
+              con[e] = (uint8_t)ma;
+              con[rr.partner_a >> 1] = (uint8_t)mbb;
+            }
+          }
+        }
+
+        // ---- CHECK TO VARIABLE
+        if (do_cn) {
+          // pi_e^-1 of my z's (linear: XOR of basis images)
+          int oidx[R];
+          {
+            const uint64_t pv = rr.pinv;
+            int base = 0;
+            if constexpr (TT > 1) {
+#pragma unroll
+              for (int b = 0; b < MB - 4; ++b)
+                if ((t >> b) & 1) base ^= (int)((pv >> (8 * (LJ + b))) & 0xFFu);
+            }
+            oidx[0] = base;
+#pragma unroll
+            for (int rb = 0; rb < LR; ++rb) {
+              const int zb = (TT > 1) ? (rb < LJ ? rb : 4 + rb - LJ) : rb;
+              const int img = (int)((pv >> (8 * zb)) & 0xFFu);
+#pragma unroll
+              for (int jj = 0; jj < (1 << rb); ++jj) oidx[(1 << rb) + jj] = oidx[jj] ^ img;
+            }
+            if (!active) {
+#pragma unroll
+              for (int r = 0; r < R; ++r) oidx[r] = zr[r];
+            }
+          }
+          if constexpr (TT > 1) __syncwarp();  // transposition / DB reads of X done
+          if (cvalid) {
+            // scatter: X_e(pi_e^-1 z) = U_e(z) = T_e(.); padding teams hold the neutral message
+#pragma unroll
+            for (int r = 0; r < R; ++r) X[oidx[r]] = active ? __uint_as_float(up[r]) : 0.0f;
+          }
+          check_sync(lc, TPC);
+          switch (JPT) {
+            case 1: tot_sum<R, 1, TT, C::TEAM>(smem, gbase, TOT, wgrp, SPLIT, pck, cvalid); break;
+            case 2: tot_sum<R, (R >= 2 ? 2 : 1), TT, C::TEAM>(smem, gbase, TOT, wgrp, SPLIT, pck, cvalid); break;
+            case 4: tot_sum<R, (R >= 4 ? 4 : 1), TT, C::TEAM>(smem, gbase, TOT, wgrp, SPLIT, pck, cvalid); break;
+            case 8: tot_sum<R, (R >= 8 ? 8 : 1), TT, C::TEAM>(smem, gbase, TOT, wgrp, SPLIT, pck, cvalid); break;
+            default: tot_sum<R, R, TT, C::TEAM>(smem, gbase, TOT, wgrp, SPLIT, pck, cvalid); break;
+          }
+          check_sync(lc, TPC);
+          if (active) {
+            float out[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const float xt = TOT[oidx[r]];
+              const float mg = fabsf(xt) - __uint_as_float(up[r] & ~kSign);  // >= 0 up to rounding
+              out[r] = __uint_as_float((__float_as_uint(mg) & ~kSign) | ((__float_as_uint(xt) ^ up[r]) & kSign));
+            }
+            float* dst = Wout + (size_t)e * Q;
+            if constexpr (TT > 1) {
+              constexpr int V = C::V;
+#pragma unroll
+              for (int h = 0; h < TT; ++h) {
+                float* dp = dst + ((t << LJ) | (h << 4));
+                if constexpr (V == 1) {
+                  dp[0] = out[h];
+                } else if constexpr (V == 2) {
+                  *reinterpret_cast<float2*>(dp) = make_float2(out[2 * h], out[2 * h + 1]);
+                } else {
+#pragma unroll
+                  for (int q4 = 0; q4 < V / 4; ++q4)
+                    *reinterpret_cast<float4*>(dp + 4 * q4) = make_float4(out[h * V + 4 * q4], out[h * V + 4 * q4 + 1],
+                                                                          out[h * V + 4 * q4 + 2], out[h * V + 4 * q4 + 3]);
+                }
+              }
+            } else if constexpr (R >= 4) {
+#pragma unroll
+              for (int ch = 0; ch < CH; ++ch)
+                reinterpret_cast<float4*>(dst)[ch] = make_float4(out[4 * ch], out[4 * ch + 1], out[4 * ch + 2], out[4 * ch + 3]);
+            } else {
+#pragma unroll
+              for (int r = 0; r < R; ++r) dst[r] = out[r];
+            }
+          }
+        }
+        __syncthreads();  // buffers of this chunk are free
+        buf ^= 1;
+      }
+      cp_async_wait<0>();
+      if (step) break;
+
+      // ---- end of the pass: stopping rule, cluster-uniform
+      cluster_sync_all();  // every message, estimate and syndrome byte of the pass is written
+      if (tid == 0) sh_bad = 0;
+      __syncthreads();
+      if (ell >= 1) {
+        // my checks' syndromes s_c = XOR of the contribution bytes on their kpad edge slots
+        int bad = 0;
+        const int kp = cd.kpad;
+        for (int i = tid; i < nch * CPC; i += nthr) {
+          const int kc = i / CPC, l = i - kc * CPC;
+          const int c = ((int)rank + kc * (int)csz) * CPC + l;
+          if (c >= cd.M) continue;
+          const uint32_t* cs = reinterpret_cast<const uint32_t*>(con + (size_t)c * kp);
+          uint32_t acc = 0;
+          for (int w = 0; w < kp / 4; ++w) acc ^= __ldcg(cs + w);
+          acc ^= acc >> 16;
+          acc ^= acc >> 8;
+          bad |= (int)(acc & 0xFFu);
+        }
+        if (__syncthreads_or(bad != 0) && tid == 0) dsmem_or((ell & 1) ? flag1 : flag0, 1);
+      }
+      if (rank == 0 && tid == 0) sh_flag[(ell + 1) & 1] = 0;  // read before this pass by everyone
+      cluster_sync_all();
+      int ok = 0;
+      if (ell >= 1) ok = dsmem_ld((ell & 1) ? flag1 : flag0) == 0;
+      const bool done = (ell >= 1 && call->early_stop && ok) || ell >= max_iters;
+      if (done) {
+        if (rank == 0 && tid == 0) {
+          call->ok[f] = (uint8_t)ok;
+          call->iters[f] = ell;
+          if (call->events_out) call->events_out[f] = ws.slot_events[slot];
+          ws.slot_events[slot] = 0;
+        }
+        break;
+      }
+    }
+    if (step) continue;
+  }
+  cp_async_wait<0>();
+  // no CTA may exit while others can still address its shared memory
+  if (!step) cluster_sync_all();
+}
+
+}  // namespace nb

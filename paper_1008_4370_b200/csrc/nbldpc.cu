@@ -10,12 +10,14 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <new>
 #include <vector>
 
 #include "../../include/nbldpc.h"
 #include "decoder.cuh"
+#include "lf_cluster.cuh"
 
 using nb::CallDev;
 using nb::CodeDev;
@@ -59,9 +61,13 @@ struct nbldpc_code_s {
   uint8_t* gf_log_d = nullptr;
   std::mutex mu;
   Workspace ws;
-  // launch geometry
+  // launch geometry of the pass kernel (NBLDPC_VN_DIRECT)
   int TT = 1, TPC = 1, CPC = 1, groups = 1, block = 32, big = 0, blocks_per_sm = 1, sms = 148;  // TPC padded
   size_t smem = 0;
+  // launch geometry of the cluster kernel (NBLDPC_VN_SEPARABLE): TPC a power of two, clusters of
+  // p_cs CTAs per frame, p_ncl clusters resident
+  int p_tpc = 1, p_cpc = 1, p_groups = 1, p_block = 32, p_big = 0, p_cs = 1, p_ncl = 1, p_recs = 0;
+  size_t p_smem = 0;
 };
 
 namespace {
@@ -106,11 +112,11 @@ size_t slot_bytes_of(const nbldpc_code_s* c) {
   const size_t q = c->q;
   size_t b = 0;
   b += 2 * (size_t)c->E * q * sizeof(float);  // W ping-pong
-  b += (size_t)c->N * c->m * sizeof(float);   // tanh
+  b += (size_t)c->N * 8 * sizeof(float);      // tanh (rows of 8)
   b += (size_t)c->N;                          // xhat
   b += (size_t)c->N * c->m * sizeof(float);   // soft
   b += (size_t)c->con_stride;                 // syndrome contributions
-  b += 4 * sizeof(int32_t);
+  b += 5 * sizeof(int32_t);
   return b;
 }
 
@@ -153,6 +159,61 @@ void* pass_kernel_ptr(int m, int big, int direct) {
   return direct ? pass_kernel_ptr_t<true>(m, big) : pass_kernel_ptr_t<false>(m, big);
 }
 
+template <int MB, int NTHR>
+void* cluster_fn() { return reinterpret_cast<void*>(&nb::lf_cluster_kernel<MB, NTHR>); }
+void* persist_kernel_ptr(int m, int big) {
+  switch (m * 2 + (big ? 1 : 0)) {
+    case 2: return cluster_fn<1, 256>();
+    case 3: return cluster_fn<1, 512>();
+    case 4: return cluster_fn<2, 256>();
+    case 5: return cluster_fn<2, 512>();
+    case 6: return cluster_fn<3, 256>();
+    case 7: return cluster_fn<3, 512>();
+    case 8: return cluster_fn<4, 256>();
+    case 9: return cluster_fn<4, 512>();
+    case 10: return cluster_fn<5, 256>();
+    case 11: return cluster_fn<5, 512>();
+    case 12: return cluster_fn<6, 256>();
+    case 13: return cluster_fn<6, 512>();
+    case 14: return cluster_fn<7, 256>();
+    case 15: return cluster_fn<7, 512>();
+    case 16: return cluster_fn<8, 256>();
+    case 17: return cluster_fn<8, 512>();
+  }
+  return nullptr;
+}
+// shared-memory words per edge team of the cluster kernel (nb::CCfg<m>::TEAM)
+int persist_team_words(int m) {
+  switch (m) {
+    case 1: return nb::CCfg<1>::TEAM;
+    case 2: return nb::CCfg<2>::TEAM;
+    case 3: return nb::CCfg<3>::TEAM;
+    case 4: return nb::CCfg<4>::TEAM;
+    case 5: return nb::CCfg<5>::TEAM;
+    case 6: return nb::CCfg<6>::TEAM;
+    case 7: return nb::CCfg<7>::TEAM;
+    case 8: return nb::CCfg<8>::TEAM;
+  }
+  return 0;
+}
+
+cudaError_t launch_cluster(const nbldpc_code_s* c, const nb::ClusterParams& P, int ncl, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(ncl * c->p_cs));
+  cfg.blockDim = dim3((unsigned)c->p_block);
+  cfg.dynamicSmemBytes = c->p_smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)c->p_cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[] = {const_cast<nb::ClusterParams*>(&P)};
+  return cudaLaunchKernelExC(&cfg, persist_kernel_ptr(c->m, c->p_big), args);
+}
+
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a property of the kernel (one instantiation per
 // (m, block variant)) shared by every code on the device: only ever raise it.
 std::mutex g_attr_mu;
@@ -167,6 +228,18 @@ cudaError_t ensure_smem_attr(const nbldpc_code_s* c) {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
     if (e != cudaSuccess) return e;
     g_attr_smem[d][k] = c->smem;
+  }
+  if (c->p_cs > 8) {
+    cudaError_t e = cudaFuncSetAttribute(persist_kernel_ptr(c->m, c->p_big), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  static size_t p_attr[64][18] = {};
+  const int d = c->device & 63, k = c->m * 2 + c->p_big;
+  if (p_attr[d][k] < c->p_smem) {
+    cudaError_t e = cudaFuncSetAttribute(persist_kernel_ptr(c->m, c->p_big), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)c->p_smem);
+    if (e != cudaSuccess) return e;
+    p_attr[d][k] = c->p_smem;
   }
   return cudaSuccess;
 }
@@ -209,7 +282,7 @@ nbldpc_status_t ensure_workspace(nbldpc_code_s* c, int S) {
     return o;
   };
   const size_t oW = take(2 * (size_t)S * c->E * q * sizeof(float));
-  const size_t oT = take((size_t)S * c->N * c->m * sizeof(float));
+  const size_t oT = take((size_t)S * c->N * 8 * sizeof(float));
   const size_t oX = take((size_t)S * c->N);
   const size_t oS = take((size_t)S * c->N * c->m * sizeof(float));
   const size_t oP = take((size_t)S * c->con_stride);
@@ -217,6 +290,7 @@ nbldpc_status_t ensure_workspace(nbldpc_code_s* c, int S) {
   const size_t oI = take((size_t)S * sizeof(int32_t));
   const size_t oV = take((size_t)S * sizeof(int32_t));
   const size_t oC = take((size_t)S * sizeof(int32_t));
+  const size_t oE = take((size_t)S * sizeof(int32_t));
   const size_t oG = take(16 * sizeof(int32_t));
   const size_t oK = take(sizeof(CallDev));
   void* base = nullptr;
@@ -238,6 +312,7 @@ nbldpc_status_t ensure_workspace(nbldpc_code_s* c, int S) {
   w.dev.slot_iter = reinterpret_cast<int32_t*>(b + oI);
   w.dev.slot_events = reinterpret_cast<int32_t*>(b + oV);
   w.dev.slot_counter = reinterpret_cast<int32_t*>(b + oC);
+  w.dev.slot_epoch = reinterpret_cast<int32_t*>(b + oE);
   w.dev.glob = reinterpret_cast<int32_t*>(b + oG);
   w.dev.call = reinterpret_cast<CallDev*>(b + oK);
   if (!w.host_flag) NB_TRY(cudaMallocHost(&w.host_flag, 64));
@@ -261,6 +336,28 @@ PassParams make_params(const nbldpc_code_s* c, int step_mode, float* u_out) {  /
   P.checks_per_cta = c->CPC;
   P.tpc = c->TPC;
   P.step_mode = step_mode;
+  P.u_out = u_out;
+  return P;
+}
+
+nb::ClusterParams make_cparams(const nbldpc_code_s* c, int step_mode, int step_iter, float* u_out) {
+  nb::ClusterParams P{};
+  P.code.m = c->m;
+  P.code.M = c->M;
+  P.code.N = c->N;
+  P.code.E = c->E;
+  P.code.k_max = c->k_max;
+  P.code.kpad = c->kpad;
+  P.code.edges = c->edges_d;
+  P.code.gf_exp = c->gf_exp_d;
+  P.code.gf_log = c->gf_log_d;
+  P.ws = c->ws.dev;
+  P.chunks = c->p_groups;
+  P.checks_per_cta = c->p_cpc;
+  P.tpc = c->p_tpc;
+  P.step_mode = step_mode;
+  P.step_iter = step_iter;
+  P.rec_per_cta = c->p_recs;
   P.u_out = u_out;
   return P;
 }
@@ -359,7 +456,8 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   if (direct != 0 && direct != 1) return NBLDPC_ERR_INVALID_ARGUMENT;
   if (slots < 0) return NBLDPC_ERR_INVALID_ARGUMENT;
   if ((soft && !is_device_ptr(soft)) || (events && !is_device_ptr(events))) return NBLDPC_ERR_INVALID_ARGUMENT;
-  const int S = slots > 0 ? std::min(slots, frames) : default_slots(c, frames);
+  int S = slots > 0 ? std::min(slots, frames) : default_slots(c, frames);
+  if (!direct) S = std::min(slots > 0 ? slots : c->p_ncl, std::min(c->p_ncl, frames));  // slots = clusters
   NB_TRY(cudaSetDevice(c->device));
   nbldpc_status_t rs = ensure_workspace(c, S);
   if (rs != NBLDPC_OK) return rs;
@@ -376,11 +474,22 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   call.mode = mode;
   call.early_stop = early;
   call.want_soft = soft != nullptr;
-  nb::nb_setup_kernel<<<(S + 255) / 256, 256, 0, st>>>(w.dev, call);
+  if (direct) {
+    nb::nb_setup_kernel<<<(S + 255) / 256, 256, 0, st>>>(w.dev, call);
+  } else {
+    nb::nb_cluster_setup_kernel<<<(S + 255) / 256, 256, 0, st>>>(w.dev, call);
+  }
   NB_TRY(cudaGetLastError());
   w.last_stream = st;
   w.last_graph = use_graph >= 0;
   w.last_host_launches = 1;
+  if (!direct) {
+    nb::ClusterParams PP = make_cparams(c, 0, 0, nullptr);
+    NB_TRY(launch_cluster(c, PP, S, st));
+    w.last_graph = 0;
+    w.last_host_launches = 2;
+    return NBLDPC_OK;
+  }
   if (use_graph >= 0) {
     rs = build_graph(c, direct);
     if (rs != NBLDPC_OK) return rs;
@@ -569,7 +678,58 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
   c->groups = (M + c->CPC - 1) / c->CPC;
   c->block = (int)align_up((size_t)c->CPC * c->TPC, 32);
   c->smem = ((size_t)(c->block / tt) * team_floats(m) + (size_t)c->CPC * q) * sizeof(float);
+  {
+    // persistent kernel: threads per check = next power of two >= k_max * TT
+    int tpc = 1;
+    while (tpc < k_max * tt) tpc <<= 1;
+    if (tpc > kBigBlock) {
+      nbldpc_destroy(c);
+      return NBLDPC_ERR_UNSUPPORTED;
+    }
+    c->p_tpc = tpc;
+    c->p_big = tpc > 256 ? 1 : 0;
+    c->p_cpc = std::min(std::max(1, 256 / tpc), M);
+    c->p_groups = (M + c->p_cpc - 1) / c->p_cpc;
+    c->p_block = (int)align_up((size_t)c->p_cpc * tpc, 32);
+    // cluster size: the largest divisor of the chunk count that is <= 8 (portable clusters)
+    // small clusters measured fastest (fewer CTAs per barrier, more chunks per CTA per iteration):
+    // 2 CTAs per frame when the chunk count is even
+    int cs = c->p_groups % 2 == 0 ? 2 : 1;
+    if (const char* env = getenv("NBLDPC_CLUSTER_SIZE")) {  // tuning override (a divisor of the chunk count)
+      const int v = atoi(env);
+      if (v >= 1 && v <= 16 && c->p_groups % v == 0) cs = v;
+    }
+    c->p_cs = cs;
+    const int kt = tpc / tt;
+    c->p_recs = ((c->p_groups + cs - 1) / cs) * c->p_cpc * kt;
+    c->p_smem = ((size_t)(c->p_block / tt) * persist_team_words(m) + (size_t)c->p_cpc * q) * sizeof(float) +
+                (size_t)c->p_recs * sizeof(nb::EdgeRec);
+    if (c->p_smem > 227 * 1024) {
+      nbldpc_destroy(c);
+      return NBLDPC_ERR_UNSUPPORTED;
+    }
+  }
   if (cudaError_t e = ensure_smem_attr(c)) return bail(e);
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(c->p_cs * 64));
+    cfg.blockDim = dim3((unsigned)c->p_block);
+    cfg.dynamicSmemBytes = c->p_smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)c->p_cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaError_t e = cudaOccupancyMaxActiveClusters(&ncl, persist_kernel_ptr(m, c->p_big), &cfg)) return bail(e);
+    if (ncl < 1) {
+      nbldpc_destroy(c);
+      return NBLDPC_ERR_UNSUPPORTED;
+    }
+    c->p_ncl = ncl;
+  }
   int bps = 0;
   if (cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pass_kernel_ptr(m, c->big, 0), c->block, c->smem))
     return bail(e);
@@ -612,7 +772,7 @@ nbldpc_status_t nbldpc_last_decode_launches(nbldpc_code_t c, long long* launches
     *launches = 0;
     return NBLDPC_OK;
   }
-  if (!w.last_graph) {
+  if (!w.last_graph) {  // host loop or persistent kernel
     *launches = w.last_host_launches;
     return NBLDPC_OK;
   }
@@ -711,14 +871,21 @@ nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int i
   nb::nb_step_setup_kernel<<<(frames + 255) / 256, 256, 0, st>>>(w.dev, call, iter);
   NB_TRY(cudaGetLastError());
   if (iter >= 1) {
-    nb::nb_tanh_kernel<<<256, 256, 0, st>>>(llr, w.dev.Tt, (size_t)frames * c->N * c->m);
+    nb::nb_tanh_kernel<<<256, 256, 0, st>>>(llr, w.dev.Tt, (size_t)frames * c->N, c->m);
     NB_TRY(cudaGetLastError());
-    float* wcur = w.dev.W + (size_t)(iter & 1) * frames * c->E * c->q;
-    NB_TRY(cudaMemcpyAsync(wcur, w_in, msg, cudaMemcpyDeviceToDevice, st));
   }
-  PassParams P = make_params(c, 1, u_out);
-  NB_TRY(launch_pass(c, P, vn_algorithm, st));
-  float* wnxt = w.dev.W + (size_t)((iter + 1) & 1) * frames * c->E * c->q;
+  // the direct pass kernel selects buffers by iteration parity, the persistent one by epoch (0)
+  const int in_buf = vn_algorithm ? (iter & 1) : 0;
+  float* wcur = w.dev.W + (size_t)in_buf * frames * c->E * c->q;
+  float* wnxt = w.dev.W + (size_t)(in_buf ^ 1) * frames * c->E * c->q;
+  if (iter >= 1) NB_TRY(cudaMemcpyAsync(wcur, w_in, msg, cudaMemcpyDeviceToDevice, st));
+  if (vn_algorithm) {
+    PassParams P = make_params(c, 1, u_out);
+    NB_TRY(launch_pass(c, P, 1, st));
+  } else {
+    nb::ClusterParams PP = make_cparams(c, 1, iter, u_out);
+    NB_TRY(launch_cluster(c, PP, std::min(frames, c->p_ncl), st));
+  }
   NB_TRY(cudaMemcpyAsync(w_out, wnxt, msg, cudaMemcpyDeviceToDevice, st));
   if (iter >= 1) {
     NB_TRY(cudaMemcpyAsync(hard, w.dev.xhat, (size_t)frames * c->N, cudaMemcpyDeviceToDevice, st));
