@@ -61,10 +61,45 @@ struct CCfg {
   static constexpr int STG = QS + 8;
   static constexpr int XS = TT > 1 ? Q + Q / 4 : Q;
   static constexpr int TEAM0 = 2 * STG + XS;
-  static constexpr int TEAM = TEAM0 + ((4 - TEAM0 % 32) + 32) % 32;  // team stride = 4 mod 32 words
+  // team stride = 4 s (mod 32) words with s = 1 (TT = 1) or 8 / TT: the 8 threads of every quarter
+  // warp then hit 8 distinct bank quads in the 128-bit stage / transposition accesses
+  static constexpr int SQ = TT == 1 ? 1 : (TT <= 8 ? 8 / TT : 0);
+  static constexpr int TEAM = TEAM0 + (((4 * SQ) - TEAM0 % 32) + 64) % 32;
+  static constexpr bool BULK = Q >= 4;  // message rows are whole 16-byte chunks: bulk-copied
 };
 
-__host__ __device__ constexpr int ctz_c(int r) { return (r & 1) ? 0 : 1 + ctz_c(r >> 1); }
+// Global position of message entry z (TT > 1): the 16-byte chunk c of the 16-entry block b is stored
+// at chunk c ^ (b & 3), so that the phase-A reads of a bulk-copied row are bank-conflict free.
+template <int MB>
+__host__ __device__ __forceinline__ int gpos(int z) {
+  if constexpr (MB >= 5) {
+    return (z & ~15) | ((((z >> 2) & 3) ^ ((z >> 4) & 3)) << 2) | (z & 3);
+  } else {
+    return z;
+  }
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* mb, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* mb, uint32_t tx) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(smem_u32(mb)),
+               "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          smem_u32(mb)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mb) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(mb))
+               : "memory");
+}
 
 template <int CH>
 __device__ __forceinline__ int cswz(int c, int key) { return c ^ (key & (CH - 1)); }
@@ -146,6 +181,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   constexpr int Q = C::Q, R = C::R, TT = C::TT, LR = C::LR, LJ = C::LJ, CH = C::CH;
   extern __shared__ __align__(16) float smem[];
   __shared__ int sh_frame, sh_flag[2], sh_bad;
+  __shared__ __align__(8) uint64_t sh_mbar[2];  // stage buffers: all teams arrive, bulk copies complete_tx
 
   const CodeDev& cd = P.code;
   const WorkDev& ws = P.ws;
@@ -206,9 +242,13 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   if (tid == 0) {
     sh_flag[0] = 0;
     sh_flag[1] = 0;
+    mbar_init(&sh_mbar[0], (uint32_t)nteams);
+    mbar_init(&sh_mbar[1], (uint32_t)nteams);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  cluster_sync_all();  // every CTA of the cluster has started before any DSMEM access
+  cluster_sync_all();
+  uint32_t mb_parity = 0;  // bit b: parity of the next completion of stage buffer b  // every CTA of the cluster has started before any DSMEM access
 
   const CallDev* call = ws.call;
   const int max_iters = call->max_iters;
@@ -256,43 +296,43 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
       const bool do_cn = step || ell < max_iters;
 
       // stage chunk kc into buffer b: partner message, own message (v's first edge), channel terms
+      // stage chunk kc into buffer b (one arrival per team on sh_mbar[b]): the partner message row and
+      // the channel terms, bulk-copied by the team's first thread (plain loads at l = 0 and for q = 2)
       auto stage = [&](int kc, int b) {
-        if (!in_check) return;
-        const EdgeRec rr = recs[(kc * CPC + lc) * KT + j];
-        if (rr.partner_a < 0) return;
+        if (t != 0) return;
         float* st = TB + b * C::STG;
-        const int var = rr.var;
-        if (t == 0) {
-          if (ell == 0) {
-            const float* src = call->llr + ((size_t)f * cd.N + var) * MB;
+        uint32_t tx = 0;
+        EdgeRec rr{-1, 0, 0};
+        if (in_check) rr = recs[(kc * CPC + lc) * KT + j];
+        const bool act = in_check && rr.partner_a >= 0;
+        if (act && ell == 0) {
+          const float* src = call->llr + ((size_t)f * cd.N + rr.var) * MB;
 #pragma unroll
-            for (int bb = 0; bb < MB; ++bb) cp_async4(st + C::QS + bb, src + bb);
-          } else {
-            const float* src = Tt + (size_t)var * 8;
-            cp_async16(st + C::QS, src);
-            cp_async16(st + C::QS + 4, src + 4);
-          }
+          for (int bb = 0; bb < MB; ++bb) st[C::QS + bb] = __ldg(src + bb);
+        } else if (act && !C::BULK) {
+          const float* src = Tt + (size_t)rr.var * 8;
+#pragma unroll
+          for (int bb = 0; bb < MB; ++bb) st[C::QS + bb] = __ldcg(src + bb);
+          const float* sp = Win + (size_t)(rr.partner_a >> 1) * Q;
+#pragma unroll
+          for (int r = 0; r < Q; ++r) st[r] = __ldcg(sp + r);
+        } else if (act) {
+          tx = Q * 4 + 32;
         }
-        if (ell == 0) return;
-        const float* sp = Win + (size_t)(rr.partner_a >> 1) * Q + t * R;
-        if constexpr (R >= 4) {
-          const int key = TT > 1 ? t : j;
-#pragma unroll
-          for (int ch = 0; ch < CH; ++ch) cp_async16(st + t * R + 4 * cswz<CH>(ch, key), sp + 4 * ch);
-        } else {
-          cp_async8(st, sp);
+        mbar_arrive_tx(&sh_mbar[b], tx);
+        if (tx) {
+          bulk_g2s(st, Win + (size_t)(rr.partner_a >> 1) * Q, Q * 4, &sh_mbar[b]);
+          bulk_g2s(st + C::QS, Tt + (size_t)rr.var * 8, 32, &sh_mbar[b]);
         }
       };
 
       int buf = 0;
       if (nch > 0) stage(0, 0);
-      cp_async_commit();
 #pragma unroll 1
       for (int kc = 0; kc < nch; ++kc) {
         if (kc + 1 < nch) stage(kc + 1, buf ^ 1);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
+        mbar_wait(&sh_mbar[buf], (mb_parity >> buf) & 1u);
+        mb_parity ^= 1u << buf;
 
         const int c = ((int)rank + kc * (int)csz) * CPC + lc;
         const bool cvalid = in_check && c < cd.M;
@@ -315,7 +355,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           if constexpr (R >= 4) {
             const float4* so = reinterpret_cast<const float4*>(Win + (size_t)e * Q + t * R);
 #pragma unroll
-            for (int ch = 0; ch < CH; ++ch) wo4[ch] = __ldcg(so + ch);
+            for (int ch = 0; ch < CH; ++ch) wo4[ch] = __ldcg(so + (TT > 1 ? cswz<CH>(ch, t) : ch));
           } else {
             const float2 v2 = __ldcg(reinterpret_cast<const float2*>(Win + (size_t)e * Q));
             wo4[0] = make_float4(v2.x, v2.y, 0.f, 0.f);
@@ -348,7 +388,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           }
         } else {
           if constexpr (R >= 4) {
-            const int key = TT > 1 ? t : j;
+            const int key = TT > 1 ? t : 0;  // global chunk swizzle gpos (TT > 1)
 #pragma unroll
             for (int ch = 0; ch < CH; ++ch) {
               const float4 v = *reinterpret_cast<const float4*>(st + t * R + 4 * cswz<CH>(ch, key));
@@ -608,16 +648,16 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               constexpr int V = C::V;
 #pragma unroll
               for (int h = 0; h < TT; ++h) {
-                float* dp = dst + ((t << LJ) | (h << 4));
+                const int z0 = (t << LJ) | (h << 4);
                 if constexpr (V == 1) {
-                  dp[0] = out[h];
+                  dst[gpos<MB>(z0)] = out[h];
                 } else if constexpr (V == 2) {
-                  *reinterpret_cast<float2*>(dp) = make_float2(out[2 * h], out[2 * h + 1]);
+                  *reinterpret_cast<float2*>(dst + gpos<MB>(z0)) = make_float2(out[2 * h], out[2 * h + 1]);
                 } else {
 #pragma unroll
                   for (int q4 = 0; q4 < V / 4; ++q4)
-                    *reinterpret_cast<float4*>(dp + 4 * q4) = make_float4(out[h * V + 4 * q4], out[h * V + 4 * q4 + 1],
-                                                                          out[h * V + 4 * q4 + 2], out[h * V + 4 * q4 + 3]);
+                    *reinterpret_cast<float4*>(dst + gpos<MB>(z0 + 4 * q4)) = make_float4(
+                        out[h * V + 4 * q4], out[h * V + 4 * q4 + 1], out[h * V + 4 * q4 + 2], out[h * V + 4 * q4 + 3]);
                 }
               }
             } else if constexpr (R >= 4) {
@@ -630,6 +670,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             }
           }
         }
+        // generic-proxy writes to this stage buffer (DB) are ordered before its next bulk fill
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();  // buffers of this chunk are free
         buf ^= 1;
       }
@@ -677,6 +719,17 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   cp_async_wait<0>();
   // no CTA may exit while others can still address its shared memory
   if (!step) cluster_sync_all();
+}
+
+// message layout conversion for nbldpc_step: natural order <-> the kernel's global order gpos
+__global__ void nb_msg_layout_kernel(const float* src, float* dst, size_t nmsg, int q, int m, int to_kernel) {
+  const size_t n = nmsg * (size_t)q;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t msg = i / q;
+    const int z = (int)(i % q);
+    const int g = m >= 5 ? ((z & ~15) | ((((z >> 2) & 3) ^ ((z >> 4) & 3)) << 2) | (z & 3)) : z;
+    if (to_kernel) dst[msg * q + g] = src[i]; else dst[i] = src[msg * q + g];
+  }
 }
 
 }  // namespace nb

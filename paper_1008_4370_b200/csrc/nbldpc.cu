@@ -878,7 +878,14 @@ nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int i
   const int in_buf = vn_algorithm ? (iter & 1) : 0;
   float* wcur = w.dev.W + (size_t)in_buf * frames * c->E * c->q;
   float* wnxt = w.dev.W + (size_t)(in_buf ^ 1) * frames * c->E * c->q;
-  if (iter >= 1) NB_TRY(cudaMemcpyAsync(wcur, w_in, msg, cudaMemcpyDeviceToDevice, st));
+  if (iter >= 1) {
+    if (vn_algorithm) {
+      NB_TRY(cudaMemcpyAsync(wcur, w_in, msg, cudaMemcpyDeviceToDevice, st));
+    } else {  // the cluster kernel keeps messages in its chunk-swizzled order
+      nb::nb_msg_layout_kernel<<<512, 256, 0, st>>>(w_in, wcur, (size_t)frames * c->E, c->q, c->m, 1);
+      NB_TRY(cudaGetLastError());
+    }
+  }
   if (vn_algorithm) {
     PassParams P = make_params(c, 1, u_out);
     NB_TRY(launch_pass(c, P, 1, st));
@@ -886,7 +893,12 @@ nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int i
     nb::ClusterParams PP = make_cparams(c, 1, iter, u_out);
     NB_TRY(launch_cluster(c, PP, std::min(frames, c->p_ncl), st));
   }
-  NB_TRY(cudaMemcpyAsync(w_out, wnxt, msg, cudaMemcpyDeviceToDevice, st));
+  if (vn_algorithm) {
+    NB_TRY(cudaMemcpyAsync(w_out, wnxt, msg, cudaMemcpyDeviceToDevice, st));
+  } else {
+    nb::nb_msg_layout_kernel<<<512, 256, 0, st>>>(wnxt, w_out, (size_t)frames * c->E, c->q, c->m, 0);
+    NB_TRY(cudaGetLastError());
+  }
   if (iter >= 1) {
     NB_TRY(cudaMemcpyAsync(hard, w.dev.xhat, (size_t)frames * c->N, cudaMemcpyDeviceToDevice, st));
     if (soft)
