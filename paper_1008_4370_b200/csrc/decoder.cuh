@@ -52,6 +52,7 @@ struct CodeDev {
   const EdgeDev* edges;       // [E]
   const uint8_t* gf_exp;      // [2(q-1)+1] alpha^i
   const uint8_t* gf_log;      // [q]
+  const uint64_t* pinv_tab;   // [q] byte i of entry h: pi_h^-1(alpha^i) (entry 0 unused)
 };
 
 struct CallDev {            // per-call arguments, written on the stream before the pass loop

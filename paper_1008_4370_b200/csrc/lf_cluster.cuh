@@ -40,11 +40,11 @@ struct ClusterParams {
   float* u_out;        // step mode: optional U dump [F][E][q]
 };
 
-// compact per-edge record kept in shared memory for the CTA's chunks (16 bytes)
+// compact per-edge record kept in shared memory for the CTA's chunks (8 bytes); the Fourier
+// permutation images of h come from a per-field table (CodeDev::pinv_tab, copied to shared memory)
 struct EdgeRec {
   int32_t partner_a;  // partner edge << 1 | is_a ; -1: padding slot
-  int32_t var;
-  uint64_t pinv;      // byte i: pi_h^-1(alpha^i), i < 8
+  uint32_t var_h;     // variable << 8 | h_cv
 };
 
 template <int MB>
@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   float* const TB = smem + team * C::TEAM;  // STG[0] | STG[1] | X
   float* const X = TB + 2 * C::STG;
   float* const TOT = smem + nteams * C::TEAM + lc * Q;
-  EdgeRec* const recs = reinterpret_cast<EdgeRec*>(smem + nteams * C::TEAM + CPC * Q);
+  uint64_t* const PT = reinterpret_cast<uint64_t*>(smem + nteams * C::TEAM + CPC * Q);  // [q] pi_h^-1 images
+  EdgeRec* const recs = reinterpret_cast<EdgeRec*>(PT + Q);
 
   // TOT(w) gather offsets: thread pck owns WPT w's x JPT teams of its check (R terms, natural X)
   const int SPLIT = KT > R ? KT / R : 1;
@@ -226,19 +227,17 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
     const int kc = i / (CPC * KT), rem = i - kc * CPC * KT;
     const int l = rem / KT, jj = rem - l * KT;
     const int c = ((int)rank + kc * (int)csz) * CPC + l;
-    EdgeRec rr{-1, 0, 0};
+    EdgeRec rr{-1, 0};
     if (c < cd.M && jj < cd.k_max) {
       const EdgeDev* ep = cd.edges + (size_t)c * cd.kpad + jj;
       if (ep->var >= 0) {
         rr.partner_a = (ep->partner << 1) | (ep->is_a ? 1 : 0);
-        rr.var = ep->var;
-        uint64_t pv = 0;
-        for (int b = 0; b < 8; ++b) pv |= (uint64_t)ep->pinvb[b] << (8 * b);
-        rr.pinv = pv;
+        rr.var_h = ((uint32_t)ep->var << 8) | ep->h;
       }
     }
     recs[i] = rr;
   }
+  for (int h = tid; h < Q; h += nthr) PT[h] = cd.pinv_tab[h];
   if (tid == 0) {
     sh_flag[0] = 0;
     sh_flag[1] = 0;
@@ -302,15 +301,16 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         if (t != 0) return;
         float* st = TB + b * C::STG;
         uint32_t tx = 0;
-        EdgeRec rr{-1, 0, 0};
+        EdgeRec rr{-1, 0};
         if (in_check) rr = recs[(kc * CPC + lc) * KT + j];
         const bool act = in_check && rr.partner_a >= 0;
+        const int rvar = (int)(rr.var_h >> 8);
         if (act && ell == 0) {
-          const float* src = call->llr + ((size_t)f * cd.N + rr.var) * MB;
+          const float* src = call->llr + ((size_t)f * cd.N + rvar) * MB;
 #pragma unroll
           for (int bb = 0; bb < MB; ++bb) st[C::QS + bb] = __ldg(src + bb);
         } else if (act && !C::BULK) {
-          const float* src = Tt + (size_t)rr.var * 8;
+          const float* src = Tt + (size_t)rvar * 8;
 #pragma unroll
           for (int bb = 0; bb < MB; ++bb) st[C::QS + bb] = __ldcg(src + bb);
           const float* sp = Win + (size_t)(rr.partner_a >> 1) * Q;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         mbar_arrive_tx(&sh_mbar[b], tx);
         if (tx) {
           bulk_g2s(st, Win + (size_t)(rr.partner_a >> 1) * Q, Q * 4, &sh_mbar[b]);
-          bulk_g2s(st + C::QS, Tt + (size_t)rr.var * 8, 32, &sh_mbar[b]);
+          bulk_g2s(st + C::QS, Tt + (size_t)rvar * 8, 32, &sh_mbar[b]);
         }
       };
 
@@ -336,12 +336,12 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 
         const int c = ((int)rank + kc * (int)csz) * CPC + lc;
         const bool cvalid = in_check && c < cd.M;
-        EdgeRec rr{-1, 0, 0};
+        EdgeRec rr{-1, 0};
         if (in_check) rr = recs[(kc * CPC + lc) * KT + j];
         const bool active = cvalid && rr.partner_a >= 0;
         const bool is_a = active && (rr.partner_a & 1);
         const int e = c * cd.kpad + j;
-        const int var = rr.var;
+        const int var = (int)(rr.var_h >> 8);
         float* st = TB + buf * C::STG;
 
         // ---- channel terms t_i = tanh(L_i / 2)
@@ -443,10 +443,13 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             const float mag = lg0 - lg2a(fmaxf(fabsf(x[r]), 7.52316385e-37f));
             up[r] = (__float_as_uint(mag) & ~kSign) | (__float_as_uint(x[r]) & kSign);
           }
-          if (!(raw0 > 0.0f)) {  // DC term <= 0: neutral message + numerical event (reading R10)
+          if (!active) {  // padding edge: the neutral message (0, 0) in every entry
+#pragma unroll
+            for (int r = 0; r < R; ++r) up[r] = 0u;
+          } else if (!(raw0 > 0.0f)) {  // DC term <= 0: neutral message + numerical event (reading R10)
 #pragma unroll
             for (int r = 0; r < R; ++r) up[r] = __float_as_uint(zr[r] == 0 ? 0.0f : kFloor);
-            if (active && t == 0) atomicAdd(&ws.slot_events[step ? 0 : slot], 1);
+            if (t == 0) atomicAdd(&ws.slot_events[step ? 0 : slot], 1);
           }
         }
         if (P.u_out != nullptr && active) {
@@ -600,7 +603,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           // pi_e^-1 of my z's (linear: XOR of basis images)
           int oidx[R];
           {
-            const uint64_t pv = rr.pinv;
+            const uint64_t pv = PT[rr.var_h & 0xFFu];
             int base = 0;
             if constexpr (TT > 1) {
 #pragma unroll
@@ -624,7 +627,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           if (cvalid) {
             // scatter: X_e(pi_e^-1 z) = U_e(z) = T_e(.); padding teams hold the neutral message
 #pragma unroll
-            for (int r = 0; r < R; ++r) X[oidx[r]] = active ? __uint_as_float(up[r]) : 0.0f;
+            for (int r = 0; r < R; ++r) X[oidx[r]] = __uint_as_float(up[r]);
           }
           check_sync(lc, TPC);
           switch (JPT) {

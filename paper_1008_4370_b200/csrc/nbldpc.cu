@@ -59,6 +59,7 @@ struct nbldpc_code_s {
   EdgeDev* edges_d = nullptr;
   uint8_t* gf_exp_d = nullptr;
   uint8_t* gf_log_d = nullptr;
+  uint64_t* pinv_tab_d = nullptr;
   std::mutex mu;
   Workspace ws;
   // launch geometry of the pass kernel (NBLDPC_VN_DIRECT)
@@ -330,6 +331,7 @@ PassParams make_params(const nbldpc_code_s* c, int step_mode, float* u_out) {  /
   P.code.edges = c->edges_d;
   P.code.gf_exp = c->gf_exp_d;
   P.code.gf_log = c->gf_log_d;
+  P.code.pinv_tab = c->pinv_tab_d;
   P.ws = c->ws.dev;
   P.groups = c->groups;
   P.slot_lanes = c->ws.Y;
@@ -351,6 +353,7 @@ nb::ClusterParams make_cparams(const nbldpc_code_s* c, int step_mode, int step_i
   P.code.edges = c->edges_d;
   P.code.gf_exp = c->gf_exp_d;
   P.code.gf_log = c->gf_log_d;
+  P.code.pinv_tab = c->pinv_tab_d;
   P.ws = c->ws.dev;
   P.chunks = c->p_groups;
   P.checks_per_cta = c->p_cpc;
@@ -654,6 +657,22 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
   if (cudaError_t e = cudaMemcpy(c->edges_d, edges.data(), sizeof(EdgeDev) * E, cudaMemcpyHostToDevice)) return bail(e);
   if (cudaError_t e = cudaMemcpy(c->gf_exp_d, gexp.data(), gexp.size(), cudaMemcpyHostToDevice)) return bail(e);
   if (cudaError_t e = cudaMemcpy(c->gf_log_d, glog.data(), q, cudaMemcpyHostToDevice)) return bail(e);
+  {
+    // pi_h^-1(alpha^i) = pi_{h^-1}(alpha^i): bit j = bit i of h^-1 * alpha^j
+    std::vector<uint64_t> pt(q, 0);
+    for (int h = 1; h < q; ++h) {
+      const int hi = ginv(h);
+      uint64_t v = 0;
+      for (int bi = 0; bi < m; ++bi) {
+        int img = 0;
+        for (int bj = 0; bj < m; ++bj) img |= ((gmul(hi, 1 << bj) >> bi) & 1) << bj;
+        v |= (uint64_t)img << (8 * bi);
+      }
+      pt[h] = v;
+    }
+    if (cudaError_t e = cudaMalloc(&c->pinv_tab_d, sizeof(uint64_t) * q)) return bail(e);
+    if (cudaError_t e = cudaMemcpy(c->pinv_tab_d, pt.data(), sizeof(uint64_t) * q, cudaMemcpyHostToDevice)) return bail(e);
+  }
   // launch geometry: teams of TT threads per edge, k_max teams per check, <= 256 threads per CTA
   c->TT = tt;
   {
@@ -703,7 +722,7 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
     const int kt = tpc / tt;
     c->p_recs = ((c->p_groups + cs - 1) / cs) * c->p_cpc * kt;
     c->p_smem = ((size_t)(c->p_block / tt) * persist_team_words(m) + (size_t)c->p_cpc * q) * sizeof(float) +
-                (size_t)c->p_recs * sizeof(nb::EdgeRec);
+                (size_t)q * sizeof(uint64_t) + (size_t)c->p_recs * sizeof(nb::EdgeRec);
     if (c->p_smem > 227 * 1024) {
       nbldpc_destroy(c);
       return NBLDPC_ERR_UNSUPPORTED;
@@ -749,6 +768,7 @@ void nbldpc_destroy(nbldpc_code_t c) {
   cudaFree(c->edges_d);
   cudaFree(c->gf_exp_d);
   cudaFree(c->gf_log_d);
+  cudaFree(c->pinv_tab_d);
   delete c;
 }
 
