@@ -43,7 +43,7 @@ struct ClusterParams {
 // compact per-edge record kept in shared memory for the CTA's chunks (8 bytes); the Fourier
 // permutation images of h come from a per-field table (CodeDev::pinv_tab, copied to shared memory)
 struct EdgeRec {
-  int32_t partner_a;  // partner edge << 1 | is_a ; -1: padding slot
+  int32_t partner_a;  // partner edge << 9 | h of the partner edge << 1 | is_a ; -1: padding slot
   uint32_t var_h;     // variable << 8 | h_cv
 };
 
@@ -210,6 +210,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   float* const TOT = smem + nteams * C::TEAM + lc * Q;
   uint64_t* const PT = reinterpret_cast<uint64_t*>(smem + nteams * C::TEAM + CPC * Q);  // [q] pi_h^-1 images
   EdgeRec* const recs = reinterpret_cast<EdgeRec*>(PT + Q);
+  uint8_t* const GL = reinterpret_cast<uint8_t*>(recs + P.rec_per_cta);  // [q] log_alpha
+  uint8_t* const GE = GL + Q;                                            // [2q] alpha^i
 
   // TOT(w) gather offsets: thread pck owns WPT w's x JPT teams of its check (R terms, natural X)
   const int SPLIT = KT > R ? KT / R : 1;
@@ -231,13 +233,17 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
     if (c < cd.M && jj < cd.k_max) {
       const EdgeDev* ep = cd.edges + (size_t)c * cd.kpad + jj;
       if (ep->var >= 0) {
-        rr.partner_a = (ep->partner << 1) | (ep->is_a ? 1 : 0);
+        rr.partner_a = (ep->partner << 9) | ((int)cd.edges[ep->partner].h << 1) | (ep->is_a ? 1 : 0);
         rr.var_h = ((uint32_t)ep->var << 8) | ep->h;
       }
     }
     recs[i] = rr;
   }
-  for (int h = tid; h < Q; h += nthr) PT[h] = cd.pinv_tab[h];
+  for (int h = tid; h < Q; h += nthr) {
+    PT[h] = cd.pinv_tab[h];
+    GL[h] = cd.gf_log[h];
+  }
+  for (int i = tid; i < 2 * Q - 1; i += nthr) GE[i] = cd.gf_exp[i < 2 * (Q - 1) + 1 ? i : 0];
   if (tid == 0) {
     sh_flag[0] = 0;
     sh_flag[1] = 0;
@@ -313,7 +319,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           const float* src = Tt + (size_t)rvar * 8;
 #pragma unroll
           for (int bb = 0; bb < MB; ++bb) st[C::QS + bb] = __ldcg(src + bb);
-          const float* sp = Win + (size_t)(rr.partner_a >> 1) * Q;
+          const float* sp = Win + (size_t)(rr.partner_a >> 9) * Q;
 #pragma unroll
           for (int r = 0; r < Q; ++r) st[r] = __ldcg(sp + r);
         } else if (act) {
@@ -321,7 +327,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         }
         mbar_arrive_tx(&sh_mbar[b], tx);
         if (tx) {
-          bulk_g2s(st, Win + (size_t)(rr.partner_a >> 1) * Q, Q * 4, &sh_mbar[b]);
+          bulk_g2s(st, Win + (size_t)(rr.partner_a >> 9) * Q, Q * 4, &sh_mbar[b]);
           bulk_g2s(st + C::QS, Tt + (size_t)rvar * 8, 32, &sh_mbar[b]);
         }
       };
@@ -351,7 +357,15 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         // W_e (own message, for v's decision at its first edge) straight from L2 into registers;
         // consumed after the variable node
         float4 wo4[CH];
+#ifdef NB_DIAG_DEC_NOLOAD
+#pragma unroll
+        for (int ch = 0; ch < CH; ++ch) wo4[ch] = make_float4(0.5f, 0.25f, 0.125f, 1.0f);
+#endif
+#ifdef NB_DIAG_DEC_NOLOAD
+        if (false) {
+#else
         if (is_a && do_dec) {
+#endif
           if constexpr (R >= 4) {
             const float4* so = reinterpret_cast<const float4*>(Win + (size_t)e * Q + t * R);
 #pragma unroll
@@ -528,12 +542,14 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               mf[0] = x[0] * d[0];
             }
           }
+#ifndef NB_DIAG_DEC_NORED
           if constexpr (TT > 1) {
 #pragma unroll
             for (int off = TT / 2; off >= 1; off >>= 1)
 #pragma unroll
               for (int b = 0; b <= MB; ++b) mf[b] += __shfl_xor_sync(0xffffffffu, mf[b], off);
           }
+#endif
           const uint32_t s0z = mf[0] < 0.0f ? 1u : 0u;  // sgn_GF2 M(0); an exact zero has sign 0
           if (is_a && t == 0) {
             int xv = 0;
@@ -541,15 +557,14 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             for (int b = 0; b < MB; ++b) xv |= (int)(((mf[b + 1] < 0.0f) ? 1u : 0u) ^ s0z) << b;
             xout[var] = (uint8_t)xv;
             if (mode == 0) {  // syndrome contributions h_cv xhat_v to both checks of v
-              const EdgeDev* ep = cd.edges + e;
               int ca = 0, cbv = 0;
-              if (xv != 0) {
-                const int lx = __ldg(&cd.gf_log[xv]);
-                ca = __ldg(&cd.gf_exp[ep->logh + lx]);
-                cbv = __ldg(&cd.gf_exp[ep->plogh + lx]);
+              if (xv != 0) {  // shared-memory GF tables: no global round trip on the decision's tail
+                const int lx = GL[xv];
+                ca = GE[GL[rr.var_h & 0xFFu] + lx];
+                cbv = GE[GL[(rr.partner_a >> 1) & 0xFF] + lx];
               }
               con[e] = (uint8_t)ca;
-              con[rr.partner_a >> 1] = (uint8_t)cbv;
+              con[rr.partner_a >> 9] = (uint8_t)cbv;
             }
             if (want_soft) {
               const float l0 = __logf(fabsf(mf[0]));
@@ -562,7 +577,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             uint64_t pa = 0, pbv = 0;
             if (is_a) {
               const uint32_t* ea = reinterpret_cast<const uint32_t*>(cd.edges + e) + 3;
-              const uint32_t* eb = reinterpret_cast<const uint32_t*>(cd.edges + (rr.partner_a >> 1)) + 3;
+              const uint32_t* eb = reinterpret_cast<const uint32_t*>(cd.edges + (rr.partner_a >> 9)) + 3;
               pa = (uint64_t)__ldg(ea) | ((uint64_t)__ldg(ea + 1) << 32);
               pbv = (uint64_t)__ldg(eb) | ((uint64_t)__ldg(eb + 1) << 32);
             }
@@ -593,7 +608,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             }
             if (is_a && t == 0) {
               con[e] = (uint8_t)ma;
-              con[rr.partner_a >> 1] = (uint8_t)mbb;
+              con[rr.partner_a >> 9] = (uint8_t)mbb;
             }
           }
         }

@@ -586,6 +586,7 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
   }
   const int tt = team_threads(m);
   if (k_max * tt > kBigBlock) return NBLDPC_ERR_UNSUPPORTED;
+  if ((long long)M * 64 >= (1ll << 22)) return NBLDPC_ERR_UNSUPPORTED;  // edge slots must fit 22 bits
 
   // internal edge slots: e = c * kpad + j (j-th nonzero of row c in canonical order), kpad the
   // next power of two >= max(4, k_max); the padding slots have var = -1
@@ -722,7 +723,7 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
     const int kt = tpc / tt;
     c->p_recs = ((c->p_groups + cs - 1) / cs) * c->p_cpc * kt;
     c->p_smem = ((size_t)(c->p_block / tt) * persist_team_words(m) + (size_t)c->p_cpc * q) * sizeof(float) +
-                (size_t)q * sizeof(uint64_t) + (size_t)c->p_recs * sizeof(nb::EdgeRec);
+                (size_t)q * sizeof(uint64_t) + (size_t)c->p_recs * sizeof(nb::EdgeRec) + align_up(3 * (size_t)q, 16);
     if (c->p_smem > 227 * 1024) {
       nbldpc_destroy(c);
       return NBLDPC_ERR_UNSUPPORTED;

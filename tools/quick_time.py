@@ -1,6 +1,6 @@
 """Quick timing of decode on one config (development aid, not the bench contract).
 usage: python tools/quick_time.py CFG [frames] [slots] [point] [vn list e.g. 0,1] [graph list e.g. 0,-1]"""
-import sys, json
+import os, sys, json
 import torch
 sys.path.insert(0, '.')
 import synth, paper_1008_4370_b200 as nb
@@ -16,11 +16,12 @@ code = nb.Code(c['m'], c['poly'], M, c['N'], r, co, h)
 llr = torch.from_numpy(synth.config_llr(name, 0, F, point=point)).cuda()
 for vn in vns:
     for g in graphs:
-        out = code.decode(llr, c['max_iters'], slots=slots, use_graph=g, vn_algorithm=vn); torch.cuda.synchronize()
+        es = not os.environ.get('NO_EARLY')
+        out = code.decode(llr, c['max_iters'], slots=slots, use_graph=g, vn_algorithm=vn, early_stop=es); torch.cuda.synchronize()
         ts = []
         for _ in range(3):
             e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-            e0.record(); out = code.decode(llr, c['max_iters'], slots=slots, use_graph=g, vn_algorithm=vn); e1.record()
+            e0.record(); out = code.decode(llr, c['max_iters'], slots=slots, use_graph=g, vn_algorithm=vn, early_stop=es); e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
         it = out['iters'].cpu().numpy(); ok = out['ok'].cpu().numpy()
