@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   constexpr int Q = C::Q, R = C::R, TT = C::TT, LR = C::LR, LJ = C::LJ, CH = C::CH;
   extern __shared__ __align__(16) float smem[];
   __shared__ int sh_frame, sh_flag[2], sh_bad;
-  __shared__ __align__(8) uint64_t sh_mbar[2];  // stage buffers: all teams arrive, bulk copies complete_tx
+  __shared__ __align__(8) uint64_t sh_mbar[16];  // [group][buffer]: the group's teams arrive, bulk copies complete_tx
 
   const CodeDev& cd = P.code;
   const WorkDev& ws = P.ws;
@@ -196,6 +196,19 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   const int CPC = P.checks_per_cta;
   const int KT = TPC / TT;                       // teams per check (incl. padding teams)
   const int nch = ((int)P.chunks - (int)rank + (int)csz - 1) / (int)csz;  // my chunks: rank + k*csz
+  // independent groups of GT = max(32, TPC) threads (a warp, or one check): each runs its own stage
+  // pipeline (mbarriers) over the chunks, so warps of a CTA never wait for one another inside a pass
+  const int GT = TPC > 32 ? TPC : 32;
+  const int ngrp = nthr / GT;
+  const int grp = threadIdx.x / GT;
+  uint64_t* const gmbar = &sh_mbar[2 * grp];
+  auto group_sync = [&]() {
+    if (GT == 32) {
+      __syncwarp();
+    } else {
+      asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(GT) : "memory");
+    }
+  };
 
   // ---- my position in a chunk (fixed)
   const int lc = tid / TPC;
@@ -247,8 +260,10 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   if (tid == 0) {
     sh_flag[0] = 0;
     sh_flag[1] = 0;
-    mbar_init(&sh_mbar[0], (uint32_t)nteams);
-    mbar_init(&sh_mbar[1], (uint32_t)nteams);
+    for (int gg = 0; gg < ngrp; ++gg) {
+      mbar_init(&sh_mbar[2 * gg], (uint32_t)(GT / TT));
+      mbar_init(&sh_mbar[2 * gg + 1], (uint32_t)(GT / TT));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -301,7 +316,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
       const bool do_cn = step || ell < max_iters;
 
       // stage chunk kc into buffer b: partner message, own message (v's first edge), channel terms
-      // stage chunk kc into buffer b (one arrival per team on sh_mbar[b]): the partner message row and
+      // stage chunk kc into buffer b (one arrival per team on gmbar[b]): the partner message row and
       // the channel terms, bulk-copied by the team's first thread (plain loads at l = 0 and for q = 2)
       auto stage = [&](int kc, int b) {
         if (t != 0) return;
@@ -325,10 +340,10 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         } else if (act) {
           tx = Q * 4 + 32;
         }
-        mbar_arrive_tx(&sh_mbar[b], tx);
+        mbar_arrive_tx(&gmbar[b], tx);
         if (tx) {
-          bulk_g2s(st, Win + (size_t)(rr.partner_a >> 9) * Q, Q * 4, &sh_mbar[b]);
-          bulk_g2s(st + C::QS, Tt + (size_t)rvar * 8, 32, &sh_mbar[b]);
+          bulk_g2s(st, Win + (size_t)(rr.partner_a >> 9) * Q, Q * 4, &gmbar[b]);
+          bulk_g2s(st + C::QS, Tt + (size_t)rvar * 8, 32, &gmbar[b]);
         }
       };
 
@@ -337,7 +352,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #pragma unroll 1
       for (int kc = 0; kc < nch; ++kc) {
         if (kc + 1 < nch) stage(kc + 1, buf ^ 1);
-        mbar_wait(&sh_mbar[buf], (mb_parity >> buf) & 1u);
+        mbar_wait(&gmbar[buf], (mb_parity >> buf) & 1u);
         mb_parity ^= 1u << buf;
 
         const int c = ((int)rank + kc * (int)csz) * CPC + lc;
@@ -690,7 +705,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         }
         // generic-proxy writes to this stage buffer (DB) are ordered before its next bulk fill
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();  // buffers of this chunk are free
+        group_sync();  // the group's buffers of this chunk are free
         buf ^= 1;
       }
       cp_async_wait<0>();
