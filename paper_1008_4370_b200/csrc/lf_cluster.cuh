@@ -63,7 +63,7 @@ struct CCfg {
   static constexpr int TEAM0 = 2 * STG + XS;
   // team stride = 4 s (mod 32) words with s = 1 (TT = 1) or 8 / TT: the 8 threads of every quarter
   // warp then hit 8 distinct bank quads in the 128-bit stage / transposition accesses
-  static constexpr int SQ = TT == 1 ? 1 : (TT <= 8 ? 8 / TT : 0);
+  static constexpr int SQ = TT == 1 ? 1 : (TT <= 8 ? 8 / TT : 4);  // TT = 16: two teams per warp
   static constexpr int TEAM = TEAM0 + (((4 * SQ) - TEAM0 % 32) + 64) % 32;
   static constexpr bool BULK = Q >= 4;  // message rows are whole 16-byte chunks: bulk-copied
 };
@@ -99,6 +99,44 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(mb))
                : "memory");
+}
+
+// decision buffer: row tb (16 floats) holds D at the phase-B coordinates (tb, rb); its 16-byte chunks
+// are XOR-swizzled by (tb >> 1) & 3 so that 8 consecutive rows read in one LDS.128 hit 8 bank quads
+__device__ __forceinline__ int db_word(int tb, int rb) { return 16 * tb + ((((rb >> 2) ^ (tb >> 1)) & 3) << 2) + (rb & 3); }
+
+// Sum NV per-lane values over the TT lanes of a team by recursive halving (reduce-scatter): each level
+// exchanges half of the remaining slots with the partner lane.  Returns the OR over the team of
+// [total < 0] << index; lane-local slot k then holds the total of value index off + k (k < nfin).
+template <int NV, int TT>
+__device__ __forceinline__ uint32_t team_sign_bits(float (&v)[NV], int lane, int& off, int& nfin) {
+  int n = NV, nv = NV;  // n: slots (compile-time sequence), nv: this lane's slots holding real values
+  off = 0;
+#pragma unroll
+  for (int o = TT / 2; o >= 1; o >>= 1) {
+    const int h = (n + 1) / 2;
+    const bool upper = (lane & o) != 0;
+    nv = upper ? (nv > h ? nv - h : 0) : (nv < h ? nv : h);
+#pragma unroll
+    for (int k = 0; k < (NV + 1) / 2; ++k) {
+      if (k < h) {
+        const float lo = v[k];
+        const float hi = (h + k < n) ? v[h + k] : 0.0f;
+        const float send = upper ? lo : hi;
+        const float keep = upper ? hi : lo;
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    if (upper) off += h;
+    n = h;
+  }
+  nfin = nv;
+  uint32_t bits = 0;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+    if (k < n && k < nv && v[k] < 0.0f) bits |= 1u << (off + k);
+  const unsigned tmask = (TT >= 32) ? 0xffffffffu : (((1u << TT) - 1u) << (lane & ~(TT - 1) & 31));
+  return __reduce_or_sync(tmask, bits);
 }
 
 template <int CH>
@@ -500,7 +538,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #pragma unroll
                 for (int k4 = 0; k4 < 4; ++k4) {
                   const int w = 4 * ch + k4;  // z = 16 t + w: tB = w >> LJ, rB = (w & (2^LJ - 1)) | t << LJ
-                  DB[16 * (w >> LJ) + (w & ((1 << LJ) - 1)) + (t << LJ)] = d4[k4];
+                  DB[db_word(w >> LJ, (w & ((1 << LJ) - 1)) | (t << LJ))] = d4[k4];
                 }
               }
             } else if constexpr (R >= 4) {
@@ -523,8 +561,16 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             // pairwise FFMA2 dot products: M(0) and the register-bit points in-thread, the
             // thread-bit points against the partner thread's row
             float d[R];
+            if constexpr (TT > 1) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) d[r] = DB[16 * t + r];
+              for (int ch = 0; ch < 4; ++ch) {
+                const float4 v4 = *reinterpret_cast<const float4*>(DB + db_word(t, 4 * ch));
+                d[4 * ch] = v4.x; d[4 * ch + 1] = v4.y; d[4 * ch + 2] = v4.z; d[4 * ch + 3] = v4.w;
+              }
+            } else {
+#pragma unroll
+              for (int r = 0; r < R; ++r) d[r] = DB[r];
+            }
             if constexpr (R >= 2) {
               float2 acc[MB + 1];
 #pragma unroll
@@ -544,11 +590,15 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               if constexpr (TT > 1) {
 #pragma unroll
                 for (int b = 0; b < MB - 4; ++b) {
-                  const float* row = DB + 16 * (t ^ (1 << b));
+                  const int tp = t ^ (1 << b);
 #pragma unroll
-                  for (int p = 0; p < R / 2; ++p)
-                    acc[LJ + b + 1] = __ffma2_rn(make_float2(x[2 * p], x[2 * p + 1]),
-                                                 make_float2(row[2 * p], row[2 * p + 1]), acc[LJ + b + 1]);
+                  for (int ch = 0; ch < 4; ++ch) {
+                    const float4 v4 = *reinterpret_cast<const float4*>(DB + db_word(tp, 4 * ch));
+                    acc[LJ + b + 1] = __ffma2_rn(make_float2(x[4 * ch], x[4 * ch + 1]), make_float2(v4.x, v4.y),
+                                                 acc[LJ + b + 1]);
+                    acc[LJ + b + 1] = __ffma2_rn(make_float2(x[4 * ch + 2], x[4 * ch + 3]), make_float2(v4.z, v4.w),
+                                                 acc[LJ + b + 1]);
+                  }
                 }
               }
 #pragma unroll
@@ -557,19 +607,49 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               mf[0] = x[0] * d[0];
             }
           }
-#ifndef NB_DIAG_DEC_NORED
-          if constexpr (TT > 1) {
+          // signs of M(0) and M(alpha^i) over the team (bit i of sbits = [M(.) < 0], index 0 = M(0))
+          uint32_t sbits;
+          int s_off = 0, s_n = MB + 1;
+#ifndef NB_RS_MIN_TT
+#define NB_RS_MIN_TT 8
+#endif
+          if constexpr (TT >= NB_RS_MIN_TT) {
+            sbits = team_sign_bits<MB + 1, TT>(mf, lane, s_off, s_n);
+          } else if constexpr (TT > 1) {  // small teams: full butterfly all-reduce, every lane holds all totals
 #pragma unroll
             for (int off = TT / 2; off >= 1; off >>= 1)
 #pragma unroll
               for (int b = 0; b <= MB; ++b) mf[b] += __shfl_xor_sync(0xffffffffu, mf[b], off);
-          }
-#endif
-          const uint32_t s0z = mf[0] < 0.0f ? 1u : 0u;  // sgn_GF2 M(0); an exact zero has sign 0
-          if (is_a && t == 0) {
-            int xv = 0;
+            sbits = 0;
 #pragma unroll
-            for (int b = 0; b < MB; ++b) xv |= (int)(((mf[b + 1] < 0.0f) ? 1u : 0u) ^ s0z) << b;
+            for (int b = 0; b <= MB; ++b) sbits |= (mf[b] < 0.0f ? 1u : 0u) << b;
+          } else {
+            sbits = 0;
+#pragma unroll
+            for (int b = 0; b <= MB; ++b) sbits |= (mf[b] < 0.0f ? 1u : 0u) << b;
+          }
+          const uint32_t s0z = sbits & 1u;  // sgn_GF2 M(0); an exact zero has sign 0
+          if (want_soft && is_a) {
+            // soft output: the team's totals through the consumed stage buffer (rare path)
+            if constexpr (TT >= NB_RS_MIN_TT) {
+              __syncwarp(__activemask());
+#pragma unroll
+              for (int k = 0; k <= MB; ++k)
+                if (k < s_n && s_off + k <= MB) DB[s_off + k] = mf[k];
+              __syncwarp(__activemask());
+              if (t == 0) {
+#pragma unroll
+                for (int b = 0; b <= MB; ++b) mf[b] = DB[b];
+              }
+            }
+            if (t == 0) {
+              const float l0 = __logf(fabsf(mf[0]));
+#pragma unroll
+              for (int b = 0; b < MB; ++b) sout[(size_t)var * MB + b] = __logf(fabsf(mf[b + 1])) - l0;
+            }
+          }
+          if (is_a && t == 0) {
+            const int xv = (int)(((sbits >> 1) ^ (s0z ? 0xFFu : 0u)) & ((1u << MB) - 1u));
             xout[var] = (uint8_t)xv;
             if (mode == 0) {  // syndrome contributions h_cv xhat_v to both checks of v
               int ca = 0, cbv = 0;
@@ -580,11 +660,6 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               }
               con[e] = (uint8_t)ca;
               con[rr.partner_a >> 9] = (uint8_t)cbv;
-            }
-            if (want_soft) {
-              const float l0 = __logf(fabsf(mf[0]));
-#pragma unroll
-              for (int b = 0; b < MB; ++b) sout[(size_t)var * MB + b] = __logf(fabsf(mf[b + 1])) - l0;
             }
           }
           if (mode == 1) {
@@ -607,7 +682,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
                   const int yy = zr[r] ^ z;
                   int w;
                   if constexpr (TT > 1) {
-                    w = 16 * ((yy >> LJ) & (TT - 1)) + ((yy & ((1 << LJ) - 1)) | ((yy >> 4) << LJ));
+                    w = db_word((yy >> LJ) & (TT - 1), (yy & ((1 << LJ) - 1)) | ((yy >> 4) << LJ));
                   } else {
                     w = yy;
                   }
