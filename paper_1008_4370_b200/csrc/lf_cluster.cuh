@@ -59,8 +59,9 @@ struct CCfg {
   // per-team shared memory (floats): stage buffers [2] x (Wp q | th 8), X (transposition / scatter)
   static constexpr int QS = Q < 4 ? 4 : Q;          // th at a 16-byte boundary
   static constexpr int STG = QS + 8;
-  static constexpr int XS = TT > 1 ? Q + Q / 4 : Q;
-  static constexpr int TEAM0 = 2 * STG + XS;
+  // the consumed stage buffer of the chunk doubles as the transposition buffer, the decision buffer
+  // and the check node's scatter target (in that order), so a team needs just the two stage buffers
+  static constexpr int TEAM0 = 2 * STG;
   // team stride = 4 s (mod 32) words with s = 1 (TT = 1) or 8 / TT: the 8 threads of every quarter
   // warp then hit 8 distinct bank quads in the 128-bit stage / transposition accesses
   static constexpr int SQ = TT == 1 ? 1 : (TT <= 8 ? 8 / TT : 4);  // TT = 16: two teams per warp
@@ -99,6 +100,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(mb))
                : "memory");
+}
+
+// transposition layout: 16-byte chunk c of block b at chunk c ^ ((b ^ (b >> 2)) & 3): the phase-A
+// 128-bit stores (8 threads per quarter warp) and the phase-B reads are bank-conflict free
+__device__ __forceinline__ int tpos(int z) {
+  return (z & ~15) | ((((z >> 2) ^ (z >> 4) ^ (z >> 6)) & 3) << 2) | (z & 3);
 }
 
 // decision buffer: row tb (16 floats) holds D at the phase-B coordinates (tb, rb); its 16-byte chunks
@@ -257,7 +264,6 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   const int team = tid / TT;
   const int nteams = nthr / TT;
   float* const TB = smem + team * C::TEAM;  // STG[0] | STG[1] | X
-  float* const X = TB + 2 * C::STG;
   float* const TOT = smem + nteams * C::TEAM + lc * Q;
   uint64_t* const PT = reinterpret_cast<uint64_t*>(smem + nteams * C::TEAM + CPC * Q);  // [q] pi_h^-1 images
   EdgeRec* const recs = reinterpret_cast<EdgeRec*>(PT + Q);
@@ -269,7 +275,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   const int JPT = KT / SPLIT;
   const int wgrp = pck / SPLIT;
   const int jbase = (pck % SPLIT) * JPT;
-  const int gbase = in_check ? (lc * KT + jbase) * C::TEAM + 2 * C::STG + wgrp : 0;
+  const int gbase = in_check ? (lc * KT + jbase) * C::TEAM + wgrp : 0;  // + buf * STG per chunk
   // my phase-B z's
   int zr[R];
 #pragma unroll
@@ -467,14 +473,15 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           }
           bfly_regs<R, 0, LR>(x, th);  // z bits 0..LR-1
           if constexpr (TT > 1) {
-            // transposition through X (padded layout idx(z) = z + 4 (z >> 4))
+            // transposition through the consumed stage buffer, chunk-swizzled layout tpos(z)
+            __syncwarp();  // every thread of the team has read its phase-A chunks
 #pragma unroll
             for (int ch = 0; ch < 4; ++ch)
-              *reinterpret_cast<float4*>(X + 20 * t + 4 * ch) = make_float4(x[4 * ch], x[4 * ch + 1], x[4 * ch + 2], x[4 * ch + 3]);
+              *reinterpret_cast<float4*>(st + tpos(16 * t + 4 * ch)) = make_float4(x[4 * ch], x[4 * ch + 1], x[4 * ch + 2], x[4 * ch + 3]);
             __syncwarp();
 #pragma unroll
             for (int h = 0; h < TT; ++h) {
-              const float* src = X + ((t << LJ) | (h << 4)) + 4 * h;
+              const float* src = st + tpos((t << LJ) | (h << 4));
               if constexpr (LJ == 0) {
                 x[h] = src[0];
               } else if constexpr (LJ == 1) {
@@ -483,7 +490,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               } else {
 #pragma unroll
                 for (int q4 = 0; q4 < (1 << LJ) / 4; ++q4) {
-                  const float4 v = *reinterpret_cast<const float4*>(src + 4 * q4);
+                  const float4 v = *reinterpret_cast<const float4*>(st + tpos(((t << LJ) | (h << 4)) + 4 * q4));
                   x[(h << LJ) + 4 * q4] = v.x; x[(h << LJ) + 4 * q4 + 1] = v.y;
                   x[(h << LJ) + 4 * q4 + 2] = v.z; x[(h << LJ) + 4 * q4 + 3] = v.w;
                 }
@@ -529,6 +536,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         if (do_dec) {
           // D = Gamma^-1(W_e) in the row layout word(z) = 16 tB(z) + rB(z), over the consumed Wp
           float* DB = st;
+          if constexpr (TT > 1) __syncwarp();  // transposition reads done
           if (is_a) {
             if constexpr (TT > 1) {
 #pragma unroll
@@ -732,15 +740,15 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           if (cvalid) {
             // scatter: X_e(pi_e^-1 z) = U_e(z) = T_e(.); padding teams hold the neutral message
 #pragma unroll
-            for (int r = 0; r < R; ++r) X[oidx[r]] = __uint_as_float(up[r]);
+            for (int r = 0; r < R; ++r) st[oidx[r]] = __uint_as_float(up[r]);
           }
           check_sync(lc, TPC);
           switch (JPT) {
-            case 1: tot_sum<R, 1, TT, C::TEAM>(smem, gbase, TOT, wgrp, SPLIT, pck, cvalid); break;
-            case 2: tot_sum<R, (R >= 2 ? 2 : 1), TT, C::TEAM>(smem, gbase, TOT, wgrp, SPLIT, pck, cvalid); break;
-            case 4: tot_sum<R, (R >= 4 ? 4 : 1), TT, C::TEAM>(smem, gbase, TOT, wgrp, SPLIT, pck, cvalid); break;
-            case 8: tot_sum<R, (R >= 8 ? 8 : 1), TT, C::TEAM>(smem, gbase, TOT, wgrp, SPLIT, pck, cvalid); break;
-            default: tot_sum<R, R, TT, C::TEAM>(smem, gbase, TOT, wgrp, SPLIT, pck, cvalid); break;
+            case 1: tot_sum<R, 1, TT, C::TEAM>(smem, gbase + buf * C::STG, TOT, wgrp, SPLIT, pck, cvalid); break;
+            case 2: tot_sum<R, (R >= 2 ? 2 : 1), TT, C::TEAM>(smem, gbase + buf * C::STG, TOT, wgrp, SPLIT, pck, cvalid); break;
+            case 4: tot_sum<R, (R >= 4 ? 4 : 1), TT, C::TEAM>(smem, gbase + buf * C::STG, TOT, wgrp, SPLIT, pck, cvalid); break;
+            case 8: tot_sum<R, (R >= 8 ? 8 : 1), TT, C::TEAM>(smem, gbase + buf * C::STG, TOT, wgrp, SPLIT, pck, cvalid); break;
+            default: tot_sum<R, R, TT, C::TEAM>(smem, gbase + buf * C::STG, TOT, wgrp, SPLIT, pck, cvalid); break;
           }
           check_sync(lc, TPC);
           if (active) {
