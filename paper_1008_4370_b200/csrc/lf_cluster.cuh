@@ -350,6 +350,17 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
     float* const sout = step ? ws.soft + (size_t)f * cd.N * MB : call->soft_out + (size_t)f * cd.N * MB;
     float* const Tt = ws.Tt + (size_t)slot * cd.N * 8;
     uint8_t* const con = ws.con + (size_t)slot * ws.con_stride;
+    if (!step) {
+      // channel terms of the frame, computed once and cooperatively by the cluster's CTAs:
+      // Tt[v][i] = tanh(L_{v,i} / 2), the factors of P_v^0 = (x)_i (1, t_i)
+      const float* lf = call->llr + (size_t)f * cd.N * MB;
+      for (int i = (int)rank * nthr + tid; i < cd.N * MB; i += (int)csz * nthr) {
+        const int v = i / MB;
+        Tt[(size_t)v * 8 + (i - v * MB)] = tanhf(0.5f * __ldg(lf + i));
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // read next by bulk copies (async proxy)
+      cluster_sync_all();
+    }
 
 #pragma unroll 1
     for (int ell = step ? P.step_iter : 0;; ++ell) {
@@ -370,11 +381,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         if (in_check) rr = recs[(kc * CPC + lc) * KT + j];
         const bool act = in_check && rr.partner_a >= 0;
         const int rvar = (int)(rr.var_h >> 8);
-        if (act && ell == 0) {
-          const float* src = call->llr + ((size_t)f * cd.N + rvar) * MB;
-#pragma unroll
-          for (int bb = 0; bb < MB; ++bb) st[C::QS + bb] = __ldg(src + bb);
-        } else if (act && !C::BULK) {
+        if (act && !C::BULK) {
           const float* src = Tt + (size_t)rvar * 8;
 #pragma unroll
           for (int bb = 0; bb < MB; ++bb) st[C::QS + bb] = __ldcg(src + bb);
@@ -382,11 +389,11 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #pragma unroll
           for (int r = 0; r < Q; ++r) st[r] = __ldcg(sp + r);
         } else if (act) {
-          tx = Q * 4 + 32;
+          tx = (ell == 0 ? 0 : Q * 4) + 32;
         }
         mbar_arrive_tx(&gmbar[b], tx);
         if (tx) {
-          bulk_g2s(st, Win + (size_t)(rr.partner_a >> 9) * Q, Q * 4, &gmbar[b]);
+          if (ell != 0) bulk_g2s(st, Win + (size_t)(rr.partner_a >> 9) * Q, Q * 4, &gmbar[b]);
           bulk_g2s(st + C::QS, Tt + (size_t)rvar * 8, 32, &gmbar[b]);
         }
       };
@@ -432,14 +439,6 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           } else {
             const float2 v2 = __ldcg(reinterpret_cast<const float2*>(Win + (size_t)e * Q));
             wo4[0] = make_float4(v2.x, v2.y, 0.f, 0.f);
-          }
-        }
-        if (ell == 0 && active) {
-#pragma unroll
-          for (int b = 0; b < MB; ++b) th[b] = tanhf(0.5f * th[b]);
-          if (is_a && t == 0 && !step) {
-#pragma unroll
-            for (int b = 0; b < MB; ++b) Tt[(size_t)var * 8 + b] = th[b];
           }
         }
 
@@ -795,6 +794,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
       if (step) break;
 
       // ---- end of the pass: stopping rule, cluster-uniform
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // W_out is read next by bulk copies
       cluster_sync_all();  // every message, estimate and syndrome byte of the pass is written
       if (tid == 0) sh_bad = 0;
       __syncthreads();

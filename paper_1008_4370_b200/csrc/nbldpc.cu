@@ -714,7 +714,9 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
     // cluster size: the largest divisor of the chunk count that is <= 8 (portable clusters)
     // small clusters measured fastest (fewer CTAs per barrier, more chunks per CTA per iteration):
     // 2 CTAs per frame when the chunk count is even
+    // (measured: C2/C3/C4 fastest at 2, the one-thread-per-edge q <= 16 path at 4)
     int cs = c->p_groups % 2 == 0 ? 2 : 1;
+    if (tt == 1 && c->p_groups % 4 == 0) cs = 4;
     if (const char* env = getenv("NBLDPC_CLUSTER_SIZE")) {  // tuning override (a divisor of the chunk count)
       const int v = atoi(env);
       if (v >= 1 && v <= 16 && c->p_groups % v == 0) cs = v;
@@ -891,10 +893,8 @@ nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int i
   call.want_soft = soft != nullptr;
   nb::nb_step_setup_kernel<<<(frames + 255) / 256, 256, 0, st>>>(w.dev, call, iter);
   NB_TRY(cudaGetLastError());
-  if (iter >= 1) {
-    nb::nb_tanh_kernel<<<256, 256, 0, st>>>(llr, w.dev.Tt, (size_t)frames * c->N, c->m);
-    NB_TRY(cudaGetLastError());
-  }
+  nb::nb_tanh_kernel<<<256, 256, 0, st>>>(llr, w.dev.Tt, (size_t)frames * c->N, c->m);
+  NB_TRY(cudaGetLastError());
   // the direct pass kernel selects buffers by iteration parity, the persistent one by epoch (0)
   const int in_buf = vn_algorithm ? (iter & 1) : 0;
   float* wcur = w.dev.W + (size_t)in_buf * frames * c->E * c->q;
