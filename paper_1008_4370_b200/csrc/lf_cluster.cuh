@@ -56,28 +56,37 @@ struct CCfg {
   static constexpr int LJ = MB >= 4 ? 8 - MB : 0;   // phase-B low register bits (TT > 1)
   static constexpr int V = 1 << LJ;                 // phase-B contiguous run (floats)
   static constexpr int CH = R >= 4 ? R / 4 : 1;     // 16-byte chunks per thread
-  // per-team shared memory (floats): stage buffers [2] x (Wp q | th 8), X (transposition / scatter)
-  static constexpr int QS = Q < 4 ? 4 : Q;          // th at a 16-byte boundary
-  static constexpr int STG = QS + 8;
-  // the consumed stage buffer of the chunk doubles as the transposition buffer, the decision buffer
-  // and the check node's scatter target (in that order), so a team needs just the two stage buffers
-  static constexpr int TEAM0 = 2 * STG;
-  // team stride = 4 s (mod 32) words with s = 1 (TT = 1) or 8 / TT: the 8 threads of every quarter
-  // warp then hit 8 distinct bank quads in the 128-bit stage / transposition accesses
-  static constexpr int SQ = TT == 1 ? 1 : (TT <= 8 ? 8 / TT : 4);  // TT = 16: two teams per warp
-  static constexpr int TEAM = TEAM0 + (((4 * SQ) - TEAM0 % 32) + 64) % 32;
+  static constexpr int QS = Q < 4 ? 4 : Q;          // row stride (floats) of a staged message
   static constexpr bool BULK = Q >= 4;  // message rows are whole 16-byte chunks: bulk-copied
   // channel-term row: prefetched into registers for one- or two-thread teams (measured: C5 651 -> 546
-  // ns per frame-iteration), bulk-copied with the partner row for wider teams (C3 902 vs 1017 ns)
-  static constexpr bool THREG = TT <= 2;
+  // ns per frame-iteration), bulk-copied beside the message rows for wider teams (C3 902 vs 1017 ns)
+#ifndef NB_THREG_MAX_TT
+#define NB_THREG_MAX_TT 2
+#endif
+  static constexpr bool THREG = TT <= NB_THREG_MAX_TT;
+  static constexpr int THW = THREG ? 0 : 8;          // channel-term floats per team and stage buffer
+  // shared memory per team (floats): message row x 2 stage buffers (+ channel terms x 2); the consumed
+  // row doubles as the transposition buffer, the decision buffer and the check node's scatter target
+  static constexpr int TEAMW = 2 * QS + 2 * THW;
 };
 
-// Global position of message entry z (TT > 1): the 16-byte chunk c of the 16-entry block b is stored
-// at chunk c ^ (b & 3), so that the phase-A reads of a bulk-copied row are bank-conflict free.
+// Message storage ("reader-ordered rows"): row r holds the message CONSUMED by edge slot r, i.e. the
+// check-to-variable message of r's partner edge, so that a chunk's variable-node inputs are one
+// contiguous block (one bulk copy per group).  Entry z of row r sits at mpos(z, r): the 16-byte chunks
+// are XOR-swizzled by the block index and by low row bits, so that the phase-A reads of the staged
+// rows (rows at a stride of q floats) are bank-conflict free.
 template <int MB>
-__host__ __device__ __forceinline__ int gpos(int z) {
+__host__ __device__ __forceinline__ int mpos(int z, int row) {
+  constexpr int Q = 1 << MB;
   if constexpr (MB >= 5) {
-    return (z & ~15) | ((((z >> 2) & 3) ^ ((z >> 4) & 3)) << 2) | (z & 3);
+    constexpr int TT = Q / 16;
+    const int b = z >> 4, c = (z >> 2) & 3;
+    const int f = TT <= 4 ? (row & (8 / TT - 1)) : 0;
+    return (b << 4) | (((c ^ b ^ (b >> 2) ^ f) & 3) << 2) | (z & 3);
+  } else if constexpr (MB >= 2) {
+    constexpr int CH = Q / 4;                           // chunks per row (1, 2, 4)
+    const int key = (row / (8 / CH)) & (CH - 1);
+    return ((((z >> 2) ^ key) & (CH - 1)) << 2) | (z & 3);
   } else {
     return z;
   }
@@ -266,9 +275,15 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   const bool in_check = lc < CPC;
   const int team = tid / TT;
   const int nteams = nthr / TT;
-  float* const TB = smem + team * C::TEAM;  // STG[0] | STG[1] | X
-  float* const TOT = smem + nteams * C::TEAM + lc * Q;
-  uint64_t* const PT = reinterpret_cast<uint64_t*>(smem + nteams * C::TEAM + CPC * Q);  // [q] pi_h^-1 images
+  // shared memory: per group [2 stage buffers][GT/TT team rows][QS] | TH [2][nteams][8] | TOT | PT | ...
+  const int TG = GT / TT;                        // teams per group
+  const int CPG = GT / TPC;                      // checks per group
+  const int GBLK = TG * C::QS;                   // one stage buffer of a group (floats)
+  float* const GST = smem + grp * 2 * GBLK;      // the group's stage buffers
+  const int trow = team - grp * TG;              // my team's row within a group stage buffer
+  float* const THB = smem + nteams * 2 * C::QS + team * 8;  // + b * nteams * 8 (wide teams only)
+  float* const TOT = smem + nteams * C::TEAMW + lc * Q;
+  uint64_t* const PT = reinterpret_cast<uint64_t*>(smem + nteams * C::TEAMW + CPC * Q);  // [q] pi_h^-1 images
   EdgeRec* const recs = reinterpret_cast<EdgeRec*>(PT + Q);
   uint8_t* const GL = reinterpret_cast<uint8_t*>(recs + P.rec_per_cta);  // [q] log_alpha
   uint8_t* const GE = GL + Q;                                            // [2q] alpha^i
@@ -278,7 +293,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   const int JPT = KT / SPLIT;
   const int wgrp = pck / SPLIT;
   const int jbase = (pck % SPLIT) * JPT;
-  const int gbase = in_check ? (lc * KT + jbase) * C::TEAM + wgrp : 0;  // + buf * STG per chunk
+  const int gbase = in_check ? (int)(GST - smem) + ((lc - grp * CPG) * KT + jbase) * C::QS + wgrp : 0;  // + buf * GBLK
   // my phase-B z's
   int zr[R];
 #pragma unroll
@@ -373,32 +388,37 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
       const bool do_dec = ell >= 1;
       const bool do_cn = step || ell < max_iters;
 
-      // stage chunk kc into buffer b: partner message, own message (v's first edge), channel terms
-      // stage chunk kc into buffer b (one arrival per team on gmbar[b]): the partner message row and
-      // the channel terms, bulk-copied by the team's first thread (plain loads at l = 0 and for q = 2)
+      // stage chunk kc into buffer b of my group (one arrival per team on gmbar[b]): the group leader
+      // bulk-copies the group's block of message rows (contiguous: reader-ordered storage), wide teams
+      // bulk-copy their channel-term row; plain loads for q = 2
       auto stage = [&](int kc, int b) {
         if (t != 0) return;
-        float* st = TB + b * C::STG;
         uint32_t tx = 0;
         EdgeRec rr{-1, 0};
         if (in_check) rr = recs[(kc * CPC + lc) * KT + j];
         const bool act = in_check && rr.partner_a >= 0;
+        const int cg0 = ((int)rank + kc * (int)csz) * CPC + grp * CPG;  // the group's first check
+        const bool lead = (tid - grp * GT) == 0;
+        uint32_t blk = 0;
+        if (lead && C::BULK && ell != 0 && cg0 < cd.M)
+          blk = (uint32_t)((cd.M - cg0 < CPG ? cd.M - cg0 : CPG) * cd.kpad * Q * 4);
         if (act && !C::BULK && ell != 0) {
-          const float* sp = Win + (size_t)(rr.partner_a >> 9) * Q;
+          const float* sp = Win + ((size_t)((((int)rank + kc * (int)csz) * CPC + lc) * cd.kpad + j)) * Q;
+          float* dst = GST + b * GBLK + trow * C::QS;
 #pragma unroll
-          for (int r = 0; r < Q; ++r) st[r] = __ldcg(sp + r);
-        } else if (act && !C::BULK && !C::THREG) {
-          const float* src = Tt + (size_t)(rr.var_h >> 8) * 8;
-#pragma unroll
-          for (int bb = 0; bb < MB; ++bb) st[C::QS + bb] = __ldcg(src + bb);
-        } else if (act) {
-          tx = (ell != 0 ? Q * 4 : 0) + (C::THREG ? 0 : 32);
+          for (int r = 0; r < Q; ++r) dst[r] = __ldcg(sp + r);
         }
+        if (act && !C::THREG) tx += 32;
+        tx += blk;
         mbar_arrive_tx(&gmbar[b], tx);
-        if (tx) {
-          if (ell != 0) bulk_g2s(st, Win + (size_t)(rr.partner_a >> 9) * Q, Q * 4, &gmbar[b]);
-          if (!C::THREG) bulk_g2s(st + C::QS, Tt + (size_t)(rr.var_h >> 8) * 8, 32, &gmbar[b]);
-        }
+        // the block in pieces of <= NB_BLK_PIECE bytes (several TMA transfers in flight)
+#ifndef NB_BLK_PIECE
+#define NB_BLK_PIECE 2048
+#endif
+        for (uint32_t o = 0; o < blk; o += NB_BLK_PIECE)
+          bulk_g2s(GST + b * GBLK + o / 4, Win + (size_t)cg0 * cd.kpad * Q + o / 4,
+                   blk - o < NB_BLK_PIECE ? blk - o : NB_BLK_PIECE, &gmbar[b]);
+        if (act && !C::THREG) bulk_g2s(THB + b * nteams * 8, Tt + (size_t)(rr.var_h >> 8) * 8, 32, &gmbar[b]);
       };
       // channel-term row of chunk kc's variable, prefetched into registers one chunk ahead
       auto th_load = [&](int kc, float4 (&dst)[2]) {
@@ -432,14 +452,14 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         const bool is_a = active && (rr.partner_a & 1);
         const int e = c * cd.kpad + j;
         const int var = (int)(rr.var_h >> 8);
-        float* st = TB + buf * C::STG;
+        float* st = GST + buf * GBLK + trow * C::QS;  // my row: the message consumed by edge e
 
         // ---- channel terms t_i = tanh(L_i / 2)
         float th[MB];
         {
           const float tv[8] = {thc[0].x, thc[0].y, thc[0].z, thc[0].w, thc[1].x, thc[1].y, thc[1].z, thc[1].w};
 #pragma unroll
-          for (int b = 0; b < MB; ++b) th[b] = active ? (C::THREG ? tv[b] : st[C::QS + b]) : 0.0f;
+          for (int b = 0; b < MB; ++b) th[b] = active ? (C::THREG ? tv[b] : THB[buf * nteams * 8 + b]) : 0.0f;
         }
         // W_e (own message, for v's decision at its first edge) straight from L2 into registers;
         // consumed after the variable node
@@ -453,12 +473,13 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #else
         if (is_a && do_dec) {
 #endif
+          const int prow = rr.partner_a >> 9;  // W_e is stored in the row its reader (the partner edge) consumes
           if constexpr (R >= 4) {
-            const float4* so = reinterpret_cast<const float4*>(Win + (size_t)e * Q + t * R);
+            const float* so = Win + (size_t)prow * Q;
 #pragma unroll
-            for (int ch = 0; ch < CH; ++ch) wo4[ch] = __ldcg(so + (TT > 1 ? cswz<CH>(ch, t) : ch));
+            for (int ch = 0; ch < CH; ++ch) wo4[ch] = __ldcg(reinterpret_cast<const float4*>(so + mpos<MB>(t * R + 4 * ch, prow)));
           } else {
-            const float2 v2 = __ldcg(reinterpret_cast<const float2*>(Win + (size_t)e * Q));
+            const float2 v2 = __ldcg(reinterpret_cast<const float2*>(Win + (size_t)prow * Q));
             wo4[0] = make_float4(v2.x, v2.y, 0.f, 0.f);
           }
         }
@@ -481,10 +502,9 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           }
         } else {
           if constexpr (R >= 4) {
-            const int key = TT > 1 ? t : 0;  // global chunk swizzle gpos (TT > 1)
 #pragma unroll
             for (int ch = 0; ch < CH; ++ch) {
-              const float4 v = *reinterpret_cast<const float4*>(st + t * R + 4 * cswz<CH>(ch, key));
+              const float4 v = *reinterpret_cast<const float4*>(st + mpos<MB>(t * R + 4 * ch, e));
               x[4 * ch] = to_lin(v.x); x[4 * ch + 1] = to_lin(v.y); x[4 * ch + 2] = to_lin(v.z); x[4 * ch + 3] = to_lin(v.w);
             }
           } else {
@@ -763,11 +783,11 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           }
           check_sync(lc, TPC);
           switch (JPT) {
-            case 1: tot_sum<R, 1, TT, C::TEAM>(smem, gbase + buf * C::STG, TOT, wgrp, SPLIT, pck, cvalid); break;
-            case 2: tot_sum<R, (R >= 2 ? 2 : 1), TT, C::TEAM>(smem, gbase + buf * C::STG, TOT, wgrp, SPLIT, pck, cvalid); break;
-            case 4: tot_sum<R, (R >= 4 ? 4 : 1), TT, C::TEAM>(smem, gbase + buf * C::STG, TOT, wgrp, SPLIT, pck, cvalid); break;
-            case 8: tot_sum<R, (R >= 8 ? 8 : 1), TT, C::TEAM>(smem, gbase + buf * C::STG, TOT, wgrp, SPLIT, pck, cvalid); break;
-            default: tot_sum<R, R, TT, C::TEAM>(smem, gbase + buf * C::STG, TOT, wgrp, SPLIT, pck, cvalid); break;
+            case 1: tot_sum<R, 1, TT, C::QS>(smem, gbase + buf * GBLK, TOT, wgrp, SPLIT, pck, cvalid); break;
+            case 2: tot_sum<R, (R >= 2 ? 2 : 1), TT, C::QS>(smem, gbase + buf * GBLK, TOT, wgrp, SPLIT, pck, cvalid); break;
+            case 4: tot_sum<R, (R >= 4 ? 4 : 1), TT, C::QS>(smem, gbase + buf * GBLK, TOT, wgrp, SPLIT, pck, cvalid); break;
+            case 8: tot_sum<R, (R >= 8 ? 8 : 1), TT, C::QS>(smem, gbase + buf * GBLK, TOT, wgrp, SPLIT, pck, cvalid); break;
+            default: tot_sum<R, R, TT, C::QS>(smem, gbase + buf * GBLK, TOT, wgrp, SPLIT, pck, cvalid); break;
           }
           check_sync(lc, TPC);
           if (active) {
@@ -778,27 +798,29 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               const float mg = fabsf(xt) - __uint_as_float(up[r] & ~kSign);  // >= 0 up to rounding
               out[r] = __uint_as_float((__float_as_uint(mg) & ~kSign) | ((__float_as_uint(xt) ^ up[r]) & kSign));
             }
-            float* dst = Wout + (size_t)e * Q;
+            const int prow = rr.partner_a >> 9;  // stored where the partner edge will read it
+            float* dst = Wout + (size_t)prow * Q;
             if constexpr (TT > 1) {
               constexpr int V = C::V;
 #pragma unroll
               for (int h = 0; h < TT; ++h) {
                 const int z0 = (t << LJ) | (h << 4);
                 if constexpr (V == 1) {
-                  dst[gpos<MB>(z0)] = out[h];
+                  dst[mpos<MB>(z0, prow)] = out[h];
                 } else if constexpr (V == 2) {
-                  *reinterpret_cast<float2*>(dst + gpos<MB>(z0)) = make_float2(out[2 * h], out[2 * h + 1]);
+                  *reinterpret_cast<float2*>(dst + mpos<MB>(z0, prow)) = make_float2(out[2 * h], out[2 * h + 1]);
                 } else {
 #pragma unroll
                   for (int q4 = 0; q4 < V / 4; ++q4)
-                    *reinterpret_cast<float4*>(dst + gpos<MB>(z0 + 4 * q4)) = make_float4(
+                    *reinterpret_cast<float4*>(dst + mpos<MB>(z0 + 4 * q4, prow)) = make_float4(
                         out[h * V + 4 * q4], out[h * V + 4 * q4 + 1], out[h * V + 4 * q4 + 2], out[h * V + 4 * q4 + 3]);
                 }
               }
             } else if constexpr (R >= 4) {
 #pragma unroll
               for (int ch = 0; ch < CH; ++ch)
-                reinterpret_cast<float4*>(dst)[ch] = make_float4(out[4 * ch], out[4 * ch + 1], out[4 * ch + 2], out[4 * ch + 3]);
+                *reinterpret_cast<float4*>(dst + mpos<MB>(4 * ch, prow)) =
+                    make_float4(out[4 * ch], out[4 * ch + 1], out[4 * ch + 2], out[4 * ch + 3]);
             } else {
 #pragma unroll
               for (int r = 0; r < R; ++r) dst[r] = out[r];
@@ -857,14 +879,21 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   if (!step) cluster_sync_all();
 }
 
-// message layout conversion for nbldpc_step: natural order <-> the kernel's global order gpos
-__global__ void nb_msg_layout_kernel(const float* src, float* dst, size_t nmsg, int q, int m, int to_kernel) {
-  const size_t n = nmsg * (size_t)q;
+// message layout conversion for nbldpc_step: natural order (message of edge e in slot e) <-> the
+// cluster kernel's reader-ordered rows (message of edge e in row partner(e), entries at mpos)
+template <int MB>
+__global__ void nb_msg_layout_kernel(const float* src, float* dst, int frames, CodeDev cd, int to_kernel) {
+  constexpr int Q = 1 << MB;
+  const size_t n = (size_t)frames * cd.E * Q;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t msg = i / q;
-    const int z = (int)(i % q);
-    const int g = m >= 5 ? ((z & ~15) | ((((z >> 2) & 3) ^ ((z >> 4) & 3)) << 2) | (z & 3)) : z;
-    if (to_kernel) dst[msg * q + g] = src[i]; else dst[i] = src[msg * q + g];
+    const size_t fe = i / Q;
+    const int z = (int)(i % Q);
+    const int e = (int)(fe % cd.E);
+    const size_t f = fe / cd.E;
+    const EdgeDev& ed = cd.edges[e];
+    if (ed.var < 0) continue;
+    const size_t k = (f * cd.E + ed.partner) * Q + mpos<MB>(z, ed.partner);
+    if (to_kernel) dst[k] = src[i]; else dst[i] = src[k];
   }
 }
 

@@ -186,14 +186,14 @@ void* persist_kernel_ptr(int m, int big) {
 // shared-memory words per edge team of the cluster kernel (nb::CCfg<m>::TEAM)
 int persist_team_words(int m) {
   switch (m) {
-    case 1: return nb::CCfg<1>::TEAM;
-    case 2: return nb::CCfg<2>::TEAM;
-    case 3: return nb::CCfg<3>::TEAM;
-    case 4: return nb::CCfg<4>::TEAM;
-    case 5: return nb::CCfg<5>::TEAM;
-    case 6: return nb::CCfg<6>::TEAM;
-    case 7: return nb::CCfg<7>::TEAM;
-    case 8: return nb::CCfg<8>::TEAM;
+    case 1: return nb::CCfg<1>::TEAMW;
+    case 2: return nb::CCfg<2>::TEAMW;
+    case 3: return nb::CCfg<3>::TEAMW;
+    case 4: return nb::CCfg<4>::TEAMW;
+    case 5: return nb::CCfg<5>::TEAMW;
+    case 6: return nb::CCfg<6>::TEAMW;
+    case 7: return nb::CCfg<7>::TEAMW;
+    case 8: return nb::CCfg<8>::TEAMW;
   }
   return 0;
 }
@@ -340,6 +340,28 @@ PassParams make_params(const nbldpc_code_s* c, int step_mode, float* u_out) {  /
   P.step_mode = step_mode;
   P.u_out = u_out;
   return P;
+}
+
+nb::ClusterParams make_cparams(const nbldpc_code_s* c, int step_mode, int step_iter, float* u_out);
+
+template <int MB>
+cudaError_t launch_layout_t(const nb::CodeDev& cd, const float* src, float* dst, int frames, int to_kernel, cudaStream_t st) {
+  nb::nb_msg_layout_kernel<MB><<<512, 256, 0, st>>>(src, dst, frames, cd, to_kernel);
+  return cudaGetLastError();
+}
+cudaError_t launch_layout(const nbldpc_code_s* c, const float* src, float* dst, int frames, int to_kernel,
+                          cudaStream_t st) {
+  const nb::CodeDev cd = make_cparams(c, 0, 0, nullptr).code;
+  switch (c->m) {
+    case 1: return launch_layout_t<1>(cd, src, dst, frames, to_kernel, st);
+    case 2: return launch_layout_t<2>(cd, src, dst, frames, to_kernel, st);
+    case 3: return launch_layout_t<3>(cd, src, dst, frames, to_kernel, st);
+    case 4: return launch_layout_t<4>(cd, src, dst, frames, to_kernel, st);
+    case 5: return launch_layout_t<5>(cd, src, dst, frames, to_kernel, st);
+    case 6: return launch_layout_t<6>(cd, src, dst, frames, to_kernel, st);
+    case 7: return launch_layout_t<7>(cd, src, dst, frames, to_kernel, st);
+    default: return launch_layout_t<8>(cd, src, dst, frames, to_kernel, st);
+  }
 }
 
 nb::ClusterParams make_cparams(const nbldpc_code_s* c, int step_mode, int step_iter, float* u_out) {
@@ -700,8 +722,9 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
   c->smem = ((size_t)(c->block / tt) * team_floats(m) + (size_t)c->CPC * q) * sizeof(float);
   {
     // persistent kernel: threads per check = next power of two >= k_max * TT
-    int tpc = 1;
-    while (tpc < k_max * tt) tpc <<= 1;
+    // one team per edge slot of a check (KT = kpad teams), so that a group's message rows are the
+    // contiguous edge slots of its checks
+    int tpc = kpad * tt;
     if (tpc > kBigBlock) {
       nbldpc_destroy(c);
       return NBLDPC_ERR_UNSUPPORTED;
@@ -903,8 +926,7 @@ nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int i
     if (vn_algorithm) {
       NB_TRY(cudaMemcpyAsync(wcur, w_in, msg, cudaMemcpyDeviceToDevice, st));
     } else {  // the cluster kernel keeps messages in its chunk-swizzled order
-      nb::nb_msg_layout_kernel<<<512, 256, 0, st>>>(w_in, wcur, (size_t)frames * c->E, c->q, c->m, 1);
-      NB_TRY(cudaGetLastError());
+      NB_TRY(launch_layout(c, w_in, wcur, frames, 1, st));
     }
   }
   if (vn_algorithm) {
@@ -917,8 +939,7 @@ nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int i
   if (vn_algorithm) {
     NB_TRY(cudaMemcpyAsync(w_out, wnxt, msg, cudaMemcpyDeviceToDevice, st));
   } else {
-    nb::nb_msg_layout_kernel<<<512, 256, 0, st>>>(wnxt, w_out, (size_t)frames * c->E, c->q, c->m, 0);
-    NB_TRY(cudaGetLastError());
+    NB_TRY(launch_layout(c, wnxt, w_out, frames, 0, st));
   }
   if (iter >= 1) {
     NB_TRY(cudaMemcpyAsync(hard, w.dev.xhat, (size_t)frames * c->N, cudaMemcpyDeviceToDevice, st));
