@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         mbar_arrive_tx(&gmbar[b], tx);
         // the block in pieces of <= NB_BLK_PIECE bytes (several TMA transfers in flight)
 #ifndef NB_BLK_PIECE
-#define NB_BLK_PIECE 2048
+#define NB_BLK_PIECE 16384
 #endif
         for (uint32_t o = 0; o < blk; o += NB_BLK_PIECE)
           bulk_g2s(GST + b * GBLK + o / 4, Win + (size_t)cg0 * cd.kpad * Q + o / 4,
