@@ -583,10 +583,17 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               for (int ch = 0; ch < 4; ++ch) {
                 const float4 v = wo4[ch];
                 const float d4[4] = {to_lin(v.x), to_lin(v.y), to_lin(v.z), to_lin(v.w)};
+                // z = 16 t + w: tB = w >> LJ, rB = (w & (2^LJ - 1)) | t << LJ; runs of 2^LJ entries stay
+                // contiguous in a D row, so store them as one vector
+                if constexpr (LJ >= 2) {
+                  *reinterpret_cast<float4*>(DB + db_word(ch >> (LJ - 2), ((4 * ch) & ((1 << LJ) - 1)) | (t << LJ))) =
+                      make_float4(d4[0], d4[1], d4[2], d4[3]);
+                } else if constexpr (LJ == 1) {
+                  *reinterpret_cast<float2*>(DB + db_word(2 * ch, t << 1)) = make_float2(d4[0], d4[1]);
+                  *reinterpret_cast<float2*>(DB + db_word(2 * ch + 1, t << 1)) = make_float2(d4[2], d4[3]);
+                } else {
 #pragma unroll
-                for (int k4 = 0; k4 < 4; ++k4) {
-                  const int w = 4 * ch + k4;  // z = 16 t + w: tB = w >> LJ, rB = (w & (2^LJ - 1)) | t << LJ
-                  DB[db_word(w >> LJ, (w & ((1 << LJ) - 1)) | (t << LJ))] = d4[k4];
+                  for (int k4 = 0; k4 < 4; ++k4) DB[db_word(4 * ch + k4, t)] = d4[k4];
                 }
               }
             } else if constexpr (R >= 4) {

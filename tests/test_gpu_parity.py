@@ -273,3 +273,48 @@ def test_edge_cases_and_errors(dev):
     with pytest.raises(nb.NbldpcError) as ei:
         nb.Code(2, 0x7, M, c["N"], rows, cols, bad)
     assert ei.value.status == -1
+
+
+def _irregular_code(N, degs, m, seed):
+    """Column weight 2, check degrees `degs` (sum = 2N): socket matching with rejection of repeats."""
+    rng = np.random.default_rng(seed)
+    M = len(degs)
+    for _ in range(1000):
+        sockets = np.repeat(np.arange(M), degs)
+        var_of = np.repeat(np.arange(N), 2)[rng.permutation(2 * N)]
+        pairs = set()
+        ok = True
+        for c, v in zip(sockets, var_of):
+            if (c, v) in pairs:
+                ok = False
+                break
+            pairs.add((c, v))
+        if ok:
+            coeffs = rng.integers(1, 1 << m, size=2 * N)
+            order = np.lexsort((var_of, sockets))
+            return M, sockets[order].astype(np.int32), var_of[order].astype(np.int32), coeffs[order].astype(np.int32)
+    raise RuntimeError("no simple graph found")
+
+
+@pytest.mark.parametrize("vn", [0, 1])
+def test_irregular_check_degrees_and_cycle_codes(dev, vn):
+    """Check degrees that are not a power of two (padding edge slots) and degree-2 checks."""
+    import paper_1008_4370_b200 as nb
+
+    cases = [(4, 0x13, 40, [3, 5, 4, 6, 2, 3, 5, 4, 3, 5, 4, 6, 2, 3, 5, 4, 3, 3], 11),
+             (6, 0x43, 24, [2] * 24, 12),
+             (8, 0x11D, 36, [6, 7, 5, 6, 6, 7, 5, 6, 6, 7, 5, 6][:12], 13)]
+    for m, poly, N, degs, seed in cases:
+        degs = list(degs)
+        if sum(degs) != 2 * N:  # adjust the last degree so that the sockets match
+            degs[-1] += 2 * N - sum(degs)
+        M, rows, cols, coeffs = _irregular_code(N, degs, m, seed)
+        code = nb.Code(m, poly, M, N, rows, cols, coeffs)
+        ocode = oracle.Code(oracle.Field(m, poly), M, N, rows, cols, coeffs)
+        llr = synth.awgn_llr(N * m, 0, 40, synth.sigma2_for(2.5, 0.5), 90 + m)
+        out = code.decode(torch.from_numpy(llr).to(dev), 15, vn_algorithm=vn)
+        torch.cuda.synchronize()
+        ref = ocode.lf_decode_batch(llr, 15)
+        same = ((out["hard"].cpu().numpy() == ref["hard"]).all(1) & (out["ok"].cpu().numpy() == ref["ok"])
+                & (out["iters"].cpu().numpy() == ref["iters"]))
+        assert same.mean() >= 0.95, (m, degs[:4], same.mean())
