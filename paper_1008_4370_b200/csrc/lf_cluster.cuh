@@ -24,7 +24,17 @@
 // entries each.  Phase A: thread t holds z = 16t + r (register bits = z bits 0..3); phase B (after
 // one shared-memory transposition): z = jl | t << (8-m) | h << 4 with r = jl + 2^(8-m) h.
 #pragma once
+#include <assert.h>
+
 #include "decoder.cuh"
+
+// NB_BOUNDS_CHECK=1 (debug builds, `NBLDPC_DEFS=-DNB_BOUNDS_CHECK`): device asserts on every computed
+// shared-memory index and global message row (compute-sanitizer is not available on the GPU pool)
+#ifdef NB_BOUNDS_CHECK
+#define NB_CHECK(cond) assert(cond)
+#else
+#define NB_CHECK(cond) ((void)0)
+#endif
 
 namespace nb {
 
@@ -415,6 +425,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #ifndef NB_BLK_PIECE
 #define NB_BLK_PIECE 16384
 #endif
+        NB_CHECK(blk == 0 || ((size_t)cg0 * cd.kpad * Q * 4 + blk <= (size_t)cd.E * Q * 4 && blk <= (uint32_t)GBLK * 4));
         for (uint32_t o = 0; o < blk; o += NB_BLK_PIECE)
           bulk_g2s(GST + b * GBLK + o / 4, Win + (size_t)cg0 * cd.kpad * Q + o / 4,
                    blk - o < NB_BLK_PIECE ? blk - o : NB_BLK_PIECE, &gmbar[b]);
@@ -786,7 +797,10 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           if (cvalid) {
             // scatter: X_e(pi_e^-1 z) = U_e(z) = T_e(.); padding teams hold the neutral message
 #pragma unroll
-            for (int r = 0; r < R; ++r) st[oidx[r]] = __uint_as_float(up[r]);
+            for (int r = 0; r < R; ++r) {
+              NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
+              st[oidx[r]] = __uint_as_float(up[r]);
+            }
           }
           check_sync(lc, TPC);
           switch (JPT) {
@@ -801,11 +815,13 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             float out[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
+              NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
               const float xt = TOT[oidx[r]];
               const float mg = fabsf(xt) - __uint_as_float(up[r] & ~kSign);  // >= 0 up to rounding
               out[r] = __uint_as_float((__float_as_uint(mg) & ~kSign) | ((__float_as_uint(xt) ^ up[r]) & kSign));
             }
             const int prow = rr.partner_a >> 9;  // stored where the partner edge will read it
+            NB_CHECK(prow >= 0 && prow < cd.E);
             float* dst = Wout + (size_t)prow * Q;
             if constexpr (TT > 1) {
               constexpr int V = C::V;
