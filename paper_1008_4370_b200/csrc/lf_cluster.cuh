@@ -479,21 +479,26 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #pragma unroll
         for (int ch = 0; ch < CH; ++ch) wo4[ch] = make_float4(0.5f, 0.25f, 0.125f, 1.0f);
 #endif
+        auto load_wo = [&]() {
 #ifdef NB_DIAG_DEC_NOLOAD
-        if (false) {
+          if (false) {
 #else
-        if (is_a && do_dec) {
+          if (is_a && do_dec) {
 #endif
-          const int prow = rr.partner_a >> 9;  // W_e is stored in the row its reader (the partner edge) consumes
-          if constexpr (R >= 4) {
-            const float* so = Win + (size_t)prow * Q;
+            const int prow = rr.partner_a >> 9;  // W_e is stored in the row its reader (the partner edge) consumes
+            if constexpr (R >= 4) {
+              const float* so = Win + (size_t)prow * Q;
 #pragma unroll
-            for (int ch = 0; ch < CH; ++ch) wo4[ch] = __ldcg(reinterpret_cast<const float4*>(so + mpos<MB>(t * R + 4 * ch, prow)));
-          } else {
-            const float2 v2 = __ldcg(reinterpret_cast<const float2*>(Win + (size_t)prow * Q));
-            wo4[0] = make_float4(v2.x, v2.y, 0.f, 0.f);
+              for (int ch = 0; ch < CH; ++ch) wo4[ch] = __ldcg(reinterpret_cast<const float4*>(so + mpos<MB>(t * R + 4 * ch, prow)));
+            } else {
+              const float2 v2 = __ldcg(reinterpret_cast<const float2*>(Win + (size_t)prow * Q));
+              wo4[0] = make_float4(v2.x, v2.y, 0.f, 0.f);
+            }
           }
-        }
+        };
+#ifndef NB_WO_LATE
+        load_wo();
+#endif
 
         // ---- VARIABLE TO CHECK: x (phase B) = P^0 (*) Gamma^-1(W_e'); at l = 0, x = P^0
         float x[R];
@@ -586,6 +591,9 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         // ---- TENTATIVE DECISION at v's first edge: M_v(z) = sum_y raw(y) W_e(z ^ y)
         if (do_dec) {
           // D = Gamma^-1(W_e) in the row layout word(z) = 16 tB(z) + rB(z), over the consumed Wp
+#ifdef NB_WO_LATE
+          load_wo();
+#endif
           float* DB = st;
           if constexpr (TT > 1) __syncwarp();  // transposition reads done
           if (is_a) {
