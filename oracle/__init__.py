@@ -97,6 +97,8 @@ def _lib():
                 sig["or_lf_decision" + sfx] = (None, [vp, dp, dp, dp, dp, dp, dp, dp])
                 sig["or_lf_decode" + sfx] = (None, [vp, dp, i32, i32, i32, dp, dp, dp, dp, dp])
                 sig["or_lf_decode_batch" + sfx] = (None, [vp, dp, i32, i32, i32, i32, dp, dp, dp, dp, dp, i32])
+                sig["or_lf_decode_batch_pmf" + sfx] = (None, [vp, dp, i32, i32, i32, i32, dp, dp, dp, dp, dp, i32])
+                sig["or_lf_init_pmf" + sfx] = (None, [vp, dp, dp, dp])
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
                 fn.restype = res
@@ -310,6 +312,15 @@ class Code:
         getattr(self._L, "or_lf_init" + sfx)(self._h, _p(llr), _p(S0), _p(L0))
         return S0, L0
 
+    def lf_init_pmf(self, pmf, f32=False):
+        """Lambda^(0) from a symbol-level channel pmf [N][q]."""
+        dt, sfx = self._real(f32)
+        pmf = _f64(pmf)
+        S0 = np.zeros((self.N, self.q), np.uint8)
+        L0 = np.zeros((self.N, self.q), dt)
+        getattr(self._L, "or_lf_init_pmf" + sfx)(self._h, _p(pmf), _p(S0), _p(L0))
+        return S0, L0
+
     def lf_check_to_variable(self, Us, Ul, f32=False):
         dt, sfx = self._real(f32)
         Us, Ul = _u8(Us), np.ascontiguousarray(Ul, dt)
@@ -358,6 +369,27 @@ class Code:
         )
         out = {"hard": x.astype(np.uint8) if self.q <= 256 else x, "ok": ok.astype(np.uint8), "iters": it,
                "events": ev}
+        if soft is not None:
+            out["soft"] = soft
+        return out
+
+    def lf_decode_batch_pmf(self, pmf, max_iters: int, mode: int = EXACT, early_stop: bool = True,
+                            nthreads: int | None = None, f32: bool = False, want_soft: bool = False):
+        """Decode F frames from symbol-level channel pmfs (float32 [F][N][q])."""
+        dt, sfx = self._real(f32)
+        pmf = np.ascontiguousarray(pmf, np.float32).reshape(-1, self.N * self.q)
+        F = pmf.shape[0]
+        x = np.zeros((F, self.N), np.int32)
+        ok = np.zeros(F, np.int32)
+        it = np.zeros(F, np.int32)
+        ev = np.zeros(F, np.int32)
+        soft = np.zeros((F, self.N * self.m), dt) if want_soft else None
+        nt = nthreads or os.cpu_count() or 1
+        getattr(self._L, "or_lf_decode_batch_pmf" + sfx)(
+            self._h, _p(pmf), F, int(max_iters), int(mode), int(bool(early_stop)), _p(x), _p(ok), _p(it),
+            _p(soft) if soft is not None else None, _p(ev), int(nt),
+        )
+        out = {"hard": x.astype(np.uint8), "ok": ok.astype(np.uint8), "iters": it, "events": ev}
         if soft is not None:
             out["soft"] = soft
         return out

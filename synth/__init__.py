@@ -153,3 +153,43 @@ def config_llr(name: str, frame0: int, nframes: int, ebn0_db: float | None = Non
     eb = c["ebn0"][point] if ebn0_db is None else ebn0_db
     s2 = sigma2_for(eb, c["rate"])
     return awgn_llr(c["N"] * c["m"], frame0, nframes, s2, c["seed_noise"] + 100 * point, bits=bits)
+
+
+def orthogonal_pmf(N: int, m: int, frame0: int, nframes: int, sigma2: float, seed: int, symbols=None) -> np.ndarray:
+    """float32 symbol pmfs [nframes][N][q] of q-ary orthogonal signalling over AWGN.
+
+    A non-binary channel whose pmf does not factor over the bits (the general input of
+    PAPER.md:465-473): symbol x is sent as the x-th of q orthogonal unit-energy-per-bit
+    pulses, amplitude A = sqrt(m); the receiver sees r_y = A [y = x] + sigma n_y, so
+    Pr(X = y | r) is proportional to exp(A r_y / sigma^2).  Rows are scaled by their
+    maximum (largest entry 1).  ``symbols`` is None (all-zero codeword) or [nframes][N].
+    Noise is drawn per 256-frame chunk from Philox(key=(seed, chunk)) as in awgn_llr.
+    """
+    q = 1 << m
+    A = np.sqrt(m)
+    out = np.empty((nframes, N, q), np.float32)
+    f = frame0
+    end = frame0 + nframes
+    while f < end:
+        c = f // CHUNK
+        lo, hi = f - c * CHUNK, min(CHUNK, end - c * CHUNK)
+        n = hi - lo
+        rng = np.random.Generator(np.random.Philox(key=[seed, c]))
+        noise = rng.standard_normal((CHUNK, N, q), dtype=np.float32)[lo:hi].astype(np.float64)
+        r = np.sqrt(sigma2) * noise
+        x = np.zeros((n, N), np.int64) if symbols is None else np.asarray(symbols[f - frame0: f - frame0 + n], np.int64)
+        np.put_along_axis(r, x[..., None], np.take_along_axis(r, x[..., None], 2) + A, 2)
+        ll = (A / sigma2) * r
+        ll -= ll.max(axis=2, keepdims=True)
+        out[f - frame0: f - frame0 + n] = np.exp(ll)
+        f += n
+    return out
+
+
+def config_pmf(name: str, frame0: int, nframes: int, ebn0_db: float | None = None, symbols=None, point: int = 0):
+    """Orthogonal-signalling pmfs for config ``name`` (same Eb/N0 points as config_llr)."""
+    c = CONFIGS[name]
+    eb = c["ebn0"][point] if ebn0_db is None else ebn0_db
+    s2 = sigma2_for(eb, c["rate"])
+    return orthogonal_pmf(c["N"], c["m"], frame0, nframes, s2, c["seed_noise"] + 7000 + 100 * point, symbols)
+
