@@ -136,6 +136,24 @@ nbldpc_status_t nbldpc_decode_host(nbldpc_code_t code, const float* llr_host, in
                                    uint8_t* hard_host, uint8_t* ok_host, int32_t* iters_host, void* stream,
                                    const nbldpc_decode_opts_t* opts);
 
+/* Decodes `frames` frames from a general symbol-level channel pmf (the
+ * initialisation P_v^(0)(z) = sum_x p_v^(0)(x) (-1)^{z.x}, for channels whose prior does not factor
+ * over the bits -- q-ary modulations, symbol erasures, soft symbol demappers).
+ *   pmf : DEVICE, float32 [frames][N][2^m]; entry x of row (frame, v) is a nonnegative weight of
+ *         Pr(X_v = x | Y_v).  Any positive scale per row is allowed: the row is scaled to sum to one
+ *         (reading R23).  A row whose sum is not positive is treated as uniform and counted as a
+ *         numerical event (opts->events_out), as are the iterations it stays degenerate in.
+ *   the other arguments as nbldpc_decode_ex; soft_out holds the same posterior bit log-magnitudes.
+ * The channel spectrum of a general pmf is not a tensor product, so this entry point always runs
+ * the paper's direct q^2-term variable-node convolution (NBLDPC_VN_DIRECT; opts->vn_algorithm is
+ * ignored).  The transform of the pmf is computed inside the first pass, per frame, and kept in a
+ * per-slot buffer of N*2^m floats (allocated on first use, released with the handle).
+ * pmf must be 16-byte aligned (NBLDPC_ERR_INVALID_ARGUMENT otherwise).
+ * Stream-ordered; same results-independence and stream rules as nbldpc_decode. */
+nbldpc_status_t nbldpc_decode_pmf(nbldpc_code_t code, const float* pmf, int frames, int max_iters,
+                                  uint8_t* hard_symbols, uint8_t* syndrome_ok, int32_t* iters_used, void* stream,
+                                  const nbldpc_decode_opts_t* opts);
+
 /* One Log-Fourier iteration from a given state (step-parity tests; not on the hot path).
  * Requires every row of H to have the same degree k, a power of two >= 4 (else
  * NBLDPC_ERR_UNSUPPORTED): then the decoder's internal edge slots coincide with canonical order.

@@ -70,6 +70,7 @@ def lib():
         "nbldpc_decode": (i32, [vp, vp, i32, i32, vp, vp, vp, vp]),
         "nbldpc_decode_ex": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, ctypes.POINTER(_Opts)]),
         "nbldpc_decode_host": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, ctypes.POINTER(_Opts)]),
+        "nbldpc_decode_pmf": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, ctypes.POINTER(_Opts)]),
         "nbldpc_step": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, i32, vp]),
     }
     for name, (res, args) in sig.items():
@@ -178,6 +179,33 @@ class Code:
                                       out["ok"].data_ptr(), out["iters"].data_ptr(), _stream(stream),
                                       ctypes.byref(o))
         _check(st, "nbldpc_decode_ex")
+        return out
+
+    def decode_pmf(self, pmf, max_iters: int, *, syndrome_mode: int = 0, early_stop: bool = True, want_soft=False,
+                   want_events=False, slots: int = 0, use_graph: int = 0, out=None, stream=None):
+        """Decode frames from symbol-level channel pmfs (nbldpc_decode_pmf).
+        ``pmf``: CUDA float32 tensor [F, N, q] (any positive scale per row).  Same outputs as decode."""
+        import torch
+
+        if not (pmf.is_cuda and pmf.dtype == torch.float32 and pmf.is_contiguous()):
+            raise ValueError("pmf must be a contiguous CUDA float32 tensor")
+        F = pmf.numel() // (self.N * self.q)
+        if F * self.N * self.q != pmf.numel() or F < 1:
+            raise ValueError("pmf size is not a multiple of N*q")
+        dev = pmf.device
+        if out is None:
+            out = {"hard": torch.empty((F, self.N), dtype=torch.uint8, device=dev),
+                   "ok": torch.empty(F, dtype=torch.uint8, device=dev),
+                   "iters": torch.empty(F, dtype=torch.int32, device=dev)}
+            if want_soft:
+                out["soft"] = torch.empty((F, self.N * self.m), dtype=torch.float32, device=dev)
+            if want_events:
+                out["events"] = torch.empty(F, dtype=torch.int32, device=dev)
+        o = self._opts(syndrome_mode, early_stop, out.get("soft"), out.get("events"), slots, use_graph, 1)
+        st = self._L.nbldpc_decode_pmf(self._h, pmf.data_ptr(), F, int(max_iters), out["hard"].data_ptr(),
+                                       out["ok"].data_ptr(), out["iters"].data_ptr(), _stream(stream),
+                                       ctypes.byref(o))
+        _check(st, "nbldpc_decode_pmf")
         return out
 
     def decode_host(self, llr_host, max_iters: int, *, syndrome_mode: int = 0, slots: int = 0, use_graph: int = 0,

@@ -65,6 +65,8 @@ struct CallDev {            // per-call arguments, written on the stream before 
   int frames, max_iters, mode, early_stop;
   int want_soft;
   int pad[3];
+  const float* pmf;   // nbldpc_decode_pmf: [frames][N][q] channel pmf (else NULL)
+  float* p0buf;       // nbldpc_decode_pmf: [S][N][q] P_v^0 = WHT(pmf) / sum(pmf) per slot
 };
 
 struct WorkDev {
@@ -224,8 +226,9 @@ __device__ __forceinline__ int atom_add_release_gpu(int* p, int v) {
 }
 __device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
-template <int MB, int MAXB, bool DIRECT>
+template <int MB, int MAXB, bool DIRECT, bool PMF = false>
 __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(PassParams P) {
+  static_assert(DIRECT || !PMF, "a general channel pmf needs the direct convolution");
   using C = Cfg<MB>;
   constexpr int Q = C::Q, R = C::R, TT = C::TT, LR = C::LR, NB = C::TT;
   extern __shared__ __align__(16) float smem[];
@@ -302,7 +305,7 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
     const int s = yl0 + i * Y;
     const int f = sh_frame[i], ell = sh_iter[i];
     float* th = NB_TH(buf);
-    if (t == 0) {
+    if (!PMF && t == 0) {
       const float* src = ell == 0 ? llr + ((size_t)f * cd.N + ed.var) * MB : ws.Tt + ((size_t)s * cd.N + ed.var) * 8;
 #pragma unroll
       for (int b = 0; b < MB; ++b) cp_async4(th + b, src + b);
@@ -346,8 +349,8 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
     // ---- channel terms t_i = tanh(L_{v,i}/2): computed at l = 0, cached per slot after
     float th[MB];
 #pragma unroll
-    for (int b = 0; b < MB; ++b) th[b] = active ? NB_TH(buf)[b] : 0.0f;
-    if (ell == 0 && active) {
+    for (int b = 0; b < MB; ++b) th[b] = (active && !PMF) ? NB_TH(buf)[b] : 0.0f;
+    if (!PMF && ell == 0 && active) {
 #pragma unroll
       for (int b = 0; b < MB; ++b) th[b] = tanhf(0.5f * th[b]);
       if (is_a && t == 0) {
@@ -357,7 +360,52 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
     }
     // P_v^0(z) for the thread's block z = t*R + zl (closed form)
     float p0[R];
-    {
+    if constexpr (PMF) {
+      // general pmf: at l = 0 P = WHT(p) / sum(p) -- LR butterfly stages in
+      // registers, MB - LR across the team by shuffles -- kept per slot for the later passes
+      const float* src = ell == 0 ? call->pmf + ((size_t)f * cd.N + (active ? ed.var : 0)) * Q
+                                  : call->p0buf + ((size_t)s * cd.N + (active ? ed.var : 0)) * Q;
+      if constexpr (R >= 4) {
+#pragma unroll
+        for (int c4 = 0; c4 < R / 4; ++c4) {
+          const float4 v = active ? __ldcg(reinterpret_cast<const float4*>(src + t * R) + c4) : make_float4(0, 0, 0, 0);
+          p0[4 * c4] = v.x; p0[4 * c4 + 1] = v.y; p0[4 * c4 + 2] = v.z; p0[4 * c4 + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int zl = 0; zl < R; ++zl) p0[zl] = active ? __ldcg(src + t * R + zl) : 0.0f;
+      }
+      if (ell == 0) {
+#pragma unroll
+        for (int b = 0; b < LR; ++b)
+#pragma unroll
+          for (int zl = 0; zl < R; ++zl)
+            if (!(zl & (1 << b))) {
+              const float u = p0[zl], w = p0[zl | (1 << b)];
+              p0[zl] = u + w;
+              p0[zl | (1 << b)] = u - w;
+            }
+#pragma unroll
+        for (int b = LR; b < MB; ++b) {
+          const int off = 1 << (b - LR);
+#pragma unroll
+          for (int zl = 0; zl < R; ++zl) {
+            const float o = __shfl_xor_sync(0xffffffffu, p0[zl], off);
+            p0[zl] = (t & off) ? o - p0[zl] : p0[zl] + o;
+          }
+        }
+        float tot = p0[0];
+        if constexpr (TT > 1) tot = __shfl_sync(0xffffffffu, p0[0], lane & ~(TT - 1));
+        const float inv = tot > 0.0f ? 1.0f / tot : 0.0f;  // degenerate row: all zero -> event below
+#pragma unroll
+        for (int zl = 0; zl < R; ++zl) p0[zl] *= inv;
+        if (is_a) {
+          float* dst = call->p0buf + ((size_t)s * cd.N + ed.var) * Q + t * R;
+#pragma unroll
+          for (int zl = 0; zl < R; ++zl) dst[zl] = p0[zl];
+        }
+      }
+    } else {
       float hi = 1.0f;
 #pragma unroll
       for (int b = LR; b < MB; ++b)

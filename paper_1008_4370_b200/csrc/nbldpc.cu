@@ -43,6 +43,8 @@ struct Workspace {
   size_t llr_stage_bytes = 0;
   uint8_t* out_stage = nullptr;
   size_t out_stage_bytes = 0;
+  float* p0buf = nullptr;  // nbldpc_decode_pmf: [S][N][q] channel spectra
+  size_t p0buf_bytes = 0;
   // launch accounting of the most recent decode
   cudaStream_t last_stream = nullptr;
   int last_graph = 0;
@@ -127,37 +129,40 @@ void free_workspace(Workspace& w) {
   if (w.host_flag) cudaFreeHost(w.host_flag);
   if (w.llr_stage) cudaFree(w.llr_stage);
   if (w.out_stage) cudaFree(w.out_stage);
+  if (w.p0buf) cudaFree(w.p0buf);
   w = Workspace{};
 }
 
-template <int MB, int MAXB, bool DIRECT>
-void* pass_fn() { return reinterpret_cast<void*>(&nb::nb_pass_kernel<MB, MAXB, DIRECT>); }
+template <int MB, int MAXB, bool DIRECT, bool PMF>
+void* pass_fn() { return reinterpret_cast<void*>(&nb::nb_pass_kernel<MB, MAXB, DIRECT, PMF>); }
 
-template <bool DIRECT>
+template <bool DIRECT, bool PMF>
 void* pass_kernel_ptr_t(int m, int big) {
   switch (m * 2 + (big ? 1 : 0)) {
-    case 2: return pass_fn<1, 256, DIRECT>();
-    case 3: return pass_fn<1, kBigBlock, DIRECT>();
-    case 4: return pass_fn<2, 256, DIRECT>();
-    case 5: return pass_fn<2, kBigBlock, DIRECT>();
-    case 6: return pass_fn<3, 256, DIRECT>();
-    case 7: return pass_fn<3, kBigBlock, DIRECT>();
-    case 8: return pass_fn<4, 256, DIRECT>();
-    case 9: return pass_fn<4, kBigBlock, DIRECT>();
-    case 10: return pass_fn<5, 256, DIRECT>();
-    case 11: return pass_fn<5, kBigBlock, DIRECT>();
-    case 12: return pass_fn<6, 256, DIRECT>();
-    case 13: return pass_fn<6, kBigBlock, DIRECT>();
-    case 14: return pass_fn<7, 256, DIRECT>();
-    case 15: return pass_fn<7, kBigBlock, DIRECT>();
-    case 16: return pass_fn<8, 256, DIRECT>();
-    case 17: return pass_fn<8, kBigBlock, DIRECT>();
+    case 2: return pass_fn<1, 256, DIRECT, PMF>();
+    case 3: return pass_fn<1, kBigBlock, DIRECT, PMF>();
+    case 4: return pass_fn<2, 256, DIRECT, PMF>();
+    case 5: return pass_fn<2, kBigBlock, DIRECT, PMF>();
+    case 6: return pass_fn<3, 256, DIRECT, PMF>();
+    case 7: return pass_fn<3, kBigBlock, DIRECT, PMF>();
+    case 8: return pass_fn<4, 256, DIRECT, PMF>();
+    case 9: return pass_fn<4, kBigBlock, DIRECT, PMF>();
+    case 10: return pass_fn<5, 256, DIRECT, PMF>();
+    case 11: return pass_fn<5, kBigBlock, DIRECT, PMF>();
+    case 12: return pass_fn<6, 256, DIRECT, PMF>();
+    case 13: return pass_fn<6, kBigBlock, DIRECT, PMF>();
+    case 14: return pass_fn<7, 256, DIRECT, PMF>();
+    case 15: return pass_fn<7, kBigBlock, DIRECT, PMF>();
+    case 16: return pass_fn<8, 256, DIRECT, PMF>();
+    case 17: return pass_fn<8, kBigBlock, DIRECT, PMF>();
   }
   return nullptr;
 }
-// direct = 1: the paper's q^2-term convolution; 0: separable butterflies
+// direct = 1: the paper's q^2-term convolution; 0: separable butterflies;
+// 2: the direct convolution with the channel spectrum of a general pmf (nbldpc_decode_pmf)
 void* pass_kernel_ptr(int m, int big, int direct) {
-  return direct ? pass_kernel_ptr_t<true>(m, big) : pass_kernel_ptr_t<false>(m, big);
+  if (direct == 2) return pass_kernel_ptr_t<true, true>(m, big);
+  return direct ? pass_kernel_ptr_t<true, false>(m, big) : pass_kernel_ptr_t<false, false>(m, big);
 }
 
 template <int MB, int NTHR>
@@ -218,12 +223,12 @@ cudaError_t launch_cluster(const nbldpc_code_s* c, const nb::ClusterParams& P, i
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a property of the kernel (one instantiation per
 // (m, block variant)) shared by every code on the device: only ever raise it.
 std::mutex g_attr_mu;
-size_t g_attr_smem[64][36] = {};
+size_t g_attr_smem[64][54] = {};
 
 cudaError_t ensure_smem_attr(const nbldpc_code_s* c) {
   std::lock_guard<std::mutex> lk(g_attr_mu);
-  for (int direct = 0; direct < 2; ++direct) {
-    const int d = c->device & 63, k = (c->m * 2 + c->big) * 2 + direct;
+  for (int direct = 0; direct < 3; ++direct) {
+    const int d = c->device & 63, k = (c->m * 2 + c->big) * 3 + direct;
     if (g_attr_smem[d][k] >= c->smem) continue;
     cudaError_t e = cudaFuncSetAttribute(pass_kernel_ptr(c->m, c->big, direct),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
@@ -462,8 +467,10 @@ int default_slots(const nbldpc_code_s* c, int frames) {
   return (int)S;
 }
 
+// pmf != NULL: nbldpc_decode_pmf (llr unused; the direct kernel with the general channel spectrum)
 nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int max_iters, uint8_t* hard,
-                            uint8_t* ok, int32_t* iters, cudaStream_t st, const nbldpc_decode_opts_t* opts) {
+                            uint8_t* ok, int32_t* iters, cudaStream_t st, const nbldpc_decode_opts_t* opts,
+                            const float* pmf = nullptr) {
   int mode = 0, early = 1, slots = 0, use_graph = 0, direct = 0;
   float* soft = nullptr;
   int32_t* events = nullptr;
@@ -479,6 +486,7 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   }
   if (mode != 0 && mode != 1) return NBLDPC_ERR_INVALID_ARGUMENT;
   if (direct != 0 && direct != 1) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (pmf) direct = 2;
   if (slots < 0) return NBLDPC_ERR_INVALID_ARGUMENT;
   if ((soft && !is_device_ptr(soft)) || (events && !is_device_ptr(events))) return NBLDPC_ERR_INVALID_ARGUMENT;
   int S = slots > 0 ? std::min(slots, frames) : default_slots(c, frames);
@@ -488,6 +496,21 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   if (rs != NBLDPC_OK) return rs;
   Workspace& w = c->ws;
   CallDev call{};
+  if (pmf) {
+    const size_t need = (size_t)S * c->N * c->q * sizeof(float);
+    if (w.p0buf_bytes < need) {
+      if (w.p0buf) {
+        NB_TRY(cudaStreamSynchronize(st));  // a previous pmf decode on this stream may still read it
+        cudaFree(w.p0buf);
+        w.p0buf = nullptr;
+        w.p0buf_bytes = 0;
+      }
+      NB_TRY(cudaMalloc(&w.p0buf, need));
+      w.p0buf_bytes = need;
+    }
+    call.pmf = pmf;
+    call.p0buf = w.p0buf;
+  }
   call.llr = llr;
   call.hard = hard;
   call.ok = ok;
@@ -836,6 +859,16 @@ nbldpc_status_t nbldpc_decode_ex(nbldpc_code_t c, const float* llr, int frames, 
     return NBLDPC_ERR_INVALID_ARGUMENT;
   std::lock_guard<std::mutex> lk(c->mu);
   return decode_impl(c, llr, frames, max_iters, hard, ok, iters, static_cast<cudaStream_t>(stream), opts);
+}
+
+nbldpc_status_t nbldpc_decode_pmf(nbldpc_code_t c, const float* pmf, int frames, int max_iters, uint8_t* hard,
+                                  uint8_t* ok, int32_t* iters, void* stream, const nbldpc_decode_opts_t* opts) {
+  if (!c || frames < 1 || max_iters < 1) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (!is_device_ptr(pmf) || !is_device_ptr(hard) || !is_device_ptr(ok) || !is_device_ptr(iters))
+    return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (((uintptr_t)pmf & 15) != 0) return NBLDPC_ERR_INVALID_ARGUMENT;  // rows are read as float4
+  std::lock_guard<std::mutex> lk(c->mu);
+  return decode_impl(c, nullptr, frames, max_iters, hard, ok, iters, static_cast<cudaStream_t>(stream), opts, pmf);
 }
 
 nbldpc_status_t nbldpc_decode(nbldpc_code_t c, const float* llr, int frames, int max_iters, uint8_t* hard,

@@ -1,0 +1,167 @@
+"""GPU parity of the symbol-pmf input (nbldpc_decode_pmf) against the oracle.
+
+Inputs: q-ary orthogonal signalling over AWGN (synth.orthogonal_pmf), a channel whose pmf does
+not factor over the bits.  Same bar as the LLR path: hard decisions,
+syndrome flags and iteration counts bit-exact on every stable frame (fp64 and fp32 oracle
+trajectories agree), soft outputs within the R22 tolerance."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import synth
+from helpers import bit_prior
+from parity import config_inputs, oracle_code
+
+pytestmark = pytest.mark.gpu
+
+_codes = {}
+
+
+def gpu_code(name):
+    import paper_1008_4370_b200 as nb
+
+    if name not in _codes:
+        c = synth.CONFIGS[name]
+        M, rows, cols, coeffs = synth.config_code(name)
+        _codes[name] = nb.Code(c["m"], c["poly"], M, c["N"], rows, cols, coeffs)
+    return _codes[name]
+
+
+@pytest.fixture(scope="module")
+def dev():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch.device("cuda:0")
+
+
+def _pmf_inputs(name, F, ebn0):
+    _, _, xs = config_inputs(name, 0, F)
+    return synth.config_pmf(name, 0, F, ebn0_db=ebn0, symbols=xs), xs
+
+
+def _compare(name, out, pmf, idx, max_iters):
+    """Bit-exact on stable frames; returns the number of unstable frames among idx."""
+    ocode = oracle_code(name)
+    ref = ocode.lf_decode_batch_pmf(pmf[idx], max_iters)
+    hard = out["hard"].cpu().numpy()[idx]
+    ok = out["ok"].cpu().numpy()[idx]
+    it = out["iters"].cpu().numpy()[idx]
+    same = (hard == ref["hard"]).all(1) & (ok == ref["ok"]) & (it == ref["iters"])
+    unstable = 0
+    if not same.all():
+        bad = np.where(~same)[0]
+        twin = ocode.lf_decode_batch_pmf(pmf[idx][bad], max_iters, f32=True)
+        for n, b in enumerate(bad):
+            stable = (np.array_equal(twin["hard"][n], ref["hard"][b]) and twin["ok"][n] == ref["ok"][b]
+                      and twin["iters"][n] == ref["iters"][b])
+            assert not stable, (f"{name}: stable frame {idx[b]} differs: gpu iters {it[b]} ok {ok[b]} vs "
+                                f"oracle {ref['iters'][b]} {ref['ok'][b]}")
+            unstable += 1
+    return unstable
+
+
+PMF_CASES = [
+    # name, Eb/N0 (dB), gpu frames, oracle sample
+    ("C1", 2.0, 64, 64),
+    ("C2", 0.5, 256, 8),
+    ("C3", 1.0, 64, 4),
+    ("C5", 3.5, 256, 16),
+]
+
+
+@pytest.mark.parametrize("name,ebn0,F,nsample", PMF_CASES)
+def test_pmf_decode_parity(dev, name, ebn0, F, nsample):
+    c = synth.CONFIGS[name]
+    pmf, xs = _pmf_inputs(name, F, ebn0)
+    code = gpu_code(name)
+    out = code.decode_pmf(torch.from_numpy(pmf).to(dev), c["max_iters"])
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(2)
+    idx = np.arange(F) if nsample >= F else np.sort(rng.choice(F, nsample, replace=False))
+    unstable = _compare(name, out, pmf, idx, c["max_iters"])
+    assert unstable <= max(1, len(idx) // 10)
+    it = out["iters"].cpu().numpy()
+    assert it.min() >= 1 and it.max() <= c["max_iters"]
+    ocode = oracle_code(name)
+    hard, okg = out["hard"].cpu().numpy(), out["ok"].cpu().numpy()
+    for f in rng.choice(F, min(F, 32), replace=False):
+        assert bool(okg[f]) == ocode.syndrome(hard[f])[0]
+
+
+def test_pmf_soft_parity(dev):
+    # posterior bit log-magnitudes after a fixed number of iterations (R22: 1e-3 ln on entries
+    # above e^-5, where the fp32 decision sums keep that precision)
+    name = "C1"
+    pmf, _ = _pmf_inputs(name, 64, 2.0)
+    code = gpu_code(name)
+    ocode = oracle_code(name)
+    for iters in (1, 3):
+        out = code.decode_pmf(torch.from_numpy(pmf).to(dev), iters, early_stop=False, want_soft=True,
+                              want_events=True)
+        ref = ocode.lf_decode_batch_pmf(pmf, iters, early_stop=False, want_soft=True)
+        soft = out["soft"].cpu().numpy()
+        big = ref["soft"] > -5.0
+        assert np.abs(soft[big] - ref["soft"][big]).max() <= 1e-3, iters
+        assert int(out["events"].sum()) == 0
+
+
+def test_factorised_pmf_equals_llr_path(dev):
+    # a bit-product pmf is the LLR input in another form: same decisions
+    name = "C5"
+    c = synth.CONFIGS[name]
+    _, llr, _ = config_inputs(name, 0, 128, point=4)
+    m, N = c["m"], c["N"]
+    pmf = np.stack([np.stack([bit_prior(f[v * m:(v + 1) * m].astype(np.float64)) for v in range(N)])
+                    for f in llr]).astype(np.float32)
+    code = gpu_code(name)
+    a = code.decode(torch.from_numpy(llr).to(dev), c["max_iters"], vn_algorithm=1)
+    b = code.decode_pmf(torch.from_numpy(pmf).to(dev), c["max_iters"])
+    same = ((a["hard"] == b["hard"]).all(1) & (a["ok"] == b["ok"]) & (a["iters"] == b["iters"])).float().mean()
+    assert same.item() >= 0.95
+
+
+def test_pmf_invariance_and_edge_cases(dev):
+    import paper_1008_4370_b200 as nb
+
+    name = "C2"
+    c = synth.CONFIGS[name]
+    pmf, _ = _pmf_inputs(name, 96, 0.5)
+    code = gpu_code(name)
+    x = torch.from_numpy(pmf).to(dev)
+    base = code.decode_pmf(x, c["max_iters"])
+    for kw in (dict(slots=1), dict(slots=13), dict(use_graph=-1, slots=5)):
+        o = code.decode_pmf(x, c["max_iters"], **kw)
+        for k in ("hard", "ok", "iters"):
+            assert torch.equal(o[k], base[k]), (kw, k)
+    # row scale does not matter (rows are scaled to probabilities, reading R23)
+    o = code.decode_pmf(x * 3.5, c["max_iters"])
+    same = ((o["hard"] == base["hard"]).all(1) & (o["iters"] == base["iters"])).float().mean()
+    assert same.item() >= 0.95
+    # the LLR path on the same handle is unaffected by a pmf decode in between
+    _, llr, _ = config_inputs(name, 0, 32)
+    l1 = code.decode(torch.from_numpy(llr).to(dev), c["max_iters"])
+    code.decode_pmf(x, c["max_iters"])
+    l2 = code.decode(torch.from_numpy(llr).to(dev), c["max_iters"])
+    for k in ("hard", "ok", "iters"):
+        assert torch.equal(l1[k], l2[k])
+    # point masses on the sent (all-zero) codeword: converged at the first iteration
+    pm = torch.zeros_like(x[:4])
+    pm[..., 0] = 1.0
+    o = code.decode_pmf(pm.contiguous(), c["max_iters"], want_events=True)
+    assert (o["iters"] == 1).all() and (o["ok"] == 1).all() and not o["hard"].any()
+    # a row with zero sum is treated as uniform and counted as an event
+    z = x[:2].clone()
+    z[0, 5] = 0.0
+    o = code.decode_pmf(z, c["max_iters"], want_events=True)
+    assert int(o["events"][0]) >= 1 and int(o["events"][1]) == 0
+    # argument errors
+    with pytest.raises(ValueError):
+        code.decode_pmf(x[:, :, :-1].contiguous(), 10)
+    flat = torch.zeros(x[:1].numel() + 1, device=dev)
+    L = nb.lib()
+    h = torch.zeros((1, c["N"]), dtype=torch.uint8, device=dev)
+    k = torch.zeros(1, dtype=torch.uint8, device=dev)
+    i = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = L.nbldpc_decode_pmf(code._h, flat.data_ptr() + 4, 1, 10, h.data_ptr(), k.data_ptr(), i.data_ptr(),
+                             None, None)
+    assert st == -1  # misaligned pmf
