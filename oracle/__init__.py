@@ -97,7 +97,9 @@ def _lib():
                 sig["or_lf_decision" + sfx] = (None, [vp, dp, dp, dp, dp, dp, dp, dp])
                 sig["or_lf_decode" + sfx] = (None, [vp, dp, i32, i32, i32, dp, dp, dp, dp, dp])
                 sig["or_lf_decode_batch" + sfx] = (None, [vp, dp, i32, i32, i32, i32, dp, dp, dp, dp, dp, i32])
-                sig["or_lf_decode_batch_pmf" + sfx] = (None, [vp, dp, i32, i32, i32, i32, dp, dp, dp, dp, dp, i32])
+                sig["or_lf_decode_batch_ex" + sfx] = (None, [vp, dp, i32, i32, i32, i32, i32, dp, dp, dp, dp, dp, dp,
+                                                               dp, i32])
+                sig["or_lf_symbol_posterior" + sfx] = (None, [vp, dp, dp, dp, dp, dp, dp])
                 sig["or_lf_init_pmf" + sfx] = (None, [vp, dp, dp, dp])
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
@@ -351,45 +353,51 @@ class Code:
         getattr(self._L, "or_lf_decision" + sfx)(self._h, _p(S0), _p(L0), _p(Ws), _p(Wl), _p(x), _p(soft), _p(pb))
         return x, soft, pb
 
-    def lf_decode_batch(self, llr, max_iters: int, mode: int = EXACT, early_stop: bool = True,
-                        want_soft: bool = False, nthreads: int | None = None, f32: bool = False):
-        """Decode F frames (llr float32 [F][N*m]); returns dict of numpy arrays."""
+    def lf_symbol_posterior(self, S0, L0, Ws, Wl, f32=False):
+        """Symbol posterior mu_v / sum mu_v [N][q] and symbol-MAP decision [N]."""
         dt, sfx = self._real(f32)
-        llr = np.ascontiguousarray(llr, np.float32).reshape(-1, self.N * self.m)
-        F = llr.shape[0]
-        x = np.zeros((F, self.N), np.int32)
-        ok = np.zeros(F, np.int32)
-        it = np.zeros(F, np.int32)
-        ev = np.zeros(F, np.int32)
-        soft = np.zeros((F, self.N * self.m), dt) if want_soft else None
-        nt = nthreads or os.cpu_count() or 1
-        getattr(self._L, "or_lf_decode_batch" + sfx)(
-            self._h, _p(llr), F, int(max_iters), int(mode), int(bool(early_stop)), _p(x), _p(ok), _p(it),
-            _p(soft) if soft is not None else None, _p(ev), int(nt),
-        )
-        out = {"hard": x.astype(np.uint8) if self.q <= 256 else x, "ok": ok.astype(np.uint8), "iters": it,
-               "events": ev}
-        if soft is not None:
-            out["soft"] = soft
-        return out
+        S0, Ws = _u8(S0), _u8(Ws)
+        L0, Wl = np.ascontiguousarray(L0, dt), np.ascontiguousarray(Wl, dt)
+        post = np.zeros((self.N, self.q), dt)
+        xmap = np.zeros(self.N, np.int32)
+        getattr(self._L, "or_lf_symbol_posterior" + sfx)(self._h, _p(S0), _p(L0), _p(Ws), _p(Wl), _p(post), _p(xmap))
+        return post, xmap
 
-    def lf_decode_batch_pmf(self, pmf, max_iters: int, mode: int = EXACT, early_stop: bool = True,
-                            nthreads: int | None = None, f32: bool = False, want_soft: bool = False):
-        """Decode F frames from symbol-level channel pmfs (float32 [F][N][q])."""
+    def _decode_batch(self, inp, is_pmf, max_iters, mode, early_stop, want_soft, want_post, nthreads, f32):
         dt, sfx = self._real(f32)
-        pmf = np.ascontiguousarray(pmf, np.float32).reshape(-1, self.N * self.q)
-        F = pmf.shape[0]
+        row = self.N * (self.q if is_pmf else self.m)
+        inp = np.ascontiguousarray(inp, np.float32).reshape(-1, row)
+        F = inp.shape[0]
         x = np.zeros((F, self.N), np.int32)
         ok = np.zeros(F, np.int32)
         it = np.zeros(F, np.int32)
         ev = np.zeros(F, np.int32)
         soft = np.zeros((F, self.N * self.m), dt) if want_soft else None
+        post = np.zeros((F, self.N, self.q), dt) if want_post else None
+        xmap = np.zeros((F, self.N), np.int32) if want_post else None
         nt = nthreads or os.cpu_count() or 1
-        getattr(self._L, "or_lf_decode_batch_pmf" + sfx)(
-            self._h, _p(pmf), F, int(max_iters), int(mode), int(bool(early_stop)), _p(x), _p(ok), _p(it),
-            _p(soft) if soft is not None else None, _p(ev), int(nt),
+        opt = lambda a: _p(a) if a is not None else None  # noqa: E731
+        getattr(self._L, "or_lf_decode_batch_ex" + sfx)(
+            self._h, _p(inp), int(bool(is_pmf)), F, int(max_iters), int(mode), int(bool(early_stop)), _p(x), _p(ok),
+            _p(it), opt(soft), _p(ev), opt(post), opt(xmap), int(nt),
         )
         out = {"hard": x.astype(np.uint8), "ok": ok.astype(np.uint8), "iters": it, "events": ev}
         if soft is not None:
             out["soft"] = soft
+        if want_post:
+            out["post"] = post
+            out["map"] = xmap.astype(np.uint8)
         return out
+
+    def lf_decode_batch(self, llr, max_iters: int, mode: int = EXACT, early_stop: bool = True,
+                        want_soft: bool = False, nthreads: int | None = None, f32: bool = False,
+                        want_post: bool = False):
+        """Decode F frames (llr float32 [F][N*m]); returns dict of numpy arrays (hard, ok, iters,
+        events; soft [F][N*m]; post [F][N][q] and map [F][N] at the stopping iteration)."""
+        return self._decode_batch(llr, False, max_iters, mode, early_stop, want_soft, want_post, nthreads, f32)
+
+    def lf_decode_batch_pmf(self, pmf, max_iters: int, mode: int = EXACT, early_stop: bool = True,
+                            nthreads: int | None = None, f32: bool = False, want_soft: bool = False,
+                            want_post: bool = False):
+        """Decode F frames from symbol-level channel pmfs (float32 [F][N][q]); outputs as lf_decode_batch."""
+        return self._decode_batch(pmf, True, max_iters, mode, early_stop, want_soft, want_post, nthreads, f32)

@@ -131,3 +131,51 @@ def test_orthogonal_channel_pmf_decodes():
     # ... and decoding lowers the symbol error rate of the symbol-wise MAP decisions (N = 16 is
     # short, so some frames converge to a neighbouring codeword)
     assert (r["hard"] != 0).mean() < 0.5 * (pmf.argmax(2) != 0).mean()
+
+
+@pytest.mark.parametrize("m,N,k,seed,pmf_in", [(3, 12, 4, 51, False), (4, 12, 3, 52, True), (2, 16, 4, 53, True)])
+def test_symbol_posterior_equals_sp_posterior(m, N, k, seed, pmf_in):
+    # mu_v = IWHT-side sum of M_v is SP's posterior (Appendix lemma); map = argmax
+    code = _code(m, N, k, seed)
+    q = 1 << m
+    rng = np.random.default_rng(seed)
+    if pmf_in:
+        pmf = rng.random((N, q)) ** 4 + 1e-3
+        p0 = pmf / pmf.sum(1, keepdims=True)
+        S0, L0 = code.lf_init_pmf(pmf)
+    else:
+        llr = rng.normal(1.0, 2.0, N * m)
+        p0 = code.sp_init(llr)
+        S0, L0 = code.lf_init(llr)
+    _, ecol, _ = code.edges()
+    u, Us, Ul = p0[ecol].copy(), S0[ecol].copy(), L0[ecol].copy()
+    for _ in range(4):
+        w = code.sp_check_to_variable(u)
+        Ws, Wl = code.lf_check_to_variable(Us, Ul)
+        qv = code.sp_posterior(p0, w)
+        post, xmap = code.lf_symbol_posterior(S0, L0, Ws, Wl)
+        np.testing.assert_allclose(post, qv, rtol=1e-8, atol=1e-12)
+        top2 = np.sort(qv, 1)[:, -2:]
+        clear = top2[:, 1] - top2[:, 0] > 1e-9
+        assert np.array_equal(xmap[clear], qv.argmax(1)[clear])
+        u = code.sp_variable_to_check(p0, w)
+        Us, Ul, _ = code.lf_variable_to_check(S0, L0, Ws, Wl)
+
+
+def test_symbol_posterior_exact_on_tree():
+    m, N, rows, cols = 2, 7, [0, 0, 0, 1, 1, 1, 2, 2, 2], [0, 1, 2, 2, 3, 4, 4, 5, 6]
+    q = 1 << m
+    rng = np.random.default_rng(91)
+    coeffs = rng.integers(1, q, len(rows))
+    code = oracle.Code(oracle.Field(m, DEFAULT_POLY[m]), 3, N, rows, cols, coeffs)
+    cw = enumerate_codewords(3, N, m, DEFAULT_POLY[m], rows, cols, coeffs)
+    pmf = (rng.random((N, q)) ** 2 + 1e-2).astype(np.float32)
+    pri = pmf.astype(np.float64)
+    wgt = np.prod([pri[v, cw[:, v]] for v in range(N)], axis=0)
+    post = np.zeros((N, q))
+    for v in range(N):
+        np.add.at(post[v], cw[:, v], wgt)
+    post /= post.sum(1, keepdims=True)
+    r = code.lf_decode_batch_pmf(pmf[None], max_iters=4, early_stop=False, want_post=True)
+    np.testing.assert_allclose(r["post"][0], post, rtol=1e-9, atol=1e-13)
+    assert np.array_equal(r["map"][0], post.argmax(1))
