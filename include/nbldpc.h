@@ -72,6 +72,14 @@ typedef struct {
   int use_graph;     /* 0 = default (CUDA graph with a device-side WHILE loop), 1 = force graph,
                         -1 = host-driven launch loop */
   int vn_algorithm;  /* nbldpc_vn_algorithm_t, default NBLDPC_VN_SEPARABLE */
+  float* symbol_post_out;   /* device, 16-byte aligned, [frames][N][2^m] or NULL: the symbol posterior
+                               mu_v(x) / sum_x mu_v(x), mu_v(x) = sum_z M_v(z) (-1)^{z.x}, at the
+                               stopping iteration */
+  uint8_t* symbol_map_out;  /* device, [frames][N] or NULL: argmax_x mu_v(x), ties -> lowest x
+                               (the paper's symbol-level TENTATIVE DECISION) */
+  /* Either symbol output selects the direct kernel (NBLDPC_VN_DIRECT): the symbol decision is
+   * evaluated at every iteration (the stopping one is not known in advance), 2 WHTs of size 2^m
+   * per variable, plus N*2^m*4 + N bytes per resident slot allocated on first use. */
 } nbldpc_decode_opts_t;
 
 /* Builds a code from H given as nnz (row, col, coefficient) triplets in any order.

@@ -38,7 +38,8 @@ class NbldpcError(RuntimeError):
 class _Opts(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_size_t), ("syndrome_mode", ctypes.c_int), ("no_early_stop", ctypes.c_int),
                 ("soft_out", ctypes.c_void_p), ("events_out", ctypes.c_void_p), ("slots", ctypes.c_int),
-                ("use_graph", ctypes.c_int), ("vn_algorithm", ctypes.c_int)]
+                ("use_graph", ctypes.c_int), ("vn_algorithm", ctypes.c_int), ("symbol_post_out", ctypes.c_void_p),
+                ("symbol_map_out", ctypes.c_void_p)]
 
 
 def header_symbols() -> list[str]:
@@ -142,7 +143,8 @@ class Code:
     def slot_bytes(self) -> int:
         return int(self._L.nbldpc_slot_bytes(self._h))
 
-    def _opts(self, syndrome_mode=0, early_stop=True, soft=None, events=None, slots=0, use_graph=0, vn_algorithm=0):
+    def _opts(self, syndrome_mode=0, early_stop=True, soft=None, events=None, slots=0, use_graph=0, vn_algorithm=0,
+              post=None, xmap=None):
         o = _Opts()
         o.struct_size = ctypes.sizeof(_Opts)
         o.syndrome_mode = int(syndrome_mode)
@@ -152,12 +154,31 @@ class Code:
         o.slots = int(slots)
         o.use_graph = int(use_graph)
         o.vn_algorithm = int(vn_algorithm)
+        o.symbol_post_out = _ptr(post)
+        o.symbol_map_out = _ptr(xmap)
         return o
 
+    def _outputs(self, F, dev, want_soft, want_events, want_post):
+        import torch
+
+        out = {"hard": torch.empty((F, self.N), dtype=torch.uint8, device=dev),
+               "ok": torch.empty(F, dtype=torch.uint8, device=dev),
+               "iters": torch.empty(F, dtype=torch.int32, device=dev)}
+        if want_soft:
+            out["soft"] = torch.empty((F, self.N * self.m), dtype=torch.float32, device=dev)
+        if want_events:
+            out["events"] = torch.empty(F, dtype=torch.int32, device=dev)
+        if want_post:
+            out["post"] = torch.empty((F, self.N, self.q), dtype=torch.float32, device=dev)
+            out["map"] = torch.empty((F, self.N), dtype=torch.uint8, device=dev)
+        return out
+
     def decode(self, llr, max_iters: int, *, syndrome_mode: int = 0, early_stop: bool = True, want_soft=False,
-               want_events=False, slots: int = 0, use_graph: int = 0, vn_algorithm: int = 0, out=None, stream=None):
+               want_events=False, want_post=False, slots: int = 0, use_graph: int = 0, vn_algorithm: int = 0, out=None,
+               stream=None):
         """Decode frames. ``llr``: CUDA float32 tensor [F, N*m].  Returns a dict of CUDA tensors
-        (hard uint8 [F,N], ok uint8 [F], iters int32 [F], optional soft float32 [F,N*m], events int32 [F])."""
+        (hard uint8 [F,N], ok uint8 [F], iters int32 [F], optional soft float32 [F,N*m], events int32 [F],
+        post float32 [F,N,q] symbol posterior and map uint8 [F,N] symbol-MAP decision)."""
         import torch
 
         if not (llr.is_cuda and llr.dtype == torch.float32 and llr.is_contiguous()):
@@ -165,16 +186,10 @@ class Code:
         F = llr.numel() // (self.N * self.m)
         if F * self.N * self.m != llr.numel() or F < 1:
             raise ValueError("llr size is not a multiple of N*m")
-        dev = llr.device
         if out is None:
-            out = {"hard": torch.empty((F, self.N), dtype=torch.uint8, device=dev),
-                   "ok": torch.empty(F, dtype=torch.uint8, device=dev),
-                   "iters": torch.empty(F, dtype=torch.int32, device=dev)}
-            if want_soft:
-                out["soft"] = torch.empty((F, self.N * self.m), dtype=torch.float32, device=dev)
-            if want_events:
-                out["events"] = torch.empty(F, dtype=torch.int32, device=dev)
-        o = self._opts(syndrome_mode, early_stop, out.get("soft"), out.get("events"), slots, use_graph, vn_algorithm)
+            out = self._outputs(F, llr.device, want_soft, want_events, want_post)
+        o = self._opts(syndrome_mode, early_stop, out.get("soft"), out.get("events"), slots, use_graph, vn_algorithm,
+                       out.get("post"), out.get("map"))
         st = self._L.nbldpc_decode_ex(self._h, llr.data_ptr(), F, int(max_iters), out["hard"].data_ptr(),
                                       out["ok"].data_ptr(), out["iters"].data_ptr(), _stream(stream),
                                       ctypes.byref(o))
@@ -182,7 +197,7 @@ class Code:
         return out
 
     def decode_pmf(self, pmf, max_iters: int, *, syndrome_mode: int = 0, early_stop: bool = True, want_soft=False,
-                   want_events=False, slots: int = 0, use_graph: int = 0, out=None, stream=None):
+                   want_events=False, want_post=False, slots: int = 0, use_graph: int = 0, out=None, stream=None):
         """Decode frames from symbol-level channel pmfs (nbldpc_decode_pmf).
         ``pmf``: CUDA float32 tensor [F, N, q] (any positive scale per row).  Same outputs as decode."""
         import torch
@@ -192,16 +207,10 @@ class Code:
         F = pmf.numel() // (self.N * self.q)
         if F * self.N * self.q != pmf.numel() or F < 1:
             raise ValueError("pmf size is not a multiple of N*q")
-        dev = pmf.device
         if out is None:
-            out = {"hard": torch.empty((F, self.N), dtype=torch.uint8, device=dev),
-                   "ok": torch.empty(F, dtype=torch.uint8, device=dev),
-                   "iters": torch.empty(F, dtype=torch.int32, device=dev)}
-            if want_soft:
-                out["soft"] = torch.empty((F, self.N * self.m), dtype=torch.float32, device=dev)
-            if want_events:
-                out["events"] = torch.empty(F, dtype=torch.int32, device=dev)
-        o = self._opts(syndrome_mode, early_stop, out.get("soft"), out.get("events"), slots, use_graph, 1)
+            out = self._outputs(F, pmf.device, want_soft, want_events, want_post)
+        o = self._opts(syndrome_mode, early_stop, out.get("soft"), out.get("events"), slots, use_graph, 1,
+                       out.get("post"), out.get("map"))
         st = self._L.nbldpc_decode_pmf(self._h, pmf.data_ptr(), F, int(max_iters), out["hard"].data_ptr(),
                                        out["ok"].data_ptr(), out["iters"].data_ptr(), _stream(stream),
                                        ctypes.byref(o))

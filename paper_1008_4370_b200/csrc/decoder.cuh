@@ -67,6 +67,10 @@ struct CallDev {            // per-call arguments, written on the stream before 
   int pad[3];
   const float* pmf;   // nbldpc_decode_pmf: [frames][N][q] channel pmf (else NULL)
   float* p0buf;       // nbldpc_decode_pmf: [S][N][q] P_v^0 = WHT(pmf) / sum(pmf) per slot
+  float* post_out;    // symbol posterior [frames][N][q] (or NULL)
+  uint8_t* map_out;   // symbol-MAP decision [frames][N] (or NULL)
+  float* post_buf;    // [S][N][q] per-slot posterior of the latest iteration
+  uint8_t* map_buf;   // [S][N]
 };
 
 struct WorkDev {
@@ -208,6 +212,32 @@ __device__ __forceinline__ void bfly_regs(float (&x)[R], const float* th) {
   if constexpr (I < LR) {
     bfly_reg<R, I>(x, th[I]);
     bfly_regs<R, I + 1, LR>(x, th);
+  }
+}
+
+// In-place Walsh-Hadamard transform x(z) <- sum_y x(y) (-1)^{z.y} of a vector spread over a team of
+// TT = 2^(MB-LR) consecutive lanes holding R = 2^LR entries each (entry t*R + zl in x[zl] of team
+// lane t): LR stages in registers, MB - LR across the team by shuffles.  Every lane of the warp
+// must call it (full-mask shuffles).
+template <int MB, int LR, int R>
+__device__ __forceinline__ void wht_team(float (&x)[R], int t) {
+#pragma unroll
+  for (int b = 0; b < LR; ++b)
+#pragma unroll
+    for (int zl = 0; zl < R; ++zl)
+      if (!(zl & (1 << b))) {
+        const float u = x[zl], w = x[zl | (1 << b)];
+        x[zl] = u + w;
+        x[zl | (1 << b)] = u - w;
+      }
+#pragma unroll
+  for (int b = LR; b < MB; ++b) {
+    const int off = 1 << (b - LR);
+#pragma unroll
+    for (int zl = 0; zl < R; ++zl) {
+      const float o = __shfl_xor_sync(0xffffffffu, x[zl], off);
+      x[zl] = (t & off) ? o - x[zl] : x[zl] + o;
+    }
   }
 }
 
@@ -376,24 +406,7 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
         for (int zl = 0; zl < R; ++zl) p0[zl] = active ? __ldcg(src + t * R + zl) : 0.0f;
       }
       if (ell == 0) {
-#pragma unroll
-        for (int b = 0; b < LR; ++b)
-#pragma unroll
-          for (int zl = 0; zl < R; ++zl)
-            if (!(zl & (1 << b))) {
-              const float u = p0[zl], w = p0[zl | (1 << b)];
-              p0[zl] = u + w;
-              p0[zl | (1 << b)] = u - w;
-            }
-#pragma unroll
-        for (int b = LR; b < MB; ++b) {
-          const int off = 1 << (b - LR);
-#pragma unroll
-          for (int zl = 0; zl < R; ++zl) {
-            const float o = __shfl_xor_sync(0xffffffffu, p0[zl], off);
-            p0[zl] = (t & off) ? o - p0[zl] : p0[zl] + o;
-          }
-        }
+        wht_team<MB, LR, R>(p0, t);
         float tot = p0[0];
         if constexpr (TT > 1) tot = __shfl_sync(0xffffffffu, p0[0], lane & ~(TT - 1));
         const float inv = tot > 0.0f ? 1.0f / tot : 0.0f;  // degenerate row: all zero -> event below
@@ -610,6 +623,52 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
             ws.soft[((size_t)s * cd.N + ed.var) * MB + b] = (float)(log(fabs(mv[b + 1])) - l0);
         }
       }
+      if constexpr (DIRECT) {
+        if (call->post_buf != nullptr) {
+          // symbol-level decision: mu_v(x) = sum_z M_v(z) (-1)^{z.x} with
+          // M_v = raw (*) W_e, i.e. mu_v = WHT(raw) . WHT(W_e) (the XOR-convolution theorem);
+          // clamped at 0 and normalised to a posterior, argmax ties -> lowest x
+          float a[R], b[R];
+#pragma unroll
+          for (int zl = 0; zl < R; ++zl) a[zl] = raw[zl];
+          if constexpr (TT == 1) {
+#pragma unroll
+            for (int y = 0; y < Q; ++y) b[y] = is_a ? dreg[y] : 0.0f;
+          } else {
+#pragma unroll
+            for (int c4 = 0; c4 < R / 4; ++c4) {
+              float4 v = is_a ? *reinterpret_cast<const float4*>(D + cm_idx<MB>(t * R + 4 * c4)) : make_float4(0, 0, 0, 0);
+              b[4 * c4] = v.x; b[4 * c4 + 1] = v.y; b[4 * c4 + 2] = v.z; b[4 * c4 + 3] = v.w;
+            }
+          }
+          wht_team<MB, LR, R>(a, t);
+          wht_team<MB, LR, R>(b, t);
+          float tot = 0.0f, best = 0.0f;
+          int bx = 0;
+#pragma unroll
+          for (int zl = 0; zl < R; ++zl) {
+            a[zl] = fmaxf(a[zl] * b[zl], 0.0f);  // mu >= 0; rounding residues below 0 clamp to 0
+            tot += a[zl];
+            if (zl == 0 || a[zl] > best) { best = a[zl]; bx = t * R + zl; }
+          }
+          if constexpr (TT > 1) {
+#pragma unroll
+            for (int off = TT / 2; off >= 1; off >>= 1) {
+              tot += __shfl_xor_sync(0xffffffffu, tot, off);
+              const float ob = __shfl_xor_sync(0xffffffffu, best, off);
+              const int ox = __shfl_xor_sync(0xffffffffu, bx, off);
+              if (ob > best || (ob == best && ox < bx)) { best = ob; bx = ox; }
+            }
+          }
+          if (is_a) {
+            const float inv = tot > 0.0f ? 1.0f / tot : 0.0f;
+            float* dst = call->post_buf + ((size_t)s * cd.N + ed.var) * Q + t * R;
+#pragma unroll
+            for (int zl = 0; zl < R; ++zl) dst[zl] = a[zl] * inv;
+            if (t == 0) call->map_buf[(size_t)s * cd.N + ed.var] = (uint8_t)bx;
+          }
+        }
+      }
       if (mode == 1) {
         // paper-mode fast syndrome: sign bits of M_v(H_cv alpha^i) for both checks
         uint64_t pa = 0, pbv = 0;
@@ -762,6 +821,21 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
 #pragma unroll 4
       for (int i = lane; i < N * MB; i += 32)
         call->soft_out[(size_t)f * N * MB + i] = __ldcg(&ws.soft[(size_t)s * N * MB + i]);
+    }
+    if (call->post_buf != nullptr) {
+      if (call->post_out) {
+        const float4* src = reinterpret_cast<const float4*>(call->post_buf + (size_t)s * N * Q);
+        float4* dst = reinterpret_cast<float4*>(call->post_out + (size_t)f * N * Q);
+        if constexpr (Q >= 4) {
+#pragma unroll 4
+          for (int i = lane; i < N * Q / 4; i += 32) dst[i] = __ldcg(src + i);
+        } else {
+          for (int i = lane; i < N * Q; i += 32)
+            call->post_out[(size_t)f * N * Q + i] = __ldcg(call->post_buf + (size_t)s * N * Q + i);
+        }
+      }
+      if (call->map_out)
+        for (int v = lane; v < N; v += 32) call->map_out[(size_t)f * N + v] = __ldcg(&call->map_buf[(size_t)s * N + v]);
     }
     if (lane == 0) {
       call->ok[f] = (uint8_t)ok;

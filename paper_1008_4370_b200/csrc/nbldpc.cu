@@ -45,6 +45,8 @@ struct Workspace {
   size_t out_stage_bytes = 0;
   float* p0buf = nullptr;  // nbldpc_decode_pmf: [S][N][q] channel spectra
   size_t p0buf_bytes = 0;
+  float* postbuf = nullptr;  // symbol outputs: [S][N][q] posterior, then [S][N] MAP bytes
+  size_t postbuf_bytes = 0;
   // launch accounting of the most recent decode
   cudaStream_t last_stream = nullptr;
   int last_graph = 0;
@@ -130,6 +132,7 @@ void free_workspace(Workspace& w) {
   if (w.llr_stage) cudaFree(w.llr_stage);
   if (w.out_stage) cudaFree(w.out_stage);
   if (w.p0buf) cudaFree(w.p0buf);
+  if (w.postbuf) cudaFree(w.postbuf);
   w = Workspace{};
 }
 
@@ -474,6 +477,8 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   int mode = 0, early = 1, slots = 0, use_graph = 0, direct = 0;
   float* soft = nullptr;
   int32_t* events = nullptr;
+  float* post = nullptr;
+  uint8_t* xmap = nullptr;
   if (opts) {
     if (opts->struct_size < sizeof(nbldpc_decode_opts_t)) return NBLDPC_ERR_INVALID_ARGUMENT;
     mode = opts->syndrome_mode;
@@ -483,10 +488,15 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
     slots = opts->slots;
     use_graph = opts->use_graph;
     direct = opts->vn_algorithm;
+    post = opts->symbol_post_out;
+    xmap = opts->symbol_map_out;
   }
+  if ((post && (!is_device_ptr(post) || ((uintptr_t)post & 15))) || (xmap && !is_device_ptr(xmap)))
+    return NBLDPC_ERR_INVALID_ARGUMENT;
   if (mode != 0 && mode != 1) return NBLDPC_ERR_INVALID_ARGUMENT;
   if (direct != 0 && direct != 1) return NBLDPC_ERR_INVALID_ARGUMENT;
   if (pmf) direct = 2;
+  else if ((post || xmap) && direct == 0) direct = 1;  // the symbol decision lives in the direct kernel
   if (slots < 0) return NBLDPC_ERR_INVALID_ARGUMENT;
   if ((soft && !is_device_ptr(soft)) || (events && !is_device_ptr(events))) return NBLDPC_ERR_INVALID_ARGUMENT;
   int S = slots > 0 ? std::min(slots, frames) : default_slots(c, frames);
@@ -510,6 +520,24 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
     }
     call.pmf = pmf;
     call.p0buf = w.p0buf;
+  }
+  if (post || xmap) {
+    const size_t pb = align_up((size_t)S * c->N * c->q * sizeof(float), 256);
+    const size_t need = pb + (size_t)S * c->N;
+    if (w.postbuf_bytes < need) {
+      if (w.postbuf) {
+        NB_TRY(cudaStreamSynchronize(st));
+        cudaFree(w.postbuf);
+        w.postbuf = nullptr;
+        w.postbuf_bytes = 0;
+      }
+      NB_TRY(cudaMalloc(&w.postbuf, need));
+      w.postbuf_bytes = need;
+    }
+    call.post_out = post;
+    call.map_out = xmap;
+    call.post_buf = w.postbuf;
+    call.map_buf = reinterpret_cast<uint8_t*>(w.postbuf) + pb;
   }
   call.llr = llr;
   call.hard = hard;

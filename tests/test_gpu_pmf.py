@@ -165,3 +165,56 @@ def test_pmf_invariance_and_edge_cases(dev):
     st = L.nbldpc_decode_pmf(code._h, flat.data_ptr() + 4, 1, 10, h.data_ptr(), k.data_ptr(), i.data_ptr(),
                              None, None)
     assert st == -1  # misaligned pmf
+
+
+POST_CASES = [
+    # name, input, Eb/N0 or LLR point, gpu frames, oracle sample
+    ("C1", "llr", 0, 64, 32),
+    ("C5", "pmf", 3.5, 128, 8),
+    ("C2", "pmf", 0.5, 64, 4),
+    ("C3", "llr", 0, 32, 3),
+]
+
+
+@pytest.mark.parametrize("name,kind,pt,F,nsample", POST_CASES)
+def test_symbol_posterior_and_map_parity(dev, name, kind, pt, F, nsample):
+    # symbol-level TENTATIVE DECISION at the stopping iteration (reading R24):
+    # per frame the posterior is within 1e-4 of the fp64 oracle or no further than twice the
+    # oracle's own fp32 twin (the message state carries fp32 rounding into an uncertain posterior),
+    # over the sample no further than the twin in total; MAP equal where the top two are apart
+    c = synth.CONFIGS[name]
+    code = gpu_code(name)
+    ocode = oracle_code(name)
+    if kind == "pmf":
+        x, _ = _pmf_inputs(name, F, pt)
+        out = code.decode_pmf(torch.from_numpy(x).to(dev), c["max_iters"], want_post=True)
+        plain = code.decode_pmf(torch.from_numpy(x).to(dev), c["max_iters"])
+    else:
+        _, x, _ = config_inputs(name, 0, F, point=pt)
+        out = code.decode(torch.from_numpy(x).to(dev), c["max_iters"], want_post=True)
+        plain = code.decode(torch.from_numpy(x).to(dev), c["max_iters"], vn_algorithm=1)
+    for k in ("hard", "ok", "iters"):  # the symbol outputs do not perturb the decode
+        assert torch.equal(out[k], plain[k]), k
+    idx = np.sort(np.random.default_rng(3).choice(F, nsample, replace=False))
+    dec = ocode.lf_decode_batch_pmf if kind == "pmf" else ocode.lf_decode_batch
+    ref = dec(x[idx], c["max_iters"], want_post=True)
+    twin = dec(x[idx], c["max_iters"], want_post=True, f32=True)
+    post = out["post"].cpu().numpy()[idx]
+    xmap = out["map"].cpu().numpy()[idx]
+    it = out["iters"].cpu().numpy()[idx]
+    checked, eg_tot, et_tot = 0, 0.0, 0.0
+    for n in range(len(idx)):
+        stable = np.array_equal(twin["hard"][n], ref["hard"][n]) and twin["iters"][n] == ref["iters"][n]
+        if not stable or it[n] != ref["iters"][n]:
+            continue
+        checked += 1
+        np.testing.assert_allclose(post[n].sum(1), 1.0, atol=1e-4)
+        eg = np.abs(post[n] - ref["post"][n]).max()
+        et = np.abs(twin["post"][n] - ref["post"][n]).max()
+        assert eg <= max(1e-4, 2.0 * et), (n, eg, et)
+        eg_tot, et_tot = eg_tot + eg, et_tot + et
+        top2 = np.sort(ref["post"][n], 1)[:, -2:]
+        clear = top2[:, 1] - top2[:, 0] > 2.0 * max(1e-4, 2.0 * et)
+        assert np.array_equal(xmap[n][clear], ref["map"][n][clear])
+    assert checked >= max(1, (len(idx) * 3) // 4)
+    assert eg_tot <= max(1e-4 * checked, 1.25 * et_tot)
