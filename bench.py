@@ -51,20 +51,30 @@ def hbm_peak():
         return HBM_PEAK_FALLBACK, "fallback"
 
 
-def per_frame_iter(cfg, vn):
-    """Algorithmic work of one frame-iteration: SFU ops, FP32 FMAs, message bytes."""
+def per_frame_iter(cfg, vn, inp="llr", symbol_out=False):
+    """Algorithmic work of one frame-iteration: SFU ops, FP32 FMAs, message bytes.
+    inp = "pmf": the channel spectrum is a q-vector per variable (read per iteration from the slot
+    buffer) instead of m channel terms; symbol_out: + the symbol posterior written per iteration
+    and its two WHTs (counted as FMA-pipe ops)."""
     N, q, m = cfg["N"], cfg["q"], cfg["m"]
     E = 2 * N
     mufu = 2 * E * q + N * q                        # ex2 of every VN input entry, lg2 of every output, ex2 of W_a
-    fma = (E * m * q if vn == 0 else E * q * q) + N * (m + 1) * q  # VN (separable / direct) + decision points
-    bytes_ = 2 * E * q * 4 + 4 * N * m + N           # one message set read + written, channel terms, symbols
+    if inp == "pmf":  # probability-domain VN: 2 WHTs (m q add/sub each) and a product per entry
+        fma = E * q * (2 * m + 1) + N * (m + 1) * q
+    else:             # VN (separable / direct) + decision points
+        fma = (E * m * q if vn == 0 else E * q * q) + N * (m + 1) * q
+    bytes_ = 2 * E * q * 4 + N                       # one message set read + written, symbols
+    bytes_ += 4 * N * q if inp == "pmf" else 4 * N * m  # channel spectrum / channel terms
+    if symbol_out:
+        fma += N * q * (2 * m + 1)
+        bytes_ += 4 * N * q + N
     return mufu, fma, bytes_
 
 
-def roofline(cfg, vn, frame_iters, seconds, traffic):
+def roofline(cfg, vn, frame_iters, seconds, traffic, inp="llr", symbol_out=False):
     """The slower of the SFU, FP32 and HBM-message-byte bounds (BASELINE.json north_star) for the
     work done; achieved / peak of that resource over the measured kernel time."""
-    mufu, fma, byts = per_frame_iter(cfg, vn)
+    mufu, fma, byts = per_frame_iter(cfg, vn, inp, symbol_out)
     hbm, hbm_src = hbm_peak()
     t = {"alu": max(mufu / MUFU_PEAK, fma / FMA_PEAK), "hbm": byts / hbm}
     bound = max(t, key=t.get)
@@ -92,13 +102,22 @@ def roofline(cfg, vn, frame_iters, seconds, traffic):
     return r
 
 
+def channel_input(cfg, inp, point, ebn0, frame0, nframes):
+    """LLRs [F][N*m] (BPSK/AWGN) or symbol pmfs [F][N][q] (q-ary orthogonal signalling over AWGN)."""
+    if inp == "pmf":
+        return synth.config_pmf(cfg["name"], frame0, nframes, ebn0_db=ebn0, point=point)
+    return synth.config_llr(cfg["name"], frame0, nframes, ebn0_db=ebn0, point=point)
+
+
 def info_bits(cfg) -> float:
     return cfg["N"] * cfg["m"] * cfg["rate"]
 
 
-def workload_name(cfg, point):
+def workload_name(cfg, point, inp="llr", ebn0=None):
+    eb = cfg["ebn0"][point] if ebn0 is None else ebn0
+    ch = "BPSK/AWGN bit LLRs" if inp == "llr" else f"{cfg['q']}-ary orthogonal signalling/AWGN symbol pmfs"
     return (f"{cfg['name']}: GF({cfg['q']}) (2,{cfg['k']})-regular N={cfg['N']} rate {cfg['rate']:.4g}, "
-            f"Eb/N0={cfg['ebn0'][point]} dB, max {cfg['max_iters']} iters, early stop, "
+            f"{ch}, Eb/N0={eb} dB, max {cfg['max_iters']} iters, early stop, "
             f"{'random' if cfg['codeword'] == 'random' else 'all-zero'} codewords")
 
 
@@ -146,16 +165,17 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_oracle_run(cfg, point, frame0, nframes, threads=None):
+def cpu_oracle_run(cfg, point, frame0, nframes, threads=None, inp="llr", ebn0=None, symbol_out=False):
     """Times the oracle (as it stands) on frames frame0.. of the workload; returns (value, seconds, iters)."""
     import oracle
 
     M, rows, cols, coeffs = synth.config_code(cfg["name"])
     code = oracle.Code(oracle.Field(cfg["m"], cfg["poly"]), M, cfg["N"], rows, cols, coeffs)
-    llr = synth.config_llr(cfg["name"], frame0, nframes, point=point)
+    x = channel_input(cfg, inp, point, ebn0, frame0, nframes)
     nt = threads or os.cpu_count() or 1
+    dec = code.lf_decode_batch_pmf if inp == "pmf" else code.lf_decode_batch
     t0 = time.perf_counter()
-    r = code.lf_decode_batch(llr, cfg["max_iters"], nthreads=nt)
+    r = dec(x, cfg["max_iters"], nthreads=nt, want_post=symbol_out)
     dt = time.perf_counter() - t0
     it = int(r["iters"].sum())
     return info_bits(cfg) * it / dt, dt, it, nt
@@ -168,7 +188,8 @@ def run_reference(args, cfg):
     vals, dts = [], []
     nframes = args.ref_frames
     for i in range(args.warmup + args.steps):
-        v, dt, it, nt = cpu_oracle_run(cfg, args.point, i * nframes, nframes)
+        v, dt, it, nt = cpu_oracle_run(cfg, args.point, i * nframes, nframes, inp=args.input, ebn0=args.ebn0,
+                                       symbol_out=args.symbol_out)
         if i >= args.warmup:
             vals.append(v)
             dts.append(dt)
@@ -178,7 +199,7 @@ def run_reference(args, cfg):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(dts) / len(dts),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(cfg, args.point), "frames_per_step": nframes,
+        "config": {"workload": workload_name(cfg, args.point, args.input, args.ebn0), "frames_per_step": nframes,
                    "sample": f"{nframes} frames per step (frames i*{nframes}.. of the seeded stream)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nt, "kind": "oracle",
                          "sample": f"{nframes} frames per step x {args.steps} steps, fp64 C oracle, OpenMP"},
@@ -200,6 +221,10 @@ def main():
     ap.add_argument("--slots", type=int, default=0)
     ap.add_argument("--graph", type=int, default=0, help="direct path only: 0 graph, -1 host loop")
     ap.add_argument("--vn", type=int, default=0, help="0 separable (default), 1 direct q^2 convolution")
+    ap.add_argument("--input", default="llr", choices=["llr", "pmf"],
+                    help="llr: BPSK bit LLRs (nbldpc_decode); pmf: symbol pmfs (nbldpc_decode_pmf)")
+    ap.add_argument("--ebn0", type=float, default=None, help="override the config's Eb/N0 (dB)")
+    ap.add_argument("--symbol-out", action="store_true", help="also output the symbol posterior and MAP decision")
     ap.add_argument("--ref-frames", type=int, default=32)
     ap.add_argument("--cpu-frames", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -231,12 +256,15 @@ def main():
     f0, f1 = shard.frame_range(rank, world, F)
     M, rows, cols, coeffs = synth.config_code(cfg["name"])
     code = nb.Code(cfg["m"], cfg["poly"], M, cfg["N"], rows, cols, coeffs)
-    llr_np = synth.config_llr(cfg["name"], f0, f1 - f0, point=args.point)
+    pmf_in = args.input == "pmf"
+    vn = 1 if args.symbol_out else args.vn  # the symbol outputs run the slot-pass kernel
+    llr_np = channel_input(cfg, args.input, args.point, args.ebn0, f0, f1 - f0)
     llr_host = torch.from_numpy(llr_np).pin_memory()
     llr = llr_host.to(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
-    kw = dict(slots=args.slots, use_graph=args.graph, vn_algorithm=args.vn)
+    kw = dict(slots=args.slots, use_graph=args.graph, want_post=args.symbol_out, vn_algorithm=vn)
+    decode = code.decode_pmf if pmf_in else code.decode
 
     def barrier():
         if dist is not None:
@@ -245,7 +273,7 @@ def main():
 
     warm = max(3, args.warmup)
     for _ in range(warm):
-        out = code.decode(llr, cfg["max_iters"], **kw)
+        out = decode(llr, cfg["max_iters"], **kw)
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -256,7 +284,7 @@ def main():
         flush.fill_(1)  # L2 flush (untimed)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        out = code.decode(llr, cfg["max_iters"], **kw)
+        out = decode(llr, cfg["max_iters"], **kw)
         e1.record(stream)
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
@@ -267,8 +295,29 @@ def main():
     clk = clocks.stop()
 
     # end to end through the host-buffer C-ABI entry (H2D + decode + D2H inside the timed region)
-    e2e_ms, e2e_iters = 0.0, 0
-    if not args.no_e2e:
+    e2e_ms, e2e_iters, d2h = 0.0, 0, F * cfg["N"] + F + 4 * F
+    if not args.no_e2e and (pmf_in or args.symbol_out):
+        # through the Python binding: pinned H2D copy of the inputs, decode, D2H of every output
+        if args.symbol_out:
+            d2h += F * cfg["N"] * (4 * cfg["q"] + 1)
+        host_out = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in out.items()}
+        dev_in = torch.empty_like(llr)
+        barrier()
+        for i in range(args.steps + 1):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dev_in.copy_(llr_host, non_blocking=True)
+            o = decode(dev_in, cfg["max_iters"], **kw)
+            for k in o:
+                host_out[k].copy_(o[k], non_blocking=True)
+            torch.cuda.synchronize()
+            if i > 0:  # the first call is an untimed warm-up of the staging path
+                e2e_ms += 1e3 * (time.perf_counter() - t0)
+                e2e_iters += int(host_out["iters"].sum())
+        barrier()
+    elif not args.no_e2e:
+        kw.pop("want_post")
         code.decode_host(llr_host, cfg["max_iters"], **kw)
         barrier()
         for _ in range(args.steps):
@@ -293,20 +342,22 @@ def main():
     traffic = None
     if os.path.exists(args.traffic):
         try:
-            traffic = json.load(open(args.traffic)).get(f"{cfg['name']}:vn{args.vn}")
+            key = f"{cfg['name']}:vn{vn}" + (":pmf" if pmf_in else "") + (":sym" if args.symbol_out else "")
+            traffic = json.load(open(args.traffic)).get(key)
         except (OSError, ValueError):
             traffic = None
     # this rank's kernel: its frame-iterations over its own device time
-    roof = roofline(cfg, args.vn, iters_sum, sum(step_ms) * 1e-3, traffic)
+    roof = roofline(cfg, vn, iters_sum, sum(step_ms) * 1e-3, traffic, args.input, args.symbol_out)
     roof["kernel"] = ("lf_cluster_kernel (one launch per step + a 1-block setup kernel; "
-                      "CUDA events around the step)") if args.vn == 0 else "nb_pass_kernel (direct q^2 convolution)"
+                      "CUDA events around the step)") if vn == 0 else "nb_pass_kernel (slot passes)"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": warm, "ms_per_step": tim["ms"] / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": workload_name(cfg, args.point), "frames_per_gpu": F, "global_frames": F * world,
-                   "N": cfg["N"], "q": cfg["q"], "k": cfg["k"], "max_iters": cfg["max_iters"],
-                   "vn_algorithm": ["separable", "direct"][args.vn],
+        "config": {"workload": workload_name(cfg, args.point, args.input, args.ebn0), "frames_per_gpu": F,
+                   "global_frames": F * world, "N": cfg["N"], "q": cfg["q"], "k": cfg["k"],
+                   "max_iters": cfg["max_iters"], "vn_algorithm": ["separable", "direct"][vn],
+                   "input": args.input, "symbol_outputs": bool(args.symbol_out),
                    "parallelism": f"frames sharded over {world} GPU(s), no collective in the loop",
                    "l2": "flushed (256 MiB write) before every timed step",
                    "slots": args.slots or "default", "mean_iters": cnt["frame_iters"] / cnt["frames"],
@@ -317,10 +368,10 @@ def main():
     }
     if not args.no_e2e:
         line["e2e"] = {"value": info_bits(cfg) * cnt["e2e_frame_iters"] / (tim["e2e_ms"] * 1e-3), "unit": UNIT,
-                       "h2d_bytes_per_step": int(llr_np.nbytes),
-                       "d2h_bytes_per_step": int(F * cfg["N"] + F + 4 * F)}
+                       "h2d_bytes_per_step": int(llr_np.nbytes), "d2h_bytes_per_step": int(d2h)}
     if not args.no_cpu_baseline and world == 1:
-        v, dt, it, nt = cpu_oracle_run(cfg, args.point, 0, args.cpu_frames)
+        v, dt, it, nt = cpu_oracle_run(cfg, args.point, 0, args.cpu_frames, inp=args.input, ebn0=args.ebn0,
+                                       symbol_out=args.symbol_out)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": nt, "kind": "oracle",
                                 "sample": f"first {args.cpu_frames} frames of the workload, {it} frame-iterations, "
                                           f"{dt:.1f} s, fp64 C oracle with OpenMP over frames"}

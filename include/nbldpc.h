@@ -78,8 +78,9 @@ typedef struct {
   uint8_t* symbol_map_out;  /* device, [frames][N] or NULL: argmax_x mu_v(x), ties -> lowest x
                                (the paper's symbol-level TENTATIVE DECISION) */
   /* Either symbol output selects the direct kernel (NBLDPC_VN_DIRECT): the symbol decision is
-   * evaluated at every iteration (the stopping one is not known in advance), 2 WHTs of size 2^m
-   * per variable, plus N*2^m*4 + N bytes per resident slot allocated on first use. */
+   * evaluated at every iteration (the stopping one is not known in advance; 2 WHTs of size 2^m per
+   * variable) and written to the frame's output rows each time, so the last write is the
+   * stopping iteration's.  The output rows hold intermediate values until the decode completes. */
 } nbldpc_decode_opts_t;
 
 /* Builds a code from H given as nnz (row, col, coefficient) triplets in any order.
@@ -152,10 +153,12 @@ nbldpc_status_t nbldpc_decode_host(nbldpc_code_t code, const float* llr_host, in
  *         (reading R23).  A row whose sum is not positive is treated as uniform and counted as a
  *         numerical event (opts->events_out), as are the iterations it stays degenerate in.
  *   the other arguments as nbldpc_decode_ex; soft_out holds the same posterior bit log-magnitudes.
- * The channel spectrum of a general pmf is not a tensor product, so this entry point always runs
- * the paper's direct q^2-term variable-node convolution (NBLDPC_VN_DIRECT; opts->vn_algorithm is
- * ignored).  The transform of the pmf is computed inside the first pass, per frame, and kept in a
- * per-slot buffer of N*2^m floats (allocated on first use, released with the handle).
+ * The channel spectrum of a general pmf is not a tensor product, so the variable node runs in the
+ * probability domain (XOR-convolution theorem): raw = WHT(p_v . WHT(W_e')) / 2^m, 2m butterfly stages
+ * per entry.  opts->vn_algorithm picks the kernel: NBLDPC_VN_SEPARABLE (default) the cluster-per-frame
+ * kernel of nbldpc_decode, NBLDPC_VN_DIRECT the slot-pass kernel (also selected by the symbol outputs).
+ * The scaled rows are kept in a per-slot buffer of N*2^m floats (allocated on first use, released
+ * with the handle).
  * pmf must be 16-byte aligned (NBLDPC_ERR_INVALID_ARGUMENT otherwise).
  * Stream-ordered; same results-independence and stream rules as nbldpc_decode. */
 nbldpc_status_t nbldpc_decode_pmf(nbldpc_code_t code, const float* pmf, int frames, int max_iters,

@@ -197,7 +197,8 @@ class Code:
         return out
 
     def decode_pmf(self, pmf, max_iters: int, *, syndrome_mode: int = 0, early_stop: bool = True, want_soft=False,
-                   want_events=False, want_post=False, slots: int = 0, use_graph: int = 0, out=None, stream=None):
+                   want_events=False, want_post=False, slots: int = 0, use_graph: int = 0, vn_algorithm: int = 0,
+                   out=None, stream=None):
         """Decode frames from symbol-level channel pmfs (nbldpc_decode_pmf).
         ``pmf``: CUDA float32 tensor [F, N, q] (any positive scale per row).  Same outputs as decode."""
         import torch
@@ -209,7 +210,7 @@ class Code:
             raise ValueError("pmf size is not a multiple of N*q")
         if out is None:
             out = self._outputs(F, pmf.device, want_soft, want_events, want_post)
-        o = self._opts(syndrome_mode, early_stop, out.get("soft"), out.get("events"), slots, use_graph, 1,
+        o = self._opts(syndrome_mode, early_stop, out.get("soft"), out.get("events"), slots, use_graph, vn_algorithm,
                        out.get("post"), out.get("map"))
         st = self._L.nbldpc_decode_pmf(self._h, pmf.data_ptr(), F, int(max_iters), out["hard"].data_ptr(),
                                        out["ok"].data_ptr(), out["iters"].data_ptr(), _stream(stream),

@@ -67,10 +67,8 @@ struct CallDev {            // per-call arguments, written on the stream before 
   int pad[3];
   const float* pmf;   // nbldpc_decode_pmf: [frames][N][q] channel pmf (else NULL)
   float* p0buf;       // nbldpc_decode_pmf: [S][N][q] P_v^0 = WHT(pmf) / sum(pmf) per slot
-  float* post_out;    // symbol posterior [frames][N][q] (or NULL)
-  uint8_t* map_out;   // symbol-MAP decision [frames][N] (or NULL)
-  float* post_buf;    // [S][N][q] per-slot posterior of the latest iteration
-  uint8_t* map_buf;   // [S][N]
+  float* post_out;    // symbol posterior [frames][N][q] (or NULL), rewritten at every iteration
+  uint8_t* map_out;   // symbol-MAP decision [frames][N] (or NULL), idem: the last write is the stopping one
 };
 
 struct WorkDev {
@@ -391,8 +389,9 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
     // P_v^0(z) for the thread's block z = t*R + zl (closed form)
     float p0[R];
     if constexpr (PMF) {
-      // general pmf: at l = 0 P = WHT(p) / sum(p) -- LR butterfly stages in
-      // registers, MB - LR across the team by shuffles -- kept per slot for the later passes
+      // general pmf: at l = 0 the row is scaled to a probability vector p,
+      // kept per slot (p0buf) for the later passes, and P^0 = WHT(p) is the initial message;
+      // at l >= 1 p0 holds p (the variable node works in the probability domain, below)
       const float* src = ell == 0 ? call->pmf + ((size_t)f * cd.N + (active ? ed.var : 0)) * Q
                                   : call->p0buf + ((size_t)s * cd.N + (active ? ed.var : 0)) * Q;
       if constexpr (R >= 4) {
@@ -406,9 +405,13 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
         for (int zl = 0; zl < R; ++zl) p0[zl] = active ? __ldcg(src + t * R + zl) : 0.0f;
       }
       if (ell == 0) {
-        wht_team<MB, LR, R>(p0, t);
-        float tot = p0[0];
-        if constexpr (TT > 1) tot = __shfl_sync(0xffffffffu, p0[0], lane & ~(TT - 1));
+        float tot = 0.0f;
+#pragma unroll
+        for (int zl = 0; zl < R; ++zl) tot += p0[zl];
+        if constexpr (TT > 1) {
+#pragma unroll
+          for (int off = TT / 2; off >= 1; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+        }
         const float inv = tot > 0.0f ? 1.0f / tot : 0.0f;  // degenerate row: all zero -> event below
 #pragma unroll
         for (int zl = 0; zl < R; ++zl) p0[zl] *= inv;
@@ -417,6 +420,7 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
 #pragma unroll
           for (int zl = 0; zl < R; ++zl) dst[zl] = p0[zl];
         }
+        wht_team<MB, LR, R>(p0, t);
       }
     } else {
       float hi = 1.0f;
@@ -447,7 +451,16 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
           D[y] = dreg[y];  // linear copy for the paper-mode points
         }
       }
-      if constexpr (DIRECT) {
+      if constexpr (PMF) {
+        // raw = P^0 (*) W_e' = WHT(p . IWHT(W_e')) up to the factor q (XOR-convolution theorem;
+        // 2 m q butterfly operations instead of q^2 FMAs -- the normalisation removes q)
+        wht_team<MB, LR, R>(b, t);
+#pragma unroll
+        for (int zl = 0; zl < R; ++zl) b[zl] *= p0[zl];
+        wht_team<MB, LR, R>(b, t);
+#pragma unroll
+        for (int zl = 0; zl < R; ++zl) raw[zl] = b[zl];
+      } else if constexpr (DIRECT) {
         float2 acc[R / 2];
 #pragma unroll
         for (int p = 0; p < R / 2; ++p) acc[p] = make_float2(0.0f, 0.0f);
@@ -483,6 +496,29 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
 #pragma unroll
         for (int zl = 0; zl < R; ++zl) b[zl] = fmaf(th[i], __shfl_xor_sync(0xffffffffu, b[zl], off), b[zl]);
       }
+#pragma unroll
+      for (int zl = 0; zl < R; ++zl) raw[zl] = b[zl];
+      __syncwarp();  // D conversions visible to the team
+    } else if constexpr (PMF) {
+      // probability-domain variable node as above, the team's high stages by shuffles
+      float b[R];
+#pragma unroll
+      for (int c4 = 0; c4 < R / 4; ++c4) {
+        float4 v = active ? *reinterpret_cast<const float4*>(B + cm_idx<MB>(t * R + 4 * c4)) : make_float4(0, 0, 0, 0);
+        b[4 * c4] = to_lin(v.x); b[4 * c4 + 1] = to_lin(v.y); b[4 * c4 + 2] = to_lin(v.z); b[4 * c4 + 3] = to_lin(v.w);
+      }
+      if (is_a) {
+#pragma unroll
+        for (int c4 = 0; c4 < R / 4; ++c4) {
+          float4* pd = reinterpret_cast<float4*>(D + cm_idx<MB>(t * R + 4 * c4));
+          float4 v = *pd;
+          *pd = make_float4(to_lin(v.x), to_lin(v.y), to_lin(v.z), to_lin(v.w));
+        }
+      }
+      wht_team<MB, LR, R>(b, t);
+#pragma unroll
+      for (int zl = 0; zl < R; ++zl) b[zl] *= p0[zl];
+      wht_team<MB, LR, R>(b, t);
 #pragma unroll
       for (int zl = 0; zl < R; ++zl) raw[zl] = b[zl];
       __syncwarp();  // D conversions visible to the team
@@ -624,7 +660,7 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
         }
       }
       if constexpr (DIRECT) {
-        if (call->post_buf != nullptr) {
+        if (call->post_out != nullptr || call->map_out != nullptr) {
           // symbol-level decision: mu_v(x) = sum_z M_v(z) (-1)^{z.x} with
           // M_v = raw (*) W_e, i.e. mu_v = WHT(raw) . WHT(W_e) (the XOR-convolution theorem);
           // clamped at 0 and normalised to a posterior, argmax ties -> lowest x
@@ -660,13 +696,22 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
               if (ob > best || (ob == best && ox < bx)) { best = ob; bx = ox; }
             }
           }
-          if (is_a) {
+          // written straight to the frame's output rows at every iteration: the stopping
+          // iteration's write is the last one (no per-slot copy when the frame finishes)
+          if (is_a && call->post_out) {
             const float inv = tot > 0.0f ? 1.0f / tot : 0.0f;
-            float* dst = call->post_buf + ((size_t)s * cd.N + ed.var) * Q + t * R;
+            float* dst = call->post_out + ((size_t)f * cd.N + ed.var) * Q + t * R;
+            if constexpr (R >= 4) {
 #pragma unroll
-            for (int zl = 0; zl < R; ++zl) dst[zl] = a[zl] * inv;
-            if (t == 0) call->map_buf[(size_t)s * cd.N + ed.var] = (uint8_t)bx;
+              for (int c4 = 0; c4 < R / 4; ++c4)
+                reinterpret_cast<float4*>(dst)[c4] =
+                    make_float4(a[4 * c4] * inv, a[4 * c4 + 1] * inv, a[4 * c4 + 2] * inv, a[4 * c4 + 3] * inv);
+            } else {
+#pragma unroll
+              for (int zl = 0; zl < R; ++zl) dst[zl] = a[zl] * inv;
+            }
           }
+          if (is_a && t == 0 && call->map_out) call->map_out[(size_t)f * cd.N + ed.var] = (uint8_t)bx;
         }
       }
       if (mode == 1) {
@@ -821,21 +866,6 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
 #pragma unroll 4
       for (int i = lane; i < N * MB; i += 32)
         call->soft_out[(size_t)f * N * MB + i] = __ldcg(&ws.soft[(size_t)s * N * MB + i]);
-    }
-    if (call->post_buf != nullptr) {
-      if (call->post_out) {
-        const float4* src = reinterpret_cast<const float4*>(call->post_buf + (size_t)s * N * Q);
-        float4* dst = reinterpret_cast<float4*>(call->post_out + (size_t)f * N * Q);
-        if constexpr (Q >= 4) {
-#pragma unroll 4
-          for (int i = lane; i < N * Q / 4; i += 32) dst[i] = __ldcg(src + i);
-        } else {
-          for (int i = lane; i < N * Q; i += 32)
-            call->post_out[(size_t)f * N * Q + i] = __ldcg(call->post_buf + (size_t)s * N * Q + i);
-        }
-      }
-      if (call->map_out)
-        for (int v = lane; v < N; v += 32) call->map_out[(size_t)f * N + v] = __ldcg(&call->map_buf[(size_t)s * N + v]);
     }
     if (lane == 0) {
       call->ok[f] = (uint8_t)ok;

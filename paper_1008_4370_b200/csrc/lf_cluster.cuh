@@ -239,7 +239,55 @@ __device__ __forceinline__ void tot_sum(const float* smem, int gbase, float* TOT
   }
 }
 
-template <int MB, int NTHR>
+// One Walsh-Hadamard butterfly stage (u, w) -> (u + w, u - w) on register bit I of a thread's R entries.
+template <int R, int I>
+__device__ __forceinline__ void wht_reg(float (&x)[R]) {
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (!(r & (1 << I))) {
+      const float u = x[r], w = x[r | (1 << I)];
+      x[r] = u + w;
+      x[r | (1 << I)] = u - w;
+    }
+}
+// The full WHT of a team's vector held in the phase-B coordinates zr (pmf input):
+// every register bit, then the z bits LJ..3 that index the team's lanes by shuffles.
+template <int MB, int R, int LR, int LJ, int TT>
+__device__ __forceinline__ void wht_phase_b(float (&x)[R], int t) {
+  if constexpr (LR > 0) wht_reg<R, 0>(x);
+  if constexpr (LR > 1) wht_reg<R, 1>(x);
+  if constexpr (LR > 2) wht_reg<R, 2>(x);
+  if constexpr (LR > 3) wht_reg<R, 3>(x);
+  if constexpr (TT > 1) {
+#pragma unroll
+    for (int k = 0; k < 4 - LJ; ++k) {
+      const int off = 1 << k;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const float o = __shfl_xor_sync(0xffffffffu, x[r], off);
+        x[r] = (t & off) ? o - x[r] : x[r] + o;
+      }
+    }
+  }
+}
+// position of entry z of a normalised pmf row in the per-slot buffer: thread t of the team reads its R
+// phase-B entries zr(t, r) as one contiguous run at t R + r
+template <int MB>
+__device__ __forceinline__ int ppos(int z) {
+  if constexpr (MB > 4) {
+    constexpr int LJ = 8 - MB, TT = 1 << (MB - 4), R = 16;
+    const int jl = z & ((1 << LJ) - 1), tt = (z >> LJ) & (TT - 1), h = z >> 4;
+    return tt * R + (jl | (h << LJ));
+  } else {
+    return z;
+  }
+}
+
+// PMF = true: nbldpc_decode_pmf.  The channel prior is a general symbol pmf p_v, so P_v^0 is not a
+// tensor product; the variable node runs in the probability domain instead (XOR-convolution
+// theorem): raw = P^0 (*) W_e' = WHT(p_v . WHT(W_e')) / q -- 2m butterfly stages and a product per
+// entry (the factor q cancels in the normalisation).
+template <int MB, int NTHR, bool PMF = false>
 #ifndef NB_CLUSTER_MINB
 #define NB_CLUSTER_MINB 2
 #endif
@@ -378,7 +426,33 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
     float* const sout = step ? ws.soft + (size_t)f * cd.N * MB : call->soft_out + (size_t)f * cd.N * MB;
     float* const Tt = ws.Tt + (size_t)slot * cd.N * 8;
     uint8_t* const con = ws.con + (size_t)slot * ws.con_stride;
-    if (!step) {
+    float* const Pp = PMF ? call->p0buf + (size_t)slot * cd.N * Q : nullptr;
+    if (!step && PMF) {
+      // the frame's pmf rows scaled to probabilities p_v, one warp per row, stored at
+      // ppos(z) for the teams' phase-B reads; a row with a non-positive sum becomes all zero (its
+      // variable-node outputs are then neutral and counted as numerical events, reading R23)
+      const float* pf = call->pmf + (size_t)f * cd.N * Q;
+      const int nwarp = nthr >> 5;
+      constexpr int PER = Q >= 32 ? Q / 32 : 1;
+      for (int v = (int)rank * nwarp + (tid >> 5); v < cd.N; v += (int)csz * nwarp) {
+        float pv[PER], sum = 0.0f;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          const int z = lane + 32 * k;
+          pv[k] = z < Q ? __ldcs(pf + (size_t)v * Q + z) : 0.0f;  // streamed: read once
+          sum += pv[k];
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+        const float inv = sum > 0.0f ? 1.0f / sum : 0.0f;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+          const int z = lane + 32 * k;
+          if (z < Q) Pp[(size_t)v * Q + ppos<MB>(z)] = pv[k] * inv;
+        }
+      }
+      cluster_sync_all();
+    } else if (!step) {
       // channel terms of the frame, computed once and cooperatively by the cluster's CTAs:
       // Tt[v][i] = tanh(L_{v,i} / 2), the factors of P_v^0 = (x)_i (1, t_i)
       const float* lf = call->llr + (size_t)f * cd.N * MB;
@@ -418,7 +492,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #pragma unroll
           for (int r = 0; r < Q; ++r) dst[r] = __ldcg(sp + r);
         }
-        if (act && !C::THREG) tx += 32;
+        if (act && !C::THREG && !PMF) tx += 32;
         tx += blk;
         mbar_arrive_tx(&gmbar[b], tx);
         // the block in pieces of <= NB_BLK_PIECE bytes (several TMA transfers in flight)
@@ -429,13 +503,13 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         for (uint32_t o = 0; o < blk; o += NB_BLK_PIECE)
           bulk_g2s(GST + b * GBLK + o / 4, Win + (size_t)cg0 * cd.kpad * Q + o / 4,
                    blk - o < NB_BLK_PIECE ? blk - o : NB_BLK_PIECE, &gmbar[b]);
-        if (act && !C::THREG) bulk_g2s(THB + b * nteams * 8, Tt + (size_t)(rr.var_h >> 8) * 8, 32, &gmbar[b]);
+        if (act && !C::THREG && !PMF) bulk_g2s(THB + b * nteams * 8, Tt + (size_t)(rr.var_h >> 8) * 8, 32, &gmbar[b]);
       };
       // channel-term row of chunk kc's variable, prefetched into registers one chunk ahead
       auto th_load = [&](int kc, float4 (&dst)[2]) {
         dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
         dst[1] = dst[0];
-        if (!C::THREG || !in_check || kc >= nch) return;
+        if (PMF || !C::THREG || !in_check || kc >= nch) return;
         const EdgeRec rr = recs[(kc * CPC + lc) * KT + j];
         if (rr.partner_a < 0) return;
         const float4* src = reinterpret_cast<const float4*>(Tt + (size_t)(rr.var_h >> 8) * 8);
@@ -470,7 +544,22 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         {
           const float tv[8] = {thc[0].x, thc[0].y, thc[0].z, thc[0].w, thc[1].x, thc[1].y, thc[1].z, thc[1].w};
 #pragma unroll
-          for (int b = 0; b < MB; ++b) th[b] = active ? (C::THREG ? tv[b] : THB[buf * nteams * 8 + b]) : 0.0f;
+          for (int b = 0; b < MB; ++b) th[b] = (active && !PMF) ? (C::THREG ? tv[b] : THB[buf * nteams * 8 + b]) : 0.0f;
+        }
+        // pmf input: my R entries of p_v at the phase-B coordinates zr, straight from L2
+        float pv[PMF ? R : 1];
+        if constexpr (PMF) {
+          const float* src = Pp + (size_t)var * Q + t * R;
+          if constexpr (R >= 4) {
+#pragma unroll
+            for (int ch = 0; ch < CH; ++ch) {
+              const float4 v = active ? __ldcg(reinterpret_cast<const float4*>(src) + ch) : make_float4(0.f, 0.f, 0.f, 0.f);
+              pv[4 * ch] = v.x; pv[4 * ch + 1] = v.y; pv[4 * ch + 2] = v.z; pv[4 * ch + 3] = v.w;
+            }
+          } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) pv[r] = active ? __ldcg(src + r) : 0.0f;
+          }
         }
         // W_e (own message, for v's decision at its first edge) straight from L2 into registers;
         // consumed after the variable node
@@ -502,7 +591,12 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 
         // ---- VARIABLE TO CHECK: x (phase B) = P^0 (*) Gamma^-1(W_e'); at l = 0, x = P^0
         float x[R];
-        if (ell == 0) {
+        if (PMF && ell == 0) {
+          // P^0 = WHT(p_v)
+#pragma unroll
+          for (int r = 0; r < R; ++r) x[r] = pv[r];
+          wht_phase_b<MB, R, LR, LJ, TT>(x, t);
+        } else if (ell == 0) {
           float base = 1.0f;
           if constexpr (TT > 1) {
 #pragma unroll
@@ -527,7 +621,14 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #pragma unroll
             for (int r = 0; r < R; ++r) x[r] = to_lin(st[r]);
           }
-          bfly_regs<R, 0, LR>(x, th);  // z bits 0..LR-1
+          if constexpr (PMF) {
+            if constexpr (LR > 0) wht_reg<R, 0>(x);  // z bits 0..LR-1 of WHT(W_e')
+            if constexpr (LR > 1) wht_reg<R, 1>(x);
+            if constexpr (LR > 2) wht_reg<R, 2>(x);
+            if constexpr (LR > 3) wht_reg<R, 3>(x);
+          } else {
+            bfly_regs<R, 0, LR>(x, th);  // z bits 0..LR-1
+          }
           if constexpr (TT > 1) {
             // transposition through the consumed stage buffer, chunk-swizzled layout tpos(z)
             __syncwarp();  // every thread of the team has read its phase-A chunks
@@ -553,10 +654,23 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               }
             }
             // z bits 4..MB-1 = register bits LJ..3
-            if constexpr (LJ <= 0) bfly_reg<R, 0>(x, th[4 - LJ]);
-            if constexpr (LJ <= 1) bfly_reg<R, 1>(x, th[(5 - LJ) < MB ? 5 - LJ : 0]);
-            if constexpr (LJ <= 2) bfly_reg<R, 2>(x, th[(6 - LJ) < MB ? 6 - LJ : 0]);
-            if constexpr (LJ <= 3) bfly_reg<R, 3>(x, th[(7 - LJ) < MB ? 7 - LJ : 0]);
+            if constexpr (PMF) {
+              if constexpr (LJ <= 0) wht_reg<R, 0>(x);
+              if constexpr (LJ <= 1) wht_reg<R, 1>(x);
+              if constexpr (LJ <= 2) wht_reg<R, 2>(x);
+              if constexpr (LJ <= 3) wht_reg<R, 3>(x);
+            } else {
+              if constexpr (LJ <= 0) bfly_reg<R, 0>(x, th[4 - LJ]);
+              if constexpr (LJ <= 1) bfly_reg<R, 1>(x, th[(5 - LJ) < MB ? 5 - LJ : 0]);
+              if constexpr (LJ <= 2) bfly_reg<R, 2>(x, th[(6 - LJ) < MB ? 6 - LJ : 0]);
+              if constexpr (LJ <= 3) bfly_reg<R, 3>(x, th[(7 - LJ) < MB ? 7 - LJ : 0]);
+            }
+          }
+          if constexpr (PMF) {
+            // q w'(x) = WHT(W_e')(x) at x = zr[r]: times p_v(x), back with the second WHT -> q raw
+#pragma unroll
+            for (int r = 0; r < R; ++r) x[r] *= pv[r];
+            wht_phase_b<MB, R, LR, LJ, TT>(x, t);
           }
         }
 

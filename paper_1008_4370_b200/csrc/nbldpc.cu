@@ -45,8 +45,6 @@ struct Workspace {
   size_t out_stage_bytes = 0;
   float* p0buf = nullptr;  // nbldpc_decode_pmf: [S][N][q] channel spectra
   size_t p0buf_bytes = 0;
-  float* postbuf = nullptr;  // symbol outputs: [S][N][q] posterior, then [S][N] MAP bytes
-  size_t postbuf_bytes = 0;
   // launch accounting of the most recent decode
   cudaStream_t last_stream = nullptr;
   int last_graph = 0;
@@ -132,7 +130,6 @@ void free_workspace(Workspace& w) {
   if (w.llr_stage) cudaFree(w.llr_stage);
   if (w.out_stage) cudaFree(w.out_stage);
   if (w.p0buf) cudaFree(w.p0buf);
-  if (w.postbuf) cudaFree(w.postbuf);
   w = Workspace{};
 }
 
@@ -168,28 +165,33 @@ void* pass_kernel_ptr(int m, int big, int direct) {
   return direct ? pass_kernel_ptr_t<true, false>(m, big) : pass_kernel_ptr_t<false, false>(m, big);
 }
 
-template <int MB, int NTHR>
-void* cluster_fn() { return reinterpret_cast<void*>(&nb::lf_cluster_kernel<MB, NTHR>); }
-void* persist_kernel_ptr(int m, int big) {
+template <int MB, int NTHR, bool PMF>
+void* cluster_fn() { return reinterpret_cast<void*>(&nb::lf_cluster_kernel<MB, NTHR, PMF>); }
+template <bool PMF>
+void* persist_kernel_ptr_t(int m, int big) {
   switch (m * 2 + (big ? 1 : 0)) {
-    case 2: return cluster_fn<1, 256>();
-    case 3: return cluster_fn<1, 512>();
-    case 4: return cluster_fn<2, 256>();
-    case 5: return cluster_fn<2, 512>();
-    case 6: return cluster_fn<3, 256>();
-    case 7: return cluster_fn<3, 512>();
-    case 8: return cluster_fn<4, 256>();
-    case 9: return cluster_fn<4, 512>();
-    case 10: return cluster_fn<5, 256>();
-    case 11: return cluster_fn<5, 512>();
-    case 12: return cluster_fn<6, 256>();
-    case 13: return cluster_fn<6, 512>();
-    case 14: return cluster_fn<7, 256>();
-    case 15: return cluster_fn<7, 512>();
-    case 16: return cluster_fn<8, 256>();
-    case 17: return cluster_fn<8, 512>();
+    case 2: return cluster_fn<1, 256, PMF>();
+    case 3: return cluster_fn<1, 512, PMF>();
+    case 4: return cluster_fn<2, 256, PMF>();
+    case 5: return cluster_fn<2, 512, PMF>();
+    case 6: return cluster_fn<3, 256, PMF>();
+    case 7: return cluster_fn<3, 512, PMF>();
+    case 8: return cluster_fn<4, 256, PMF>();
+    case 9: return cluster_fn<4, 512, PMF>();
+    case 10: return cluster_fn<5, 256, PMF>();
+    case 11: return cluster_fn<5, 512, PMF>();
+    case 12: return cluster_fn<6, 256, PMF>();
+    case 13: return cluster_fn<6, 512, PMF>();
+    case 14: return cluster_fn<7, 256, PMF>();
+    case 15: return cluster_fn<7, 512, PMF>();
+    case 16: return cluster_fn<8, 256, PMF>();
+    case 17: return cluster_fn<8, 512, PMF>();
   }
   return nullptr;
+}
+// pmf = 1: the nbldpc_decode_pmf variant (probability-domain variable node)
+void* persist_kernel_ptr(int m, int big, int pmf = 0) {
+  return pmf ? persist_kernel_ptr_t<true>(m, big) : persist_kernel_ptr_t<false>(m, big);
 }
 // shared-memory words per edge team of the cluster kernel (nb::CCfg<m>::TEAM)
 int persist_team_words(int m) {
@@ -206,7 +208,7 @@ int persist_team_words(int m) {
   return 0;
 }
 
-cudaError_t launch_cluster(const nbldpc_code_s* c, const nb::ClusterParams& P, int ncl, cudaStream_t st) {
+cudaError_t launch_cluster(const nbldpc_code_s* c, const nb::ClusterParams& P, int ncl, cudaStream_t st, int pmf = 0) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(ncl * c->p_cs));
   cfg.blockDim = dim3((unsigned)c->p_block);
@@ -220,7 +222,7 @@ cudaError_t launch_cluster(const nbldpc_code_s* c, const nb::ClusterParams& P, i
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void* args[] = {const_cast<nb::ClusterParams*>(&P)};
-  return cudaLaunchKernelExC(&cfg, persist_kernel_ptr(c->m, c->p_big), args);
+  return cudaLaunchKernelExC(&cfg, persist_kernel_ptr(c->m, c->p_big, pmf), args);
 }
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a property of the kernel (one instantiation per
@@ -238,17 +240,19 @@ cudaError_t ensure_smem_attr(const nbldpc_code_s* c) {
     if (e != cudaSuccess) return e;
     g_attr_smem[d][k] = c->smem;
   }
-  if (c->p_cs > 8) {
-    cudaError_t e = cudaFuncSetAttribute(persist_kernel_ptr(c->m, c->p_big), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-  }
-  static size_t p_attr[64][18] = {};
-  const int d = c->device & 63, k = c->m * 2 + c->p_big;
-  if (p_attr[d][k] < c->p_smem) {
-    cudaError_t e = cudaFuncSetAttribute(persist_kernel_ptr(c->m, c->p_big), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)c->p_smem);
-    if (e != cudaSuccess) return e;
-    p_attr[d][k] = c->p_smem;
+  static size_t p_attr[64][36] = {};
+  for (int pmf = 0; pmf < 2; ++pmf) {
+    void* fn = persist_kernel_ptr(c->m, c->p_big, pmf);
+    if (c->p_cs > 8) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    const int d = c->device & 63, k = (c->m * 2 + c->p_big) * 2 + pmf;
+    if (p_attr[d][k] < c->p_smem) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->p_smem);
+      if (e != cudaSuccess) return e;
+      p_attr[d][k] = c->p_smem;
+    }
   }
   return cudaSuccess;
 }
@@ -495,8 +499,8 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
     return NBLDPC_ERR_INVALID_ARGUMENT;
   if (mode != 0 && mode != 1) return NBLDPC_ERR_INVALID_ARGUMENT;
   if (direct != 0 && direct != 1) return NBLDPC_ERR_INVALID_ARGUMENT;
-  if (pmf) direct = 2;
-  else if ((post || xmap) && direct == 0) direct = 1;  // the symbol decision lives in the direct kernel
+  if ((post || xmap) && direct == 0) direct = 1;  // the symbol decision lives in the pass kernel
+  if (pmf && direct) direct = 2;                   // the pass kernel's pmf variant
   if (slots < 0) return NBLDPC_ERR_INVALID_ARGUMENT;
   if ((soft && !is_device_ptr(soft)) || (events && !is_device_ptr(events))) return NBLDPC_ERR_INVALID_ARGUMENT;
   int S = slots > 0 ? std::min(slots, frames) : default_slots(c, frames);
@@ -521,24 +525,8 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
     call.pmf = pmf;
     call.p0buf = w.p0buf;
   }
-  if (post || xmap) {
-    const size_t pb = align_up((size_t)S * c->N * c->q * sizeof(float), 256);
-    const size_t need = pb + (size_t)S * c->N;
-    if (w.postbuf_bytes < need) {
-      if (w.postbuf) {
-        NB_TRY(cudaStreamSynchronize(st));
-        cudaFree(w.postbuf);
-        w.postbuf = nullptr;
-        w.postbuf_bytes = 0;
-      }
-      NB_TRY(cudaMalloc(&w.postbuf, need));
-      w.postbuf_bytes = need;
-    }
-    call.post_out = post;
-    call.map_out = xmap;
-    call.post_buf = w.postbuf;
-    call.map_buf = reinterpret_cast<uint8_t*>(w.postbuf) + pb;
-  }
+  call.post_out = post;
+  call.map_out = xmap;
   call.llr = llr;
   call.hard = hard;
   call.ok = ok;
@@ -561,7 +549,7 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   w.last_host_launches = 1;
   if (!direct) {
     nb::ClusterParams PP = make_cparams(c, 0, 0, nullptr);
-    NB_TRY(launch_cluster(c, PP, S, st));
+    NB_TRY(launch_cluster(c, PP, S, st, pmf != nullptr));
     w.last_graph = 0;
     w.last_host_launches = 2;
     return NBLDPC_OK;
