@@ -32,7 +32,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRC = [os.path.join(_HERE, "oracle.c"), os.path.join(_HERE, "lf_body.inc")]
+_SRC = [os.path.join(_HERE, "oracle.c"), os.path.join(_HERE, "lf_body.inc"), os.path.join(_HERE, "logsp_body.inc")]
 _SO = os.path.join(_HERE, "liboracle.so")
 _LOCK = threading.Lock()
 _LIB = None
@@ -101,6 +101,12 @@ def _lib():
                                                                dp, i32])
                 sig["or_lf_symbol_posterior" + sfx] = (None, [vp, dp, dp, dp, dp, dp, dp])
                 sig["or_lf_init_pmf" + sfx] = (None, [vp, dp, dp, dp])
+                sig["or_ls_init" + sfx] = (None, [vp, dp, dp])
+                sig["or_ls_init_pmf" + sfx] = (None, [vp, dp, dp])
+                sig["or_ls_check_to_variable" + sfx] = (None, [vp, dp, dp])
+                sig["or_ls_variable_to_check" + sfx] = (None, [vp, dp, dp, dp])
+                sig["or_ls_decision" + sfx] = (None, [vp, dp, dp, dp, dp])
+                sig["or_ls_decode_batch" + sfx] = (None, [vp, dp, i32, i32, i32, i32, dp, dp, dp, i32])
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
                 fn.restype = res
@@ -388,6 +394,57 @@ class Code:
             out["post"] = post
             out["map"] = xmap.astype(np.uint8)
         return out
+
+    # ---- conventional Log-SP, double or the float32 twin
+    def ls_init(self, llr, f32=False):
+        dt, sfx = self._real(f32)
+        L0 = np.zeros((self.N, self.q), dt)
+        getattr(self._L, "or_ls_init" + sfx)(self._h, _p(_f64(llr)), _p(L0))
+        return L0
+
+    def ls_init_pmf(self, pmf, f32=False):
+        dt, sfx = self._real(f32)
+        L0 = np.zeros((self.N, self.q), dt)
+        getattr(self._L, "or_ls_init_pmf" + sfx)(self._h, _p(_f64(pmf)), _p(L0))
+        return L0
+
+    def ls_check_to_variable(self, V, f32=False):
+        dt, sfx = self._real(f32)
+        V = np.ascontiguousarray(V, dt)
+        W = np.zeros((self.E, self.q), dt)
+        getattr(self._L, "or_ls_check_to_variable" + sfx)(self._h, _p(V), _p(W))
+        return W
+
+    def ls_variable_to_check(self, L0, W, f32=False):
+        dt, sfx = self._real(f32)
+        L0, W = np.ascontiguousarray(L0, dt), np.ascontiguousarray(W, dt)
+        V = np.zeros((self.E, self.q), dt)
+        getattr(self._L, "or_ls_variable_to_check" + sfx)(self._h, _p(L0), _p(W), _p(V))
+        return V
+
+    def ls_decision(self, L0, W, f32=False):
+        dt, sfx = self._real(f32)
+        L0, W = np.ascontiguousarray(L0, dt), np.ascontiguousarray(W, dt)
+        x = np.zeros(self.N, np.int32)
+        mu = np.zeros((self.N, self.q), dt)
+        getattr(self._L, "or_ls_decision" + sfx)(self._h, _p(L0), _p(W), _p(x), _p(mu))
+        return x, mu
+
+    def ls_decode_batch(self, inp, max_iters: int, early_stop: bool = True, pmf: bool = False,
+                        nthreads: int | None = None, f32: bool = False):
+        """Conventional Log-SP decode of F frames (LLRs [F][N*m] or pmfs [F][N][q]); symbol-MAP
+        decisions, exact-syndrome stop."""
+        _, sfx = self._real(f32)
+        row = self.N * (self.q if pmf else self.m)
+        inp = np.ascontiguousarray(inp, np.float32).reshape(-1, row)
+        F = inp.shape[0]
+        x = np.zeros((F, self.N), np.int32)
+        ok = np.zeros(F, np.int32)
+        it = np.zeros(F, np.int32)
+        nt = nthreads or os.cpu_count() or 1
+        getattr(self._L, "or_ls_decode_batch" + sfx)(self._h, _p(inp), int(bool(pmf)), F, int(max_iters),
+                                                     int(bool(early_stop)), _p(x), _p(ok), _p(it), int(nt))
+        return {"hard": x.astype(np.uint8), "ok": ok.astype(np.uint8), "iters": it}
 
     def lf_decode_batch(self, llr, max_iters: int, mode: int = EXACT, early_stop: bool = True,
                         want_soft: bool = False, nthreads: int | None = None, f32: bool = False,

@@ -463,3 +463,23 @@ void or_sp_posterior(const or_code* c, const double* p0, const double* w, double
 #define LF_LOG logf
 #define LF_FABS fabsf
 #include "lf_body.inc"
+
+/* ------------------------------------------------------------------ */
+/* O-LS: the conventional Log-SP, the paper's       */
+/* comparison algorithm; double and a float32 diagnostic twin.         */
+/* ------------------------------------------------------------------ */
+#define LS_REAL double
+#define LS_SFX(name) name
+#define LS_EXP exp
+#define LS_LOG log
+#include "logsp_body.inc"
+#undef LS_REAL
+#undef LS_SFX
+#undef LS_EXP
+#undef LS_LOG
+
+#define LS_REAL float
+#define LS_SFX(name) name##_f32
+#define LS_EXP expf
+#define LS_LOG logf
+#include "logsp_body.inc"
