@@ -51,13 +51,18 @@ def hbm_peak():
         return HBM_PEAK_FALLBACK, "fallback"
 
 
-def per_frame_iter(cfg, vn, inp="llr", symbol_out=False):
+def per_frame_iter(cfg, vn, inp="llr", symbol_out=False, algorithm="lf"):
     """Algorithmic work of one frame-iteration: SFU ops, FP32 FMAs, message bytes.
     inp = "pmf": the channel spectrum is a q-vector per variable (read per iteration from the slot
     buffer) instead of m channel terms; symbol_out: + the symbol posterior written per iteration
     and its two WHTs (counted as FMA-pipe ops)."""
     N, q, m = cfg["N"], cfg["q"], cfg["m"]
     E = 2 * N
+    if algorithm == "logsp":
+        # conventional Log-SP (PAPER.md:231-281): 3(k-2) q^2-term log-convolutions per check (forward-
+        # backward), each input exponentiated twice and each output's log once; messages + lambda^0
+        Mc = E // cfg["k"]
+        return 3 * E * q, Mc * 3 * (cfg["k"] - 2) * q * q, 2 * E * q * 4 + 4 * N * q + N
     mufu = 2 * E * q + N * q                        # ex2 of every VN input entry, lg2 of every output, ex2 of W_a
     if inp == "pmf":  # probability-domain VN: 2 WHTs (m q add/sub each) and a product per entry
         fma = E * q * (2 * m + 1) + N * (m + 1) * q
@@ -71,10 +76,10 @@ def per_frame_iter(cfg, vn, inp="llr", symbol_out=False):
     return mufu, fma, bytes_
 
 
-def roofline(cfg, vn, frame_iters, seconds, traffic, inp="llr", symbol_out=False):
+def roofline(cfg, vn, frame_iters, seconds, traffic, inp="llr", symbol_out=False, algorithm="lf"):
     """The slower of the SFU, FP32 and HBM-message-byte bounds (BASELINE.json north_star) for the
     work done; achieved / peak of that resource over the measured kernel time."""
-    mufu, fma, byts = per_frame_iter(cfg, vn, inp, symbol_out)
+    mufu, fma, byts = per_frame_iter(cfg, vn, inp, symbol_out, algorithm)
     hbm, hbm_src = hbm_peak()
     t = {"alu": max(mufu / MUFU_PEAK, fma / FMA_PEAK), "hbm": byts / hbm}
     bound = max(t, key=t.get)
@@ -165,7 +170,7 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_oracle_run(cfg, point, frame0, nframes, threads=None, inp="llr", ebn0=None, symbol_out=False):
+def cpu_oracle_run(cfg, point, frame0, nframes, threads=None, inp="llr", ebn0=None, symbol_out=False, algorithm="lf"):
     """Times the oracle (as it stands) on frames frame0.. of the workload; returns (value, seconds, iters)."""
     import oracle
 
@@ -173,9 +178,12 @@ def cpu_oracle_run(cfg, point, frame0, nframes, threads=None, inp="llr", ebn0=No
     code = oracle.Code(oracle.Field(cfg["m"], cfg["poly"]), M, cfg["N"], rows, cols, coeffs)
     x = channel_input(cfg, inp, point, ebn0, frame0, nframes)
     nt = threads or os.cpu_count() or 1
-    dec = code.lf_decode_batch_pmf if inp == "pmf" else code.lf_decode_batch
     t0 = time.perf_counter()
-    r = dec(x, cfg["max_iters"], nthreads=nt, want_post=symbol_out)
+    if algorithm == "logsp":
+        r = code.ls_decode_batch(x, cfg["max_iters"], pmf=inp == "pmf", nthreads=nt)
+    else:
+        dec = code.lf_decode_batch_pmf if inp == "pmf" else code.lf_decode_batch
+        r = dec(x, cfg["max_iters"], nthreads=nt, want_post=symbol_out)
     dt = time.perf_counter() - t0
     it = int(r["iters"].sum())
     return info_bits(cfg) * it / dt, dt, it, nt
@@ -189,7 +197,7 @@ def run_reference(args, cfg):
     nframes = args.ref_frames
     for i in range(args.warmup + args.steps):
         v, dt, it, nt = cpu_oracle_run(cfg, args.point, i * nframes, nframes, inp=args.input, ebn0=args.ebn0,
-                                       symbol_out=args.symbol_out)
+                                       symbol_out=args.symbol_out, algorithm=args.algorithm)
         if i >= args.warmup:
             vals.append(v)
             dts.append(dt)
@@ -225,6 +233,8 @@ def main():
                     help="llr: BPSK bit LLRs (nbldpc_decode); pmf: symbol pmfs (nbldpc_decode_pmf)")
     ap.add_argument("--ebn0", type=float, default=None, help="override the config's Eb/N0 (dB)")
     ap.add_argument("--symbol-out", action="store_true", help="also output the symbol posterior and MAP decision")
+    ap.add_argument("--algorithm", default="lf", choices=["lf", "logsp"],
+                    help="lf: Log-Fourier SP (the hot path); logsp: the conventional Log-SP it is compared with")
     ap.add_argument("--ref-frames", type=int, default=32)
     ap.add_argument("--cpu-frames", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -263,7 +273,8 @@ def main():
     llr = llr_host.to(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
-    kw = dict(slots=args.slots, use_graph=args.graph, want_post=args.symbol_out, vn_algorithm=vn)
+    kw = dict(slots=args.slots, use_graph=args.graph, want_post=args.symbol_out, vn_algorithm=vn,
+              algorithm=1 if args.algorithm == "logsp" else 0)
     decode = code.decode_pmf if pmf_in else code.decode
 
     def barrier():
@@ -347,9 +358,11 @@ def main():
         except (OSError, ValueError):
             traffic = None
     # this rank's kernel: its frame-iterations over its own device time
-    roof = roofline(cfg, vn, iters_sum, sum(step_ms) * 1e-3, traffic, args.input, args.symbol_out)
+    roof = roofline(cfg, vn, iters_sum, sum(step_ms) * 1e-3, traffic, args.input, args.symbol_out, args.algorithm)
     roof["kernel"] = ("lf_cluster_kernel (one launch per step + a 1-block setup kernel; "
                       "CUDA events around the step)") if vn == 0 else "nb_pass_kernel (slot passes)"
+    if args.algorithm == "logsp":
+        roof["kernel"] = "ls_frame_kernel (conventional Log-SP, one CTA per frame; one launch per step)"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": warm, "ms_per_step": tim["ms"] / args.steps, "higher_is_better": True,
@@ -357,7 +370,7 @@ def main():
         "config": {"workload": workload_name(cfg, args.point, args.input, args.ebn0), "frames_per_gpu": F,
                    "global_frames": F * world, "N": cfg["N"], "q": cfg["q"], "k": cfg["k"],
                    "max_iters": cfg["max_iters"], "vn_algorithm": ["separable", "direct"][vn],
-                   "input": args.input, "symbol_outputs": bool(args.symbol_out),
+                   "input": args.input, "symbol_outputs": bool(args.symbol_out), "algorithm": args.algorithm,
                    "parallelism": f"frames sharded over {world} GPU(s), no collective in the loop",
                    "l2": "flushed (256 MiB write) before every timed step",
                    "slots": args.slots or "default", "mean_iters": cnt["frame_iters"] / cnt["frames"],
@@ -371,7 +384,7 @@ def main():
                        "h2d_bytes_per_step": int(llr_np.nbytes), "d2h_bytes_per_step": int(d2h)}
     if not args.no_cpu_baseline and world == 1:
         v, dt, it, nt = cpu_oracle_run(cfg, args.point, 0, args.cpu_frames, inp=args.input, ebn0=args.ebn0,
-                                       symbol_out=args.symbol_out)
+                                       symbol_out=args.symbol_out, algorithm=args.algorithm)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": nt, "kind": "oracle",
                                 "sample": f"first {args.cpu_frames} frames of the workload, {it} frame-iterations, "
                                           f"{dt:.1f} s, fp64 C oracle with OpenMP over frames"}

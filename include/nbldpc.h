@@ -58,6 +58,17 @@ typedef enum {
   NBLDPC_VN_DIRECT = 1     /* the paper's CONV (Table 1): 2^{2m} FMAs per edge */
 } nbldpc_vn_algorithm_t;
 
+/* Decoding algorithm (nbldpc_decode_opts_t::algorithm). */
+typedef enum {
+  NBLDPC_ALG_LOG_FOURIER = 0, /* the paper's Log-Fourier SP: the hot path */
+  NBLDPC_ALG_LOG_SP = 1       /* the conventional Log-SP it is compared with: log-domain
+                                 messages, check node = leave-one-out log-convolutions (forward-backward,
+                                 3(k-2) q^2-term log-convolutions per check), symbol-MAP decisions
+                                 argmax_x mu_v(x) (:271-276), exact-syndrome stop.  Same outputs as SP
+                                 (:279); soft_out, events_out, the symbol outputs and the paper syndrome
+                                 mode are not available (NBLDPC_ERR_INVALID_ARGUMENT) */
+} nbldpc_algorithm_t;
+
 /* Options of nbldpc_decode_ex / nbldpc_decode_host.  Zero-initialise, then set
  * struct_size = sizeof(nbldpc_decode_opts_t).  NULL opts = all defaults. */
 typedef struct {
@@ -81,6 +92,7 @@ typedef struct {
    * evaluated at every iteration (the stopping one is not known in advance; 2 WHTs of size 2^m per
    * variable) and written to the frame's output rows each time, so the last write is the
    * stopping iteration's.  The output rows hold intermediate values until the decode completes. */
+  int algorithm;     /* nbldpc_algorithm_t, default NBLDPC_ALG_LOG_FOURIER */
 } nbldpc_decode_opts_t;
 
 /* Builds a code from H given as nnz (row, col, coefficient) triplets in any order.

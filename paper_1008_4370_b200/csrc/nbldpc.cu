@@ -17,6 +17,7 @@
 
 #include "../../include/nbldpc.h"
 #include "decoder.cuh"
+#include "logsp.cuh"
 #include "lf_cluster.cuh"
 
 using nb::CallDev;
@@ -45,6 +46,8 @@ struct Workspace {
   size_t out_stage_bytes = 0;
   float* p0buf = nullptr;  // nbldpc_decode_pmf: [S][N][q] channel spectra
   size_t p0buf_bytes = 0;
+  void* ls_base = nullptr;  // conventional Log-SP: W [2][S][E][q], L0 [S][N][q], xhat [S][N], counter
+  size_t ls_bytes = 0;
   // launch accounting of the most recent decode
   cudaStream_t last_stream = nullptr;
   int last_graph = 0;
@@ -130,6 +133,7 @@ void free_workspace(Workspace& w) {
   if (w.llr_stage) cudaFree(w.llr_stage);
   if (w.out_stage) cudaFree(w.out_stage);
   if (w.p0buf) cudaFree(w.p0buf);
+  if (w.ls_base) cudaFree(w.ls_base);
   w = Workspace{};
 }
 
@@ -474,6 +478,82 @@ int default_slots(const nbldpc_code_s* c, int frames) {
   return (int)S;
 }
 
+// ---- conventional Log-SP (NBLDPC_ALG_LOG_SP): one CTA per frame, persistent
+template <int MB>
+void* ls_fn() { return reinterpret_cast<void*>(&nb::ls_frame_kernel<MB>); }
+void* ls_kernel_ptr(int m) {
+  switch (m) {
+    case 1: return ls_fn<1>();
+    case 2: return ls_fn<2>();
+    case 3: return ls_fn<3>();
+    case 4: return ls_fn<4>();
+    case 5: return ls_fn<5>();
+    case 6: return ls_fn<6>();
+    case 7: return ls_fn<7>();
+    case 8: return ls_fn<8>();
+  }
+  return nullptr;
+}
+
+nbldpc_status_t decode_logsp(nbldpc_code_s* c, const float* llr, const float* pmf, int frames, int max_iters,
+                             uint8_t* hard, uint8_t* ok, int32_t* iters, int early, cudaStream_t st) {
+  NB_TRY(cudaSetDevice(c->device));
+  const int q = c->q, tt = q < 16 ? 1 : q / 16;
+  // teams of tt threads, each with (k_max + 1) vectors of q floats in shared memory; at most 256
+  // threads and ~200 KB per CTA
+  const size_t per_team = (size_t)(c->k_max + 1) * q * sizeof(float);
+  const size_t tables = (size_t)3 * q * sizeof(int);
+  int teams = std::min(256 / tt, (int)((200u * 1024u - tables) / per_team));
+  if (teams < 1) return NBLDPC_ERR_UNSUPPORTED;
+  const int threads = ((teams * tt + 31) / 32) * 32;
+  const size_t smem = teams * per_team + tables;
+  void* fn = ls_kernel_ptr(c->m);
+  NB_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  NB_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
+  if (per_sm < 1) return NBLDPC_ERR_UNSUPPORTED;
+  const int S = std::min(frames, per_sm * c->sms);
+  Workspace& w = c->ws;
+  const size_t bW = align_up(2 * (size_t)S * c->E * q * sizeof(float), 256);
+  const size_t bL = align_up((size_t)S * c->N * q * sizeof(float), 256);
+  const size_t bX = align_up((size_t)S * c->N, 256);
+  const size_t need = bW + bL + bX + 256;
+  if (w.ls_bytes < need) {
+    if (w.ls_base) {
+      NB_TRY(cudaStreamSynchronize(st));
+      cudaFree(w.ls_base);
+      w.ls_base = nullptr;
+      w.ls_bytes = 0;
+    }
+    NB_TRY(cudaMalloc(&w.ls_base, need));
+    w.ls_bytes = need;
+  }
+  char* b = static_cast<char*>(w.ls_base);
+  nb::LsParams P{};
+  P.code = make_params(c, 0, nullptr).code;
+  P.W = reinterpret_cast<float*>(b);
+  P.L0s = reinterpret_cast<float*>(b + bW);
+  P.xh = reinterpret_cast<uint8_t*>(b + bW + bL);
+  P.glob = reinterpret_cast<int32_t*>(b + bW + bL + bX);
+  P.llr = llr;
+  P.pmf = pmf;
+  P.hard = hard;
+  P.ok = ok;
+  P.iters = iters;
+  P.frames = frames;
+  P.max_iters = max_iters;
+  P.early_stop = early;
+  P.teams = teams;
+  P.kmax = c->k_max;
+  NB_TRY(cudaMemsetAsync(P.glob, 0, sizeof(int32_t), st));
+  void* args[] = {&P};
+  NB_TRY(cudaLaunchKernel(fn, dim3((unsigned)S), dim3((unsigned)threads), args, smem, st));
+  w.last_stream = st;
+  w.last_graph = 0;
+  w.last_host_launches = 1;
+  return NBLDPC_OK;
+}
+
 // pmf != NULL: nbldpc_decode_pmf (llr unused; the direct kernel with the general channel spectrum)
 nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int max_iters, uint8_t* hard,
                             uint8_t* ok, int32_t* iters, cudaStream_t st, const nbldpc_decode_opts_t* opts,
@@ -494,6 +574,12 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
     direct = opts->vn_algorithm;
     post = opts->symbol_post_out;
     xmap = opts->symbol_map_out;
+    if (opts->algorithm == NBLDPC_ALG_LOG_SP) {
+      // the comparison algorithm: symbol-MAP decisions and the exact syndrome only
+      if (mode != 0 || soft || events || post || xmap) return NBLDPC_ERR_INVALID_ARGUMENT;
+      return decode_logsp(c, llr, pmf, frames, max_iters, hard, ok, iters, early, st);
+    }
+    if (opts->algorithm != NBLDPC_ALG_LOG_FOURIER) return NBLDPC_ERR_INVALID_ARGUMENT;
   }
   if ((post && (!is_device_ptr(post) || ((uintptr_t)post & 15))) || (xmap && !is_device_ptr(xmap)))
     return NBLDPC_ERR_INVALID_ARGUMENT;
