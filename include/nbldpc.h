@@ -55,7 +55,11 @@ typedef enum {
                               P^0 = (x)_i (1, tanh(L_i/2)), so the XOR-
                               convolution factors into m butterfly stages x(z) += t_i x(z ^ alpha^i):
                               m 2^m FMAs per edge */
-  NBLDPC_VN_DIRECT = 1     /* the paper's CONV (Table 1): 2^{2m} FMAs per edge */
+  NBLDPC_VN_DIRECT = 1,    /* the paper's CONV (Table 1): 2^{2m} FMAs per edge */
+  NBLDPC_VN_GENERAL = 2    /* any column weight: the (d-1)-fold convolution in the probability
+                              domain, U_i = WHT(p^0 prod_{i' != i} WHT(W_i') / 2^m), one CTA per frame; always
+                              used when some column weight is not 2 (the paper syndrome mode is then
+                              unavailable) */
 } nbldpc_vn_algorithm_t;
 
 /* Decoding algorithm (nbldpc_decode_opts_t::algorithm). */
@@ -101,8 +105,10 @@ typedef struct {
  *   M, N      : H is M x N
  *   rows, cols, coeffs : HOST arrays of length nnz, 0-based indices, coefficients in [1, 2^m-1]
  *   out       : receives the handle (caller owns it; release with nbldpc_destroy)
- * Every column must have exactly two nonzeros in distinct rows (j = 2) and every
- * row at least two.  The handle copies H, builds its device tables (GF tables, canonical edge list,
+ * Every column must have 1..16 nonzeros in distinct rows and every row at least two.  Column weight 2
+ * everywhere (the (2,k) codes of PAPER.md:36-41) runs the Log-Fourier cluster kernel; any other column
+ * weight ("the extension ... is straightforward") runs NBLDPC_VN_GENERAL, for which
+ * nbldpc_step and NBLDPC_ALG_LOG_SP are unavailable (NBLDPC_ERR_UNSUPPORTED).  The handle copies H, builds its device tables (GF tables, canonical edge list,
  * Fourier permutation bases) on the CUDA device current at the call, and is
  * immutable afterwards.  Decoding must happen on that device. */
 nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int nnz, const int32_t* rows,
@@ -119,7 +125,7 @@ const char* nbldpc_status_string(nbldpc_status_t s);
  * NBLDPC_ERR_OUT_OF_MEMORY ("" if none).  Thread-local storage, valid until the next call. */
 const char* nbldpc_last_cuda_error(void);
 
-/* Code dimensions (any pointer may be NULL): field degree m, rows M, columns N, edges E = 2N,
+/* Code dimensions (any pointer may be NULL): field degree m, rows M, columns N, edges E = nnz (2N for column weight 2),
  * largest row degree k_max. */
 nbldpc_status_t nbldpc_code_info(nbldpc_code_t code, int* m, int* M, int* N, int* E, int* k_max);
 

@@ -18,6 +18,7 @@
 #include "../../include/nbldpc.h"
 #include "decoder.cuh"
 #include "logsp.cuh"
+#include "lf_general.cuh"
 #include "lf_cluster.cuh"
 
 using nb::CallDev;
@@ -31,6 +32,7 @@ namespace {
 constexpr int kPassesPerGraphIter = 8;               // pass kernels per WHILE-body iteration
 constexpr size_t kDefaultSlotBudget = 64ull << 20;  // bytes of slot state kept L2-resident
 constexpr int kBigBlock = 512;                       // block-size variant for k_max * TT > 256
+constexpr int kMaxColWeight = 16;                    // column weights 1..16 (the general kernel)
 
 struct Workspace {
   int S = 0, Y = 1;
@@ -65,6 +67,11 @@ struct nbldpc_code_s {
   uint8_t* gf_exp_d = nullptr;
   uint8_t* gf_log_d = nullptr;
   uint64_t* pinv_tab_d = nullptr;
+  // variable -> edges (internal slots), for the general-column-weight kernel
+  int j_max = 2, nnz = 0;
+  bool colw2 = true;  // every column has weight 2: the cluster / pass kernels apply
+  int32_t* v_ptr_d = nullptr;
+  int32_t* v_edges_d = nullptr;
   std::mutex mu;
   Workspace ws;
   // launch geometry of the pass kernel (NBLDPC_VN_DIRECT)
@@ -554,6 +561,87 @@ nbldpc_status_t decode_logsp(nbldpc_code_s* c, const float* llr, const float* pm
   return NBLDPC_OK;
 }
 
+// ---- any column weight (NBLDPC_VN_GENERAL, lf_general.cuh): one CTA per frame, persistent
+template <int MB>
+void* gen_fn() { return reinterpret_cast<void*>(&nb::lfg_frame_kernel<MB>); }
+void* gen_kernel_ptr(int m) {
+  switch (m) {
+    case 1: return gen_fn<1>();
+    case 2: return gen_fn<2>();
+    case 3: return gen_fn<3>();
+    case 4: return gen_fn<4>();
+    case 5: return gen_fn<5>();
+    case 6: return gen_fn<6>();
+    case 7: return gen_fn<7>();
+    case 8: return gen_fn<8>();
+  }
+  return nullptr;
+}
+
+nbldpc_status_t decode_general(nbldpc_code_s* c, const float* llr, const float* pmf, int frames, int max_iters,
+                               uint8_t* hard, uint8_t* ok, int32_t* iters, int early, float* soft, int32_t* events,
+                               float* post, uint8_t* xmap, cudaStream_t st) {
+  NB_TRY(cudaSetDevice(c->device));
+  const int q = c->q, tt = q < 16 ? 1 : q / 16;
+  const int vs = std::max(1, c->j_max);
+  const size_t per_team = (size_t)vs * q * sizeof(float);
+  const size_t tables = (size_t)3 * q * sizeof(int);
+  const int teams = std::min(256 / tt, (int)((100u * 1024u - tables) / per_team));
+  if (teams < 1) return NBLDPC_ERR_UNSUPPORTED;
+  const int threads = ((teams * tt + 31) / 32) * 32;
+  const size_t smem = teams * per_team + tables;
+  void* fn = gen_kernel_ptr(c->m);
+  NB_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  NB_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
+  if (per_sm < 1) return NBLDPC_ERR_UNSUPPORTED;
+  const int S = std::min(frames, per_sm * c->sms);
+  Workspace& w = c->ws;
+  const size_t bM = align_up((size_t)S * c->E * q * sizeof(float), 256);
+  const size_t bX = align_up((size_t)S * c->N, 256);
+  const size_t need = 2 * bM + bX + 256;
+  if (w.ls_bytes < need) {  // shares the Log-SP workspace (one decode per handle at a time)
+    if (w.ls_base) {
+      NB_TRY(cudaStreamSynchronize(st));
+      cudaFree(w.ls_base);
+      w.ls_base = nullptr;
+      w.ls_bytes = 0;
+    }
+    NB_TRY(cudaMalloc(&w.ls_base, need));
+    w.ls_bytes = need;
+  }
+  char* b = static_cast<char*>(w.ls_base);
+  nb::GenParams P{};
+  P.code = make_params(c, 0, nullptr).code;
+  P.v_ptr = c->v_ptr_d;
+  P.v_edges = c->v_edges_d;
+  P.U = reinterpret_cast<float*>(b);
+  P.W = reinterpret_cast<float*>(b + bM);
+  P.xh = reinterpret_cast<uint8_t*>(b + 2 * bM);
+  P.glob = reinterpret_cast<int32_t*>(b + 2 * bM + bX);
+  P.llr = llr;
+  P.pmf = pmf;
+  P.hard = hard;
+  P.ok = ok;
+  P.iters = iters;
+  P.soft_out = soft;
+  P.events_out = events;
+  P.post_out = post;
+  P.map_out = xmap;
+  P.frames = frames;
+  P.max_iters = max_iters;
+  P.early_stop = early;
+  P.teams = teams;
+  P.jmax = c->j_max;
+  NB_TRY(cudaMemsetAsync(P.glob, 0, sizeof(int32_t), st));
+  void* args[] = {&P};
+  NB_TRY(cudaLaunchKernel(fn, dim3((unsigned)S), dim3((unsigned)threads), args, smem, st));
+  w.last_stream = st;
+  w.last_graph = 0;
+  w.last_host_launches = 1;
+  return NBLDPC_OK;
+}
+
 // pmf != NULL: nbldpc_decode_pmf (llr unused; the direct kernel with the general channel spectrum)
 nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int max_iters, uint8_t* hard,
                             uint8_t* ok, int32_t* iters, cudaStream_t st, const nbldpc_decode_opts_t* opts,
@@ -577,6 +665,7 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
     if (opts->algorithm == NBLDPC_ALG_LOG_SP) {
       // the comparison algorithm: symbol-MAP decisions and the exact syndrome only
       if (mode != 0 || soft || events || post || xmap) return NBLDPC_ERR_INVALID_ARGUMENT;
+      if (!c->colw2) return NBLDPC_ERR_UNSUPPORTED;  // its variable node is the degree-2 one
       return decode_logsp(c, llr, pmf, frames, max_iters, hard, ok, iters, early, st);
     }
     if (opts->algorithm != NBLDPC_ALG_LOG_FOURIER) return NBLDPC_ERR_INVALID_ARGUMENT;
@@ -584,7 +673,12 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   if ((post && (!is_device_ptr(post) || ((uintptr_t)post & 15))) || (xmap && !is_device_ptr(xmap)))
     return NBLDPC_ERR_INVALID_ARGUMENT;
   if (mode != 0 && mode != 1) return NBLDPC_ERR_INVALID_ARGUMENT;
-  if (direct != 0 && direct != 1) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (direct < 0 || direct > 2) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (!c->colw2 || direct == 2) {  // column weights != 2, or asked for: the general kernel
+    if (mode != 0) return NBLDPC_ERR_INVALID_ARGUMENT;
+    if ((soft && !is_device_ptr(soft)) || (events && !is_device_ptr(events))) return NBLDPC_ERR_INVALID_ARGUMENT;
+    return decode_general(c, llr, pmf, frames, max_iters, hard, ok, iters, early, soft, events, post, xmap, st);
+  }
   if ((post || xmap) && direct == 0) direct = 1;  // the symbol decision lives in the pass kernel
   if (pmf && direct) direct = 2;                   // the pass kernel's pmf variant
   if (slots < 0) return NBLDPC_ERR_INVALID_ARGUMENT;
@@ -723,8 +817,14 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
     colw[cols[i]]++;
     roww[rows[i]]++;
   }
-  for (int v = 0; v < N; ++v)
-    if (colw[v] != 2) return NBLDPC_ERR_UNSUPPORTED;
+  // column weights 1..16 (weight 2: the Log-Fourier cluster kernel; others: lf_general.cuh)
+  int j_max = 0;
+  bool colw2 = true;
+  for (int v = 0; v < N; ++v) {
+    if (colw[v] < 1 || colw[v] > kMaxColWeight) return NBLDPC_ERR_UNSUPPORTED;
+    j_max = std::max(j_max, colw[v]);
+    colw2 = colw2 && colw[v] == 2;
+  }
   int k_max = 0, k_min = 1 << 30;
   for (int r = 0; r < M; ++r) {
     if (roww[r] < 2) return NBLDPC_ERR_UNSUPPORTED;
@@ -766,7 +866,11 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
       ed.pinvb[bi] = (uint8_t)imginv;
     }
     const int v = cols[i];
-    if (first[v] < 0) {
+    if (!colw2) {  // no partner edge: the general kernel walks the variable's edge list
+      ed.partner = e;
+      ed.is_a = first[v] < 0 ? 1 : 0;
+      if (first[v] < 0) first[v] = e;
+    } else if (first[v] < 0) {
       first[v] = e;
       ed.is_a = 1;
     } else {
@@ -794,6 +898,9 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
   c->con_stride = (int)align_up((size_t)E, 16);
   c->row_regular = k_min == k_max && kpad == k_max;
   c->poly = prim_poly;
+  c->j_max = j_max;
+  c->colw2 = colw2;
+  c->nnz = nnz;
   auto bail = [&](cudaError_t e) {
     cudaGetLastError();
     nbldpc_destroy(c);
@@ -805,6 +912,18 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
   if (cudaError_t e = cudaMemcpy(c->edges_d, edges.data(), sizeof(EdgeDev) * E, cudaMemcpyHostToDevice)) return bail(e);
   if (cudaError_t e = cudaMemcpy(c->gf_exp_d, gexp.data(), gexp.size(), cudaMemcpyHostToDevice)) return bail(e);
   if (cudaError_t e = cudaMemcpy(c->gf_log_d, glog.data(), q, cudaMemcpyHostToDevice)) return bail(e);
+  {
+    // variable -> its edges in canonical order (internal slots)
+    std::vector<int32_t> vptr(N + 1, 0), vedges(nnz);
+    for (int v = 0; v < N; ++v) vptr[v + 1] = vptr[v] + colw[v];
+    std::vector<int32_t> pos(vptr.begin(), vptr.end() - 1);
+    for (int e = 0; e < E; ++e)
+      if (edges[e].var >= 0) vedges[pos[edges[e].var]++] = e;
+    if (cudaError_t e = cudaMalloc(&c->v_ptr_d, sizeof(int32_t) * (N + 1))) return bail(e);
+    if (cudaError_t e = cudaMalloc(&c->v_edges_d, sizeof(int32_t) * nnz)) return bail(e);
+    if (cudaError_t e = cudaMemcpy(c->v_ptr_d, vptr.data(), sizeof(int32_t) * (N + 1), cudaMemcpyHostToDevice)) return bail(e);
+    if (cudaError_t e = cudaMemcpy(c->v_edges_d, vedges.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice)) return bail(e);
+  }
   {
     // pi_h^-1(alpha^i) = pi_{h^-1}(alpha^i): bit j = bit i of h^-1 * alpha^j
     std::vector<uint64_t> pt(q, 0);
@@ -920,6 +1039,8 @@ void nbldpc_destroy(nbldpc_code_t c) {
   cudaFree(c->gf_exp_d);
   cudaFree(c->gf_log_d);
   cudaFree(c->pinv_tab_d);
+  cudaFree(c->v_ptr_d);
+  cudaFree(c->v_edges_d);
   delete c;
 }
 
@@ -928,7 +1049,7 @@ nbldpc_status_t nbldpc_code_info(nbldpc_code_t c, int* m, int* M, int* N, int* E
   if (m) *m = c->m;
   if (M) *M = c->M;
   if (N) *N = c->N;
-  if (E) *E = 2 * c->N;
+  if (E) *E = c->nnz;
   if (k_max) *k_max = c->k_max;
   return NBLDPC_OK;
 }
@@ -1034,7 +1155,7 @@ nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int i
   if (iter >= 1 && (!is_device_ptr(w_in) || !is_device_ptr(hard))) return NBLDPC_ERR_INVALID_ARGUMENT;
   if ((u_out && !is_device_ptr(u_out)) || (soft && !is_device_ptr(soft))) return NBLDPC_ERR_INVALID_ARGUMENT;
   if (vn_algorithm != 0 && vn_algorithm != 1) return NBLDPC_ERR_INVALID_ARGUMENT;
-  if (!c->row_regular) return NBLDPC_ERR_UNSUPPORTED;  // internal edge slots == canonical order only then
+  if (!c->row_regular || !c->colw2) return NBLDPC_ERR_UNSUPPORTED;  // internal slots == canonical order only then
   std::lock_guard<std::mutex> lk(c->mu);
   NB_TRY(cudaSetDevice(c->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);

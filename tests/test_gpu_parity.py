@@ -266,7 +266,7 @@ def test_edge_cases_and_errors(dev):
         nb.Code(2, 0x5, M, c["N"], rows, cols, coeffs)  # x^2+1 not primitive
     assert ei.value.status == -2
     with pytest.raises(nb.NbldpcError) as ei:
-        nb.Code(2, 0x7, M, c["N"], rows[:-1], cols[:-1], coeffs[:-1])  # a column of weight 1
+        nb.Code(2, 0x7, M, c["N"] + 1, rows, cols, coeffs)  # a column of weight 0
     assert ei.value.status == -3
     bad = coeffs.copy()
     bad[0] = 4

@@ -69,7 +69,12 @@ def test_code_create_validation_without_gpu(L):
     badr = rows.copy()
     badr[0] = M
     assert _create(L, 2, 0x7, M, N, badr, cols, coeffs)[0] == -1  # row out of range
-    assert _create(L, 2, 0x7, M, N, rows[:-1], cols[:-1], coeffs[:-1])[0] == -3  # a weight-1 column
+    assert _create(L, 2, 0x7, M, N + 1, rows, cols, coeffs)[0] == -3  # a weight-0 column (variable N)
+    hv = np.arange(17, dtype=np.int32)  # a weight-17 column: 17 extra rows of degree 2 over variables 0 and 1
+    r17 = np.concatenate([rows, M + hv, M + hv])
+    c17 = np.concatenate([cols, np.zeros(17, np.int32), np.ones(17, np.int32)])
+    h17 = np.concatenate([coeffs, np.ones(34, coeffs.dtype)])
+    assert _create(L, 2, 0x7, M + 17, N, r17, c17, h17)[0] == -3
     dup_r = np.concatenate([rows, rows[:1]])
     dup_c = np.concatenate([cols, cols[:1]])
     dup_h = np.concatenate([coeffs, coeffs[:1]])
