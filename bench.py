@@ -57,7 +57,11 @@ def per_frame_iter(cfg, vn, inp="llr", symbol_out=False, algorithm="lf"):
     buffer) instead of m channel terms; symbol_out: + the symbol posterior written per iteration
     and its two WHTs (counted as FMA-pipe ops)."""
     N, q, m = cfg["N"], cfg["q"], cfg["m"]
-    E = 2 * N
+    E = cfg["j"] * N
+    if vn == 2 or cfg["j"] != 2:
+        # general kernel: per edge 2 WHTs (W -> w, product -> U) of m q butterflies, the leave-one-out
+        # products; per variable the decision sums; messages U and W each written once and read once
+        return 2 * E * q, 2 * E * m * q + E * q * cfg["j"] + N * (m + 1) * q, 4 * E * q * 4 + 4 * N * m + N
     if algorithm == "logsp":
         # conventional Log-SP (PAPER.md:231-281): 3(k-2) q^2-term log-convolutions per check (forward-
         # backward), each input exponentiated twice and each output's log once; messages + lambda^0
@@ -121,7 +125,7 @@ def info_bits(cfg) -> float:
 def workload_name(cfg, point, inp="llr", ebn0=None):
     eb = cfg["ebn0"][point] if ebn0 is None else ebn0
     ch = "BPSK/AWGN bit LLRs" if inp == "llr" else f"{cfg['q']}-ary orthogonal signalling/AWGN symbol pmfs"
-    return (f"{cfg['name']}: GF({cfg['q']}) (2,{cfg['k']})-regular N={cfg['N']} rate {cfg['rate']:.4g}, "
+    return (f"{cfg['name']}: GF({cfg['q']}) ({cfg['j']},{cfg['k']})-regular N={cfg['N']} rate {cfg['rate']:.4g}, "
             f"{ch}, Eb/N0={eb} dB, max {cfg['max_iters']} iters, early stop, "
             f"{'random' if cfg['codeword'] == 'random' else 'all-zero'} codewords")
 
@@ -228,7 +232,8 @@ def main():
     ap.add_argument("--frames", type=int, default=0, help="frames per rank (default: the config's)")
     ap.add_argument("--slots", type=int, default=0)
     ap.add_argument("--graph", type=int, default=0, help="direct path only: 0 graph, -1 host loop")
-    ap.add_argument("--vn", type=int, default=0, help="0 separable (default), 1 direct q^2 convolution")
+    ap.add_argument("--vn", type=int, default=0,
+                    help="0 separable (default), 1 direct q^2 convolution, 2 general column weight kernel")
     ap.add_argument("--input", default="llr", choices=["llr", "pmf"],
                     help="llr: BPSK bit LLRs (nbldpc_decode); pmf: symbol pmfs (nbldpc_decode_pmf)")
     ap.add_argument("--ebn0", type=float, default=None, help="override the config's Eb/N0 (dB)")
@@ -363,13 +368,16 @@ def main():
                       "CUDA events around the step)") if vn == 0 else "nb_pass_kernel (slot passes)"
     if args.algorithm == "logsp":
         roof["kernel"] = "ls_frame_kernel (conventional Log-SP, one CTA per frame; one launch per step)"
+    elif vn == 2 or cfg["j"] != 2:
+        roof["kernel"] = "lfg_frame_kernel (general column weight, one CTA per frame; one launch per step)"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": warm, "ms_per_step": tim["ms"] / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_name(cfg, args.point, args.input, args.ebn0), "frames_per_gpu": F,
                    "global_frames": F * world, "N": cfg["N"], "q": cfg["q"], "k": cfg["k"],
-                   "max_iters": cfg["max_iters"], "vn_algorithm": ["separable", "direct"][vn],
+                   "max_iters": cfg["max_iters"], "vn_algorithm": ["separable", "direct", "general"][vn],
+                   "column_weight": cfg["j"],
                    "input": args.input, "symbol_outputs": bool(args.symbol_out), "algorithm": args.algorithm,
                    "parallelism": f"frames sharded over {world} GPU(s), no collective in the loop",
                    "l2": "flushed (256 MiB write) before every timed step",

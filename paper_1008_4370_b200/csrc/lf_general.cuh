@@ -53,8 +53,11 @@ __global__ void __launch_bounds__(256) lfg_frame_kernel(GenParams P) {
   const bool in_team = team < P.teams;
   const unsigned tmask = TT >= 32 ? 0xffffffffu : (((1u << TT) - 1u) << (lane & ~(TT - 1)));
   const int VS = P.jmax > 1 ? P.jmax : 1;  // team vectors: w_1..w_d (variable phase) / TOT (check phase)
-  float* const Tb = smem + (size_t)(in_team ? team : 0) * VS * Q;
-  int* const gexp = reinterpret_cast<int*>(smem + (size_t)P.teams * VS * Q);
+  // team stride padded to TT (mod 32): the per-thread vector entries at [i][r][t] of the teams of a
+  // warp then fall in 32 distinct banks
+  const int TS = VS * Q + ((TT - (VS * Q) % 32) & 31);
+  float* const Tb = smem + (size_t)(in_team ? team : 0) * TS;
+  int* const gexp = reinterpret_cast<int*>(smem + (size_t)P.teams * TS);
   int* const glog = gexp + 2 * Q;
   for (int i = tid; i < 2 * (Q - 1) + 1; i += nthr) gexp[i] = cd.gf_exp[i];
   for (int i = tid; i < Q; i += nthr) glog[i] = cd.gf_log[i];
@@ -99,6 +102,30 @@ __global__ void __launch_bounds__(256) lfg_frame_kernel(GenParams P) {
       for (int jj = 0; jj < (1 << i); ++jj) idx[(1 << i) + jj] = idx[jj] ^ b[i];
   };
 
+  auto ld_block = [&](const float* src, float (&x)[R]) {  // R consecutive floats (16-byte aligned when R >= 4)
+    if constexpr (R >= 4) {
+#pragma unroll
+      for (int c4 = 0; c4 < R / 4; ++c4) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(src) + c4);
+        x[4 * c4] = v.x; x[4 * c4 + 1] = v.y; x[4 * c4 + 2] = v.z; x[4 * c4 + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r] = __ldcg(src + r);
+    }
+  };
+  auto st_block = [&](float* dst, const float (&x)[R]) {
+    if constexpr (R >= 4) {
+#pragma unroll
+      for (int c4 = 0; c4 < R / 4; ++c4)
+        reinterpret_cast<float4*>(dst)[c4] = make_float4(x[4 * c4], x[4 * c4 + 1], x[4 * c4 + 2], x[4 * c4 + 3]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) dst[r] = x[r];
+    }
+  };
+#define TW(i, r) Tb[(i) * Q + (r) * TT + t]
+
   const int slot = blockIdx.x;
   const size_t EQ = (size_t)cd.E * Q;
   float* const U = P.U + (size_t)slot * EQ;
@@ -125,10 +152,10 @@ __global__ void __launch_bounds__(256) lfg_frame_kernel(GenParams P) {
         // p_v^0(x) for x = tR + r: the bit product, or the scaled pmf row
         float p0[R];
         if (P.pmf) {
-          const float* src = P.pmf + ((size_t)f * cd.N + v) * Q + t * R;
+          ld_block(P.pmf + ((size_t)f * cd.N + v) * Q + t * R, p0);
           float s = 0.0f;
 #pragma unroll
-          for (int r = 0; r < R; ++r) { p0[r] = src[r]; s += p0[r]; }
+          for (int r = 0; r < R; ++r) s += p0[r];
           s = team_sum(s);
           const float inv = s > 0.0f ? 1.0f / s : 0.0f;
 #pragma unroll
@@ -155,20 +182,20 @@ __global__ void __launch_bounds__(256) lfg_frame_kernel(GenParams P) {
         // w_i = WHT(W_i) / q, kept in the team's vectors (each thread its own block)
         if (ell > 0) {
           for (int i = 0; i < d; ++i) {
-            const float* src = W + (size_t)P.v_edges[e0 + i] * Q + t * R;
             float x[R];
+            ld_block(W + (size_t)P.v_edges[e0 + i] * Q + t * R, x);
 #pragma unroll
-            for (int r = 0; r < R; ++r) x[r] = to_lin(src[r]);
+            for (int r = 0; r < R; ++r) x[r] = to_lin(x[r]);
             wht(x);
 #pragma unroll
-            for (int r = 0; r < R; ++r) Tb[i * Q + t * R + r] = x[r] * kInvQ;
+            for (int r = 0; r < R; ++r) TW(i, r) = x[r] * kInvQ;
           }
           // decision: mu = p0 prod_i w_i; M(0) and M(alpha^b) by signed sums
           float mu[R];
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             float a = p0[r];
-            for (int i = 0; i < d; ++i) a *= Tb[i * Q + t * R + r];
+            for (int i = 0; i < d; ++i) a *= TW(i, r);
             mu[r] = a;
           }
           float Ms[MB + 1];
@@ -236,7 +263,7 @@ __global__ void __launch_bounds__(256) lfg_frame_kernel(GenParams P) {
             float a = p0[r];
             if (ell > 0)
               for (int i2 = 0; i2 < d; ++i2)
-                if (i2 != i) a *= Tb[i2 * Q + t * R + r];
+                if (i2 != i) a *= TW(i2, r);
             x[r] = a;
           }
           wht(x);
@@ -244,13 +271,13 @@ __global__ void __launch_bounds__(256) lfg_frame_kernel(GenParams P) {
           if constexpr (TT > 1) raw0 = __shfl_sync(tmask, x[0], lane & ~(TT - 1));
           const bool neutral = !(raw0 > 0.0f);  // reading R10
           const float lg0 = lg2a(raw0);
-          float* dst = U + (size_t)P.v_edges[e0 + i] * Q + t * R;
+          float pk[R];
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            float pk = pack(lg0 - lg2a(fabsf(x[r])), __float_as_uint(x[r]));
-            if (neutral) pk = (t == 0 && r == 0) ? 0.0f : kFloor;
-            dst[r] = pk;
+            pk[r] = pack(lg0 - lg2a(fabsf(x[r])), __float_as_uint(x[r]));
+            if (neutral) pk[r] = (t == 0 && r == 0) ? 0.0f : kFloor;
           }
+          st_block(U + (size_t)P.v_edges[e0 + i] * Q + t * R, pk);
           if (neutral && t == 0) atomicAdd(&sh_events, 1);
         }
       }
@@ -280,27 +307,30 @@ __global__ void __launch_bounds__(256) lfg_frame_kernel(GenParams P) {
             const float* src = U + (size_t)(eb + k) * Q;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-              const float u = src[idx[r]];
+              const float u = __ldcg(src + idx[r]);
               mag[r] += fabsf(u);
               sg[r] ^= __float_as_uint(u);
             }
           }
+          {
+            // scalar stores: the padded team stride keeps Tb only 4-byte aligned
 #pragma unroll
-          for (int r = 0; r < R; ++r) Tb[t * R + r] = __uint_as_float(__float_as_uint(mag[r]) | (sg[r] & kSign));
+            for (int r = 0; r < R; ++r) Tb[t * R + r] = __uint_as_float(__float_as_uint(mag[r]) | (sg[r] & kSign));
+          }
           if constexpr (TT > 1) __syncwarp(tmask);
           // W_j(z) = TOT(pi_j^-1 z) - U_j(z)
           for (int j = 0; j < kc; ++j) {
             const EdgeDev ed = cd.edges[eb + j];
             int idx[R];
             perm_block(ed.pinvb, idx);
-            const float* uj = U + (size_t)(eb + j) * Q + t * R;
-            float* dst = W + (size_t)(eb + j) * Q + t * R;
+            float uj[R], o[R];
+            ld_block(U + (size_t)(eb + j) * Q + t * R, uj);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               const float tt = Tb[idx[r]];
-              const float u = uj[r];
-              dst[r] = pack(fabsf(tt) - fabsf(u), __float_as_uint(tt) ^ __float_as_uint(u));
+              o[r] = pack(fabsf(tt) - fabsf(uj[r]), __float_as_uint(tt) ^ __float_as_uint(uj[r]));
             }
+            st_block(W + (size_t)(eb + j) * Q + t * R, o);
           }
           if constexpr (TT > 1) __syncwarp(tmask);
         }
@@ -331,6 +361,7 @@ __global__ void __launch_bounds__(256) lfg_frame_kernel(GenParams P) {
     }
     __syncthreads();
   }
+#undef TW
 }
 
 }  // namespace nb

@@ -584,7 +584,8 @@ nbldpc_status_t decode_general(nbldpc_code_s* c, const float* llr, const float* 
   NB_TRY(cudaSetDevice(c->device));
   const int q = c->q, tt = q < 16 ? 1 : q / 16;
   const int vs = std::max(1, c->j_max);
-  const size_t per_team = (size_t)vs * q * sizeof(float);
+  const int ts = vs * q + ((tt - (vs * q) % 32) & 31);  // the kernel's padded team stride (floats)
+  const size_t per_team = (size_t)ts * sizeof(float);
   const size_t tables = (size_t)3 * q * sizeof(int);
   const int teams = std::min(256 / tt, (int)((100u * 1024u - tables) / per_team));
   if (teams < 1) return NBLDPC_ERR_UNSUPPORTED;

@@ -31,13 +31,16 @@ CONFIGS = {
     "C4": dict(m=8, poly=0x11D, k=16, N=2048, frames=16384, ebn0=[3.5], max_iters=30, codeword="zero"),
     "C5": dict(m=4, poly=0x13, k=32, N=4096, frames=65536, ebn0=[3.0, 3.5, 4.0, 4.5, 5.0], max_iters=50,
                codeword="zero"),
+    # not in BASELINE.json: the column-weight-3 workload of the SURVEY 8(f) row 3 measurements
+    "J3": dict(m=6, poly=0x43, k=6, N=1024, frames=4096, ebn0=[2.0], max_iters=50, codeword="zero", j=3),
 }
 for _i, (_name, _c) in enumerate(CONFIGS.items()):
     _c["name"] = _name
     _c["index"] = _i
     _c["q"] = 1 << _c["m"]
-    _c["M"] = 2 * _c["N"] // _c["k"]
-    _c["rate"] = 1.0 - 2.0 / _c["k"]
+    _c.setdefault("j", 2)
+    _c["M"] = _c["j"] * _c["N"] // _c["k"]
+    _c["rate"] = 1.0 - _c["j"] / _c["k"]
     _c["seed_graph"] = 1000 + _i
     _c["seed_codeword"] = 2000 + _i
     _c["seed_noise"] = 3000 + _i
@@ -100,7 +103,7 @@ def make_regular_code(N: int, k: int, m: int, seed: int, j: int = 2):
 
 def config_code(name: str):
     c = CONFIGS[name]
-    return make_regular_code(c["N"], c["k"], c["m"], c["seed_graph"])
+    return make_regular_code(c["N"], c["k"], c["m"], c["seed_graph"], j=c["j"])
 
 
 def random_symbols(n: int, q: int, seed: int, stream: int = 0) -> np.ndarray:
