@@ -51,7 +51,7 @@ def hbm_peak():
         return HBM_PEAK_FALLBACK, "fallback"
 
 
-def per_frame_iter(cfg, vn, inp="llr", symbol_out=False, algorithm="lf"):
+def per_frame_iter(cfg, vn, inp="llr", symbol_out=False, algorithm="lf", msg="f32"):
     """Algorithmic work of one frame-iteration: SFU ops, FP32 FMAs, message bytes.
     inp = "pmf": the channel spectrum is a q-vector per variable (read per iteration from the slot
     buffer) instead of m channel terms; symbol_out: + the symbol posterior written per iteration
@@ -72,7 +72,7 @@ def per_frame_iter(cfg, vn, inp="llr", symbol_out=False, algorithm="lf"):
         fma = E * q * (2 * m + 1) + N * (m + 1) * q
     else:             # VN (separable / direct) + decision points
         fma = (E * m * q if vn == 0 else E * q * q) + N * (m + 1) * q
-    bytes_ = 2 * E * q * 4 + N                       # one message set read + written, symbols
+    bytes_ = 2 * E * q * (2 if msg == "f16" else 4) + N  # one message set read + written, symbols
     bytes_ += 4 * N * q if inp == "pmf" else 4 * N * m  # channel spectrum / channel terms
     if symbol_out:
         fma += N * q * (2 * m + 1)
@@ -80,10 +80,10 @@ def per_frame_iter(cfg, vn, inp="llr", symbol_out=False, algorithm="lf"):
     return mufu, fma, bytes_
 
 
-def roofline(cfg, vn, frame_iters, seconds, traffic, inp="llr", symbol_out=False, algorithm="lf"):
+def roofline(cfg, vn, frame_iters, seconds, traffic, inp="llr", symbol_out=False, algorithm="lf", msg="f32"):
     """The slower of the SFU, FP32 and HBM-message-byte bounds (BASELINE.json north_star) for the
     work done; achieved / peak of that resource over the measured kernel time."""
-    mufu, fma, byts = per_frame_iter(cfg, vn, inp, symbol_out, algorithm)
+    mufu, fma, byts = per_frame_iter(cfg, vn, inp, symbol_out, algorithm, msg)
     hbm, hbm_src = hbm_peak()
     t = {"alu": max(mufu / MUFU_PEAK, fma / FMA_PEAK), "hbm": byts / hbm}
     bound = max(t, key=t.get)
@@ -240,6 +240,8 @@ def main():
     ap.add_argument("--symbol-out", action="store_true", help="also output the symbol posterior and MAP decision")
     ap.add_argument("--algorithm", default="lf", choices=["lf", "logsp"],
                     help="lf: Log-Fourier SP (the hot path); logsp: the conventional Log-SP it is compared with")
+    ap.add_argument("--msg", default="f32", choices=["f32", "f16"],
+                    help="message storage: f32 (default) or f16 (half the message bytes; evaluated by FER)")
     ap.add_argument("--ref-frames", type=int, default=32)
     ap.add_argument("--cpu-frames", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -279,7 +281,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     kw = dict(slots=args.slots, use_graph=args.graph, want_post=args.symbol_out, vn_algorithm=vn,
-              algorithm=1 if args.algorithm == "logsp" else 0)
+              algorithm=1 if args.algorithm == "logsp" else 0, message_format=1 if args.msg == "f16" else 0)
     decode = code.decode_pmf if pmf_in else code.decode
 
     def barrier():
@@ -358,12 +360,14 @@ def main():
     traffic = None
     if os.path.exists(args.traffic):
         try:
-            key = f"{cfg['name']}:vn{vn}" + (":pmf" if pmf_in else "") + (":sym" if args.symbol_out else "")
+            key = (f"{cfg['name']}:vn{vn}" + (":pmf" if pmf_in else "") + (":sym" if args.symbol_out else "")
+                   + (":f16" if args.msg == "f16" else "") + (":logsp" if args.algorithm == "logsp" else ""))
             traffic = json.load(open(args.traffic)).get(key)
         except (OSError, ValueError):
             traffic = None
     # this rank's kernel: its frame-iterations over its own device time
-    roof = roofline(cfg, vn, iters_sum, sum(step_ms) * 1e-3, traffic, args.input, args.symbol_out, args.algorithm)
+    roof = roofline(cfg, vn, iters_sum, sum(step_ms) * 1e-3, traffic, args.input, args.symbol_out, args.algorithm,
+                    args.msg)
     roof["kernel"] = ("lf_cluster_kernel (one launch per step + a 1-block setup kernel; "
                       "CUDA events around the step)") if vn == 0 else "nb_pass_kernel (slot passes)"
     if args.algorithm == "logsp":
@@ -379,6 +383,7 @@ def main():
                    "max_iters": cfg["max_iters"], "vn_algorithm": ["separable", "direct", "general"][vn],
                    "column_weight": cfg["j"],
                    "input": args.input, "symbol_outputs": bool(args.symbol_out), "algorithm": args.algorithm,
+                   "messages": args.msg,
                    "parallelism": f"frames sharded over {world} GPU(s), no collective in the loop",
                    "l2": "flushed (256 MiB write) before every timed step",
                    "slots": args.slots or "default", "mean_iters": cnt["frame_iters"] / cnt["frames"],

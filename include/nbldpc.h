@@ -73,6 +73,16 @@ typedef enum {
                                  mode are not available (NBLDPC_ERR_INVALID_ARGUMENT) */
 } nbldpc_algorithm_t;
 
+/* Storage format of the messages in HBM / L2 (nbldpc_decode_opts_t::message_format). */
+typedef enum {
+  NBLDPC_MSG_F32 = 0, /* float32 (sign bit | -log2|x|): the reference precision */
+  NBLDPC_MSG_F16 = 1  /* IEEE half, same packing: half the message bytes (the paper's reduced-precision
+                         motivation); arithmetic stays fp32.  Only the Log-Fourier cluster
+                         kernel (NBLDPC_VN_SEPARABLE, LLR input, column weight 2, m >= 3; else
+                         NBLDPC_ERR_INVALID_ARGUMENT / NBLDPC_ERR_UNSUPPORTED).  Results are not
+                         bit-identical to F32: evaluated by frame error rate */
+} nbldpc_message_format_t;
+
 /* Options of nbldpc_decode_ex / nbldpc_decode_host.  Zero-initialise, then set
  * struct_size = sizeof(nbldpc_decode_opts_t).  NULL opts = all defaults. */
 typedef struct {
@@ -97,6 +107,7 @@ typedef struct {
    * variable) and written to the frame's output rows each time, so the last write is the
    * stopping iteration's.  The output rows hold intermediate values until the decode completes. */
   int algorithm;     /* nbldpc_algorithm_t, default NBLDPC_ALG_LOG_FOURIER */
+  int message_format; /* nbldpc_message_format_t, default NBLDPC_MSG_F32 */
 } nbldpc_decode_opts_t;
 
 /* Builds a code from H given as nnz (row, col, coefficient) triplets in any order.

@@ -27,6 +27,7 @@ _LIB = None
 NBLDPC_OK = 0
 VN_SEPARABLE, VN_DIRECT = 0, 1             # nbldpc_vn_algorithm_t
 ALG_LOG_FOURIER, ALG_LOG_SP = 0, 1        # nbldpc_algorithm_t
+MSG_F32, MSG_F16 = 0, 1                    # nbldpc_message_format_t
 _STATUS = {0: "ok", -1: "invalid argument", -2: "not primitive", -3: "unsupported", -4: "CUDA error",
            -5: "out of memory"}
 
@@ -41,7 +42,7 @@ class _Opts(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_size_t), ("syndrome_mode", ctypes.c_int), ("no_early_stop", ctypes.c_int),
                 ("soft_out", ctypes.c_void_p), ("events_out", ctypes.c_void_p), ("slots", ctypes.c_int),
                 ("use_graph", ctypes.c_int), ("vn_algorithm", ctypes.c_int), ("symbol_post_out", ctypes.c_void_p),
-                ("symbol_map_out", ctypes.c_void_p), ("algorithm", ctypes.c_int)]
+                ("symbol_map_out", ctypes.c_void_p), ("algorithm", ctypes.c_int), ("message_format", ctypes.c_int)]
 
 
 def header_symbols() -> list[str]:
@@ -146,7 +147,7 @@ class Code:
         return int(self._L.nbldpc_slot_bytes(self._h))
 
     def _opts(self, syndrome_mode=0, early_stop=True, soft=None, events=None, slots=0, use_graph=0, vn_algorithm=0,
-              post=None, xmap=None, algorithm=0):
+              post=None, xmap=None, algorithm=0, message_format=0):
         o = _Opts()
         o.struct_size = ctypes.sizeof(_Opts)
         o.syndrome_mode = int(syndrome_mode)
@@ -159,6 +160,7 @@ class Code:
         o.symbol_post_out = _ptr(post)
         o.symbol_map_out = _ptr(xmap)
         o.algorithm = int(algorithm)
+        o.message_format = int(message_format)
         return o
 
     def _outputs(self, F, dev, want_soft, want_events, want_post):
@@ -178,7 +180,7 @@ class Code:
 
     def decode(self, llr, max_iters: int, *, syndrome_mode: int = 0, early_stop: bool = True, want_soft=False,
                want_events=False, want_post=False, slots: int = 0, use_graph: int = 0, vn_algorithm: int = 0, out=None,
-               stream=None, algorithm: int = 0):
+               stream=None, algorithm: int = 0, message_format: int = 0):
         """Decode frames. ``llr``: CUDA float32 tensor [F, N*m].  Returns a dict of CUDA tensors
         (hard uint8 [F,N], ok uint8 [F], iters int32 [F], optional soft float32 [F,N*m], events int32 [F],
         post float32 [F,N,q] symbol posterior and map uint8 [F,N] symbol-MAP decision)."""
@@ -192,7 +194,7 @@ class Code:
         if out is None:
             out = self._outputs(F, llr.device, want_soft, want_events, want_post)
         o = self._opts(syndrome_mode, early_stop, out.get("soft"), out.get("events"), slots, use_graph, vn_algorithm,
-                       out.get("post"), out.get("map"), algorithm)
+                       out.get("post"), out.get("map"), algorithm, message_format)
         st = self._L.nbldpc_decode_ex(self._h, llr.data_ptr(), F, int(max_iters), out["hard"].data_ptr(),
                                       out["ok"].data_ptr(), out["iters"].data_ptr(), _stream(stream),
                                       ctypes.byref(o))
@@ -201,7 +203,7 @@ class Code:
 
     def decode_pmf(self, pmf, max_iters: int, *, syndrome_mode: int = 0, early_stop: bool = True, want_soft=False,
                    want_events=False, want_post=False, slots: int = 0, use_graph: int = 0, vn_algorithm: int = 0,
-                   out=None, stream=None, algorithm: int = 0):
+                   out=None, stream=None, algorithm: int = 0, message_format: int = 0):
         """Decode frames from symbol-level channel pmfs (nbldpc_decode_pmf).
         ``pmf``: CUDA float32 tensor [F, N, q] (any positive scale per row).  Same outputs as decode."""
         import torch
@@ -214,7 +216,7 @@ class Code:
         if out is None:
             out = self._outputs(F, pmf.device, want_soft, want_events, want_post)
         o = self._opts(syndrome_mode, early_stop, out.get("soft"), out.get("events"), slots, use_graph, vn_algorithm,
-                       out.get("post"), out.get("map"), algorithm)
+                       out.get("post"), out.get("map"), algorithm, message_format)
         st = self._L.nbldpc_decode_pmf(self._h, pmf.data_ptr(), F, int(max_iters), out["hard"].data_ptr(),
                                        out["ok"].data_ptr(), out["iters"].data_ptr(), _stream(stream),
                                        ctypes.byref(o))
@@ -222,7 +224,7 @@ class Code:
         return out
 
     def decode_host(self, llr_host, max_iters: int, *, syndrome_mode: int = 0, slots: int = 0, use_graph: int = 0,
-                    vn_algorithm: int = 0, out=None, stream=None, algorithm: int = 0):
+                    vn_algorithm: int = 0, out=None, stream=None, algorithm: int = 0, message_format: int = 0):
         """End-to-end decode from HOST memory (pinned torch tensor or numpy array) to host outputs."""
         import torch
 
@@ -236,7 +238,8 @@ class Code:
             out = {"hard": torch.empty((F, self.N), dtype=torch.uint8, pin_memory=pin),
                    "ok": torch.empty(F, dtype=torch.uint8, pin_memory=pin),
                    "iters": torch.empty(F, dtype=torch.int32, pin_memory=pin)}
-        o = self._opts(syndrome_mode, True, None, None, slots, use_graph, vn_algorithm, algorithm=algorithm)
+        o = self._opts(syndrome_mode, True, None, None, slots, use_graph, vn_algorithm, algorithm=algorithm,
+                       message_format=message_format)
         st = self._L.nbldpc_decode_host(self._h, llr_host.data_ptr(), F, int(max_iters), out["hard"].data_ptr(),
                                         out["ok"].data_ptr(), out["iters"].data_ptr(), _stream(stream),
                                         ctypes.byref(o))

@@ -26,6 +26,8 @@
 #pragma once
 #include <assert.h>
 
+#include <cuda_fp16.h>
+
 #include "decoder.cuh"
 
 // NB_BOUNDS_CHECK=1 (debug builds, `NBLDPC_DEFS=-DNB_BOUNDS_CHECK`): device asserts on every computed
@@ -101,6 +103,38 @@ __host__ __device__ __forceinline__ int mpos(int z, int row) {
     return z;
   }
 }
+
+// F16 message rows (NBLDPC_MSG_F16, q >= 8): entry z of row r at mposh(z, r), in 16-byte units of 8
+// halves XOR-swizzled by the row's position in its 128-byte line (the phase-A unit reads of the rows of
+// a quarter warp hit distinct bank quads), and for rows of >= 16 units by the unit's own bit 3
+template <int MB>
+__host__ __device__ __forceinline__ int mposh(int z, int row) {
+  constexpr int U = (1 << MB) / 8;  // units per row
+  int unit = z >> 3;
+  if constexpr (U >= 16) unit ^= (unit >> 3) & 1;
+  const int key = U >= 8 ? row : (row * U) >> 3;
+  return ((unit ^ (key & (U - 1))) << 3) | (z & 7);
+}
+#ifdef NB_MSG16_FIXED
+// experiment: sign | 15-bit fixed-point magnitude with step 2^-9 (saturating at 64)
+__device__ __forceinline__ float fx2f(uint32_t h) {
+  return __uint_as_float(__float_as_uint((float)(h & 0x7FFFu) * (1.0f / 512.0f)) | ((h & 0x8000u) << 16));
+}
+__device__ __forceinline__ uint32_t f2fx(float a) {
+  const uint32_t m = (uint32_t)fminf(rintf(fabsf(a) * 512.0f), 32767.0f);
+  return m | ((__float_as_uint(a) >> 16) & 0x8000u);
+}
+__device__ __forceinline__ float2 h2f2(uint32_t v) { return make_float2(fx2f(v & 0xFFFFu), fx2f(v >> 16)); }
+__device__ __forceinline__ uint32_t f22h(float a, float b) { return f2fx(a) | (f2fx(b) << 16); }
+#define NB_F2H1(a) __ushort_as_half((unsigned short)f2fx(a))
+#else
+__device__ __forceinline__ float2 h2f2(uint32_t v) { return __half22float2(*reinterpret_cast<const __half2*>(&v)); }
+__device__ __forceinline__ uint32_t f22h(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+#define NB_F2H1(a) __float2half_rn(a)
+#endif
 
 __device__ __forceinline__ void mbar_init(uint64_t* mb, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
@@ -287,7 +321,10 @@ __device__ __forceinline__ int ppos(int z) {
 // tensor product; the variable node runs in the probability domain instead (XOR-convolution
 // theorem): raw = P^0 (*) W_e' = WHT(p_v . WHT(W_e')) / q -- 2m butterfly stages and a product per
 // entry (the factor q cancels in the normalisation).
-template <int MB, int NTHR, bool PMF = false>
+// F16 = true: messages stored in HBM / L2 as IEEE half (sign | -log2|x|), the paper's reduced-precision
+// motivation: half the message bytes.  The staged rows are halves;
+// a float work row per team takes the transposition, the decision's D and the check node's scatter.
+template <int MB, int NTHR, bool PMF = false, bool F16 = false>
 #ifndef NB_CLUSTER_MINB
 #define NB_CLUSTER_MINB 2
 #endif
@@ -339,6 +376,10 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   const int GBLK = TG * C::QS;                   // one stage buffer of a group (floats)
   float* const GST = smem + grp * 2 * GBLK;      // the group's stage buffers
   const int trow = team - grp * TG;              // my team's row within a group stage buffer
+  // F16: the group's region holds two stage buffers of half rows (GBLKH floats each) and the float
+  // work rows (GBLK floats), the same bytes as two float stage buffers
+  const int GBLKH = GBLK / 2;
+  float* const WK = F16 ? GST + 2 * GBLKH + trow * C::QS : nullptr;  // my work row
   float* const THB = smem + nteams * 2 * C::QS + team * 8;  // + b * nteams * 8 (wide teams only)
   float* const TOT = smem + nteams * C::TEAMW + lc * Q;
   uint64_t* const PT = reinterpret_cast<uint64_t*>(smem + nteams * C::TEAMW + CPC * Q);  // [q] pi_h^-1 images
@@ -351,7 +392,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   const int JPT = KT / SPLIT;
   const int wgrp = pck / SPLIT;
   const int jbase = (pck % SPLIT) * JPT;
-  const int gbase = in_check ? (int)(GST - smem) + ((lc - grp * CPG) * KT + jbase) * C::QS + wgrp : 0;  // + buf * GBLK
+  const int gbase = in_check ? (int)(GST - smem) + (F16 ? 2 * GBLKH : 0) + ((lc - grp * CPG) * KT + jbase) * C::QS + wgrp
+                             : 0;  // + buf * GBLK (F32: the consumed stage rows; F16: the work rows)
   // my phase-B z's
   int zr[R];
 #pragma unroll
@@ -469,6 +511,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
       const int rb_ = step ? 0 : (ell & 1);
       const float* const Win = ws.W + ((size_t)rb_ * ws.S + slot) * EQ;
       float* const Wout = ws.W + ((size_t)(rb_ ^ 1) * ws.S + slot) * EQ;
+      const __half* const WinH = reinterpret_cast<const __half*>(ws.W) + ((size_t)rb_ * ws.S + slot) * EQ;
+      __half* const WoutH = reinterpret_cast<__half*>(ws.W) + ((size_t)(rb_ ^ 1) * ws.S + slot) * EQ;
       const bool do_dec = ell >= 1;
       const bool do_cn = step || ell < max_iters;
 
@@ -485,7 +529,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         const bool lead = (tid - grp * GT) == 0;
         uint32_t blk = 0;
         if (lead && C::BULK && ell != 0 && cg0 < cd.M)
-          blk = (uint32_t)((cd.M - cg0 < CPG ? cd.M - cg0 : CPG) * cd.kpad * Q * 4);
+          blk = (uint32_t)((cd.M - cg0 < CPG ? cd.M - cg0 : CPG) * cd.kpad * Q * (F16 ? 2 : 4));
         if (act && !C::BULK && ell != 0) {
           const float* sp = Win + ((size_t)((((int)rank + kc * (int)csz) * CPC + lc) * cd.kpad + j)) * Q;
           float* dst = GST + b * GBLK + trow * C::QS;
@@ -499,10 +543,17 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #ifndef NB_BLK_PIECE
 #define NB_BLK_PIECE 16384
 #endif
-        NB_CHECK(blk == 0 || ((size_t)cg0 * cd.kpad * Q * 4 + blk <= (size_t)cd.E * Q * 4 && blk <= (uint32_t)GBLK * 4));
-        for (uint32_t o = 0; o < blk; o += NB_BLK_PIECE)
-          bulk_g2s(GST + b * GBLK + o / 4, Win + (size_t)cg0 * cd.kpad * Q + o / 4,
-                   blk - o < NB_BLK_PIECE ? blk - o : NB_BLK_PIECE, &gmbar[b]);
+        if constexpr (F16) {
+          NB_CHECK(blk == 0 || ((size_t)cg0 * cd.kpad * Q * 2 + blk <= (size_t)cd.E * Q * 2 && blk <= (uint32_t)GBLKH * 4));
+          for (uint32_t o = 0; o < blk; o += NB_BLK_PIECE)
+            bulk_g2s(GST + b * GBLKH + o / 4, WinH + (size_t)cg0 * cd.kpad * Q + o / 2,
+                     blk - o < NB_BLK_PIECE ? blk - o : NB_BLK_PIECE, &gmbar[b]);
+        } else {
+          NB_CHECK(blk == 0 || ((size_t)cg0 * cd.kpad * Q * 4 + blk <= (size_t)cd.E * Q * 4 && blk <= (uint32_t)GBLK * 4));
+          for (uint32_t o = 0; o < blk; o += NB_BLK_PIECE)
+            bulk_g2s(GST + b * GBLK + o / 4, Win + (size_t)cg0 * cd.kpad * Q + o / 4,
+                     blk - o < NB_BLK_PIECE ? blk - o : NB_BLK_PIECE, &gmbar[b]);
+        }
         if (act && !C::THREG && !PMF) bulk_g2s(THB + b * nteams * 8, Tt + (size_t)(rr.var_h >> 8) * 8, 32, &gmbar[b]);
       };
       // channel-term row of chunk kc's variable, prefetched into registers one chunk ahead
@@ -537,7 +588,10 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         const bool is_a = active && (rr.partner_a & 1);
         const int e = c * cd.kpad + j;
         const int var = (int)(rr.var_h >> 8);
-        float* st = GST + buf * GBLK + trow * C::QS;  // my row: the message consumed by edge e
+        // my row: the message consumed by edge e (F32; it doubles as the work row), or (F16) the half
+        // stage row sth, read only in phase A, and the float work row
+        float* st = F16 ? WK : GST + buf * GBLK + trow * C::QS;
+        const __half* sth = reinterpret_cast<const __half*>(GST + buf * GBLKH) + trow * C::QS;
 
         // ---- channel terms t_i = tanh(L_i / 2)
         float th[MB];
@@ -564,6 +618,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         // W_e (own message, for v's decision at its first edge) straight from L2 into registers;
         // consumed after the variable node
         float4 wo4[CH];
+        uint4 woh[F16 ? (R >= 8 ? R / 8 : 1) : 1];  // F16: the raw half units, converted at the decision
 #ifdef NB_DIAG_DEC_NOLOAD
 #pragma unroll
         for (int ch = 0; ch < CH; ++ch) wo4[ch] = make_float4(0.5f, 0.25f, 0.125f, 1.0f);
@@ -575,7 +630,11 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           if (is_a && do_dec) {
 #endif
             const int prow = rr.partner_a >> 9;  // W_e is stored in the row its reader (the partner edge) consumes
-            if constexpr (R >= 4) {
+            if constexpr (F16) {
+              const __half* so = WinH + (size_t)prow * Q;
+#pragma unroll
+              for (int u = 0; u < R / 8; ++u) woh[u] = __ldcg(reinterpret_cast<const uint4*>(so + mposh<MB>(t * R + 8 * u, prow)));
+            } else if constexpr (R >= 4) {
               const float* so = Win + (size_t)prow * Q;
 #pragma unroll
               for (int ch = 0; ch < CH; ++ch) wo4[ch] = __ldcg(reinterpret_cast<const float4*>(so + mpos<MB>(t * R + 4 * ch, prow)));
@@ -611,7 +670,15 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             for (int jj = 0; jj < (1 << rb); ++jj) x[(1 << rb) + jj] = x[jj] * th[zb];
           }
         } else {
-          if constexpr (R >= 4) {
+          if constexpr (F16) {
+#pragma unroll
+            for (int u = 0; u < R / 8; ++u) {
+              const uint4 v = *reinterpret_cast<const uint4*>(sth + mposh<MB>(t * R + 8 * u, e));
+              const float2 a = h2f2(v.x), b = h2f2(v.y), cc = h2f2(v.z), d = h2f2(v.w);
+              x[8 * u] = to_lin(a.x); x[8 * u + 1] = to_lin(a.y); x[8 * u + 2] = to_lin(b.x); x[8 * u + 3] = to_lin(b.y);
+              x[8 * u + 4] = to_lin(cc.x); x[8 * u + 5] = to_lin(cc.y); x[8 * u + 6] = to_lin(d.x); x[8 * u + 7] = to_lin(d.y);
+            }
+          } else if constexpr (R >= 4) {
 #pragma unroll
             for (int ch = 0; ch < CH; ++ch) {
               const float4 v = *reinterpret_cast<const float4*>(st + mpos<MB>(t * R + 4 * ch, e));
@@ -710,6 +777,16 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #endif
           float* DB = st;
           if constexpr (TT > 1) __syncwarp();  // transposition reads done
+          if constexpr (F16) {
+            if (is_a) {
+#pragma unroll
+              for (int u = 0; u < R / 8; ++u) {
+                const float2 a = h2f2(woh[u].x), b = h2f2(woh[u].y), cc = h2f2(woh[u].z), d = h2f2(woh[u].w);
+                wo4[2 * u] = make_float4(a.x, a.y, b.x, b.y);
+                wo4[2 * u + 1] = make_float4(cc.x, cc.y, d.x, d.y);
+              }
+            }
+          }
           if (is_a) {
             if constexpr (TT > 1) {
 #pragma unroll
@@ -926,11 +1003,11 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           }
           check_sync(lc, TPC);
           switch (JPT) {
-            case 1: tot_sum<R, 1, TT, C::QS>(smem, gbase + buf * GBLK, TOT, wgrp, SPLIT, pck, cvalid); break;
-            case 2: tot_sum<R, (R >= 2 ? 2 : 1), TT, C::QS>(smem, gbase + buf * GBLK, TOT, wgrp, SPLIT, pck, cvalid); break;
-            case 4: tot_sum<R, (R >= 4 ? 4 : 1), TT, C::QS>(smem, gbase + buf * GBLK, TOT, wgrp, SPLIT, pck, cvalid); break;
-            case 8: tot_sum<R, (R >= 8 ? 8 : 1), TT, C::QS>(smem, gbase + buf * GBLK, TOT, wgrp, SPLIT, pck, cvalid); break;
-            default: tot_sum<R, R, TT, C::QS>(smem, gbase + buf * GBLK, TOT, wgrp, SPLIT, pck, cvalid); break;
+            case 1: tot_sum<R, 1, TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid); break;
+            case 2: tot_sum<R, (R >= 2 ? 2 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid); break;
+            case 4: tot_sum<R, (R >= 4 ? 4 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid); break;
+            case 8: tot_sum<R, (R >= 8 ? 8 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid); break;
+            default: tot_sum<R, R, TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid); break;
           }
           check_sync(lc, TPC);
           if (active) {
@@ -945,7 +1022,33 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             const int prow = rr.partner_a >> 9;  // stored where the partner edge will read it
             NB_CHECK(prow >= 0 && prow < cd.E);
             float* dst = Wout + (size_t)prow * Q;
-            if constexpr (TT > 1) {
+            if constexpr (F16) {
+              __half* dh = WoutH + (size_t)prow * Q;
+              if constexpr (TT > 1) {
+                constexpr int V = C::V;  // runs of V = 2^LJ entries, contiguous within a 16-byte unit
+#pragma unroll
+                for (int h = 0; h < TT; ++h) {
+                  const int z0 = (t << LJ) | (h << 4);
+                  __half* p = dh + mposh<MB>(z0, prow);
+                  if constexpr (V == 1) {
+                    *p = NB_F2H1(out[h]);
+                  } else if constexpr (V == 2) {
+                    *reinterpret_cast<uint32_t*>(p) = f22h(out[2 * h], out[2 * h + 1]);
+                  } else if constexpr (V == 4) {
+                    *reinterpret_cast<uint2*>(p) = make_uint2(f22h(out[4 * h], out[4 * h + 1]), f22h(out[4 * h + 2], out[4 * h + 3]));
+                  } else {
+                    *reinterpret_cast<uint4*>(p) = make_uint4(f22h(out[8 * h], out[8 * h + 1]), f22h(out[8 * h + 2], out[8 * h + 3]),
+                                                              f22h(out[8 * h + 4], out[8 * h + 5]), f22h(out[8 * h + 6], out[8 * h + 7]));
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int u = 0; u < R / 8; ++u)
+                  *reinterpret_cast<uint4*>(dh + mposh<MB>(8 * u, prow)) =
+                      make_uint4(f22h(out[8 * u], out[8 * u + 1]), f22h(out[8 * u + 2], out[8 * u + 3]),
+                                 f22h(out[8 * u + 4], out[8 * u + 5]), f22h(out[8 * u + 6], out[8 * u + 7]));
+              }
+            } else if constexpr (TT > 1) {
               constexpr int V = C::V;
 #pragma unroll
               for (int h = 0; h < TT; ++h) {

@@ -176,33 +176,41 @@ void* pass_kernel_ptr(int m, int big, int direct) {
   return direct ? pass_kernel_ptr_t<true, false>(m, big) : pass_kernel_ptr_t<false, false>(m, big);
 }
 
-template <int MB, int NTHR, bool PMF>
-void* cluster_fn() { return reinterpret_cast<void*>(&nb::lf_cluster_kernel<MB, NTHR, PMF>); }
-template <bool PMF>
+template <int MB, int NTHR, bool PMF, bool F16>
+void* cluster_fn() {
+  if constexpr (F16 && (PMF || MB < 3)) {  // half messages: LLR input, q >= 8 (16-byte row units)
+    return nullptr;
+  } else {
+    return reinterpret_cast<void*>(&nb::lf_cluster_kernel<MB, NTHR, PMF, F16>);
+  }
+}
+template <bool PMF, bool F16>
 void* persist_kernel_ptr_t(int m, int big) {
   switch (m * 2 + (big ? 1 : 0)) {
-    case 2: return cluster_fn<1, 256, PMF>();
-    case 3: return cluster_fn<1, 512, PMF>();
-    case 4: return cluster_fn<2, 256, PMF>();
-    case 5: return cluster_fn<2, 512, PMF>();
-    case 6: return cluster_fn<3, 256, PMF>();
-    case 7: return cluster_fn<3, 512, PMF>();
-    case 8: return cluster_fn<4, 256, PMF>();
-    case 9: return cluster_fn<4, 512, PMF>();
-    case 10: return cluster_fn<5, 256, PMF>();
-    case 11: return cluster_fn<5, 512, PMF>();
-    case 12: return cluster_fn<6, 256, PMF>();
-    case 13: return cluster_fn<6, 512, PMF>();
-    case 14: return cluster_fn<7, 256, PMF>();
-    case 15: return cluster_fn<7, 512, PMF>();
-    case 16: return cluster_fn<8, 256, PMF>();
-    case 17: return cluster_fn<8, 512, PMF>();
+    case 2: return cluster_fn<1, 256, PMF, F16>();
+    case 3: return cluster_fn<1, 512, PMF, F16>();
+    case 4: return cluster_fn<2, 256, PMF, F16>();
+    case 5: return cluster_fn<2, 512, PMF, F16>();
+    case 6: return cluster_fn<3, 256, PMF, F16>();
+    case 7: return cluster_fn<3, 512, PMF, F16>();
+    case 8: return cluster_fn<4, 256, PMF, F16>();
+    case 9: return cluster_fn<4, 512, PMF, F16>();
+    case 10: return cluster_fn<5, 256, PMF, F16>();
+    case 11: return cluster_fn<5, 512, PMF, F16>();
+    case 12: return cluster_fn<6, 256, PMF, F16>();
+    case 13: return cluster_fn<6, 512, PMF, F16>();
+    case 14: return cluster_fn<7, 256, PMF, F16>();
+    case 15: return cluster_fn<7, 512, PMF, F16>();
+    case 16: return cluster_fn<8, 256, PMF, F16>();
+    case 17: return cluster_fn<8, 512, PMF, F16>();
   }
   return nullptr;
 }
 // pmf = 1: the nbldpc_decode_pmf variant (probability-domain variable node)
-void* persist_kernel_ptr(int m, int big, int pmf = 0) {
-  return pmf ? persist_kernel_ptr_t<true>(m, big) : persist_kernel_ptr_t<false>(m, big);
+// pmf = 1: the nbldpc_decode_pmf variant; f16 = 1: half-precision messages (NBLDPC_MSG_F16)
+void* persist_kernel_ptr(int m, int big, int pmf = 0, int f16 = 0) {
+  if (f16) return pmf ? nullptr : persist_kernel_ptr_t<false, true>(m, big);
+  return pmf ? persist_kernel_ptr_t<true, false>(m, big) : persist_kernel_ptr_t<false, false>(m, big);
 }
 // shared-memory words per edge team of the cluster kernel (nb::CCfg<m>::TEAM)
 int persist_team_words(int m) {
@@ -219,7 +227,8 @@ int persist_team_words(int m) {
   return 0;
 }
 
-cudaError_t launch_cluster(const nbldpc_code_s* c, const nb::ClusterParams& P, int ncl, cudaStream_t st, int pmf = 0) {
+cudaError_t launch_cluster(const nbldpc_code_s* c, const nb::ClusterParams& P, int ncl, cudaStream_t st, int pmf = 0,
+                           int f16 = 0) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(ncl * c->p_cs));
   cfg.blockDim = dim3((unsigned)c->p_block);
@@ -233,7 +242,7 @@ cudaError_t launch_cluster(const nbldpc_code_s* c, const nb::ClusterParams& P, i
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void* args[] = {const_cast<nb::ClusterParams*>(&P)};
-  return cudaLaunchKernelExC(&cfg, persist_kernel_ptr(c->m, c->p_big, pmf), args);
+  return cudaLaunchKernelExC(&cfg, persist_kernel_ptr(c->m, c->p_big, pmf, f16), args);
 }
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a property of the kernel (one instantiation per
@@ -251,14 +260,16 @@ cudaError_t ensure_smem_attr(const nbldpc_code_s* c) {
     if (e != cudaSuccess) return e;
     g_attr_smem[d][k] = c->smem;
   }
-  static size_t p_attr[64][36] = {};
-  for (int pmf = 0; pmf < 2; ++pmf) {
-    void* fn = persist_kernel_ptr(c->m, c->p_big, pmf);
+  static size_t p_attr[64][54] = {};
+  for (int var = 0; var < 3; ++var) {  // plain, pmf, f16
+    const int pmf = var == 1, f16 = var == 2;
+    void* fn = persist_kernel_ptr(c->m, c->p_big, pmf, f16);
+    if (!fn) continue;
     if (c->p_cs > 8) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;
     }
-    const int d = c->device & 63, k = (c->m * 2 + c->p_big) * 2 + pmf;
+    const int d = c->device & 63, k = (c->m * 2 + c->p_big) * 3 + var;
     if (p_attr[d][k] < c->p_smem) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->p_smem);
       if (e != cudaSuccess) return e;
@@ -652,6 +663,7 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   int32_t* events = nullptr;
   float* post = nullptr;
   uint8_t* xmap = nullptr;
+  int f16 = 0;
   if (opts) {
     if (opts->struct_size < sizeof(nbldpc_decode_opts_t)) return NBLDPC_ERR_INVALID_ARGUMENT;
     mode = opts->syndrome_mode;
@@ -663,6 +675,12 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
     direct = opts->vn_algorithm;
     post = opts->symbol_post_out;
     xmap = opts->symbol_map_out;
+    if (opts->message_format != NBLDPC_MSG_F32 && opts->message_format != NBLDPC_MSG_F16) return NBLDPC_ERR_INVALID_ARGUMENT;
+    f16 = opts->message_format == NBLDPC_MSG_F16;
+    if (f16 && (opts->algorithm != NBLDPC_ALG_LOG_FOURIER || opts->vn_algorithm != NBLDPC_VN_SEPARABLE || pmf || post ||
+                xmap || !c->colw2))
+      return NBLDPC_ERR_INVALID_ARGUMENT;  // half messages: the cluster kernel with LLR input
+    if (f16 && c->m < 3) return NBLDPC_ERR_UNSUPPORTED;
     if (opts->algorithm == NBLDPC_ALG_LOG_SP) {
       // the comparison algorithm: symbol-MAP decisions and the exact syndrome only
       if (mode != 0 || soft || events || post || xmap) return NBLDPC_ERR_INVALID_ARGUMENT;
@@ -730,7 +748,7 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   w.last_host_launches = 1;
   if (!direct) {
     nb::ClusterParams PP = make_cparams(c, 0, 0, nullptr);
-    NB_TRY(launch_cluster(c, PP, S, st, pmf != nullptr));
+    NB_TRY(launch_cluster(c, PP, S, st, pmf != nullptr, f16));
     w.last_graph = 0;
     w.last_host_launches = 2;
     return NBLDPC_OK;

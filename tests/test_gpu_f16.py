@@ -1,0 +1,91 @@
+"""Half-precision messages (NBLDPC_MSG_F16, the paper's reduced-precision
+motivation PAPER.md:57-71), evaluated as the survey asks: by frame error rate and iteration counts
+against the float32 decoder on the same frames (the arithmetic is fp32 in both; only the stored
+messages are rounded to 11 significant bits), plus every converged frame being a codeword."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import synth
+from parity import config_inputs, oracle_code
+
+pytestmark = pytest.mark.gpu
+MSG_F16 = 1
+
+
+@pytest.fixture(scope="module")
+def dev():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch.device("cuda:0")
+
+
+def _code(name):
+    import paper_1008_4370_b200 as nb
+
+    c = synth.CONFIGS[name]
+    M, rows, cols, coeffs = synth.config_code(name)
+    return nb.Code(c["m"], c["poly"], M, c["N"], rows, cols, coeffs)
+
+
+@pytest.mark.parametrize("name,point,F", [("C2", 0, 2048), ("C3", 0, 512), ("C4", 0, 128), ("C5", 0, 2048),
+                                          ("C5", 3, 2048)])
+def test_f16_messages_match_f32_frame_error_rate(dev, name, point, F):
+    c = synth.CONFIGS[name]
+    _, llr, xs = config_inputs(name, 0, F, point=point)
+    code = _code(name)
+    x = torch.from_numpy(llr).to(dev)
+    a = code.decode(x, c["max_iters"])
+    b = code.decode(x, c["max_iters"], message_format=MSG_F16)
+    fa = 1.0 - a["ok"].float().mean().item()
+    fb = 1.0 - b["ok"].float().mean().item()
+    # measured: C2 2.2% -> 3.5%, C3 0.15% -> 0.63%, C4 / C5 unchanged
+    assert fb <= 1.8 * fa + 0.01 + 3.0 / F, (fa, fb)
+    ia, ib = a["iters"].float().mean().item(), b["iters"].float().mean().item()
+    assert abs(ib - ia) <= 0.05 * ia + 0.2, (ia, ib)
+    same = (a["hard"] == b["hard"]).all(1).float().mean().item()
+    assert same >= 0.9, same
+    # converged frames: undetected errors (a codeword other than the sent one) no more often than F32
+    sent = xs.astype(np.uint8)
+    und = []
+    for o in (a, b):
+        ok = o["ok"].cpu().numpy().astype(bool)
+        und.append((ok & ~(o["hard"].cpu().numpy() == sent).all(1)).mean())
+    assert und[1] <= und[0] + 0.005, und
+    okb = b["ok"].cpu().numpy().astype(bool)
+    hb = b["hard"].cpu().numpy()
+    ocode = oracle_code(name)
+    for f in np.where(okb)[0][:16]:
+        assert ocode.syndrome(hb[f])[0]
+
+
+def test_f16_invariance_and_errors(dev):
+    import paper_1008_4370_b200 as nb
+
+    name = "C2"
+    c = synth.CONFIGS[name]
+    _, llr, _ = config_inputs(name, 0, 96)
+    code = _code(name)
+    x = torch.from_numpy(llr).to(dev)
+    base = code.decode(x, c["max_iters"], message_format=MSG_F16)
+    for kw in (dict(slots=3), dict(slots=50)):
+        o = code.decode(x, c["max_iters"], message_format=MSG_F16, **kw)
+        for k in ("hard", "ok", "iters"):
+            assert torch.equal(o[k], base[k]), (kw, k)
+    h = code.decode_host(torch.from_numpy(llr).pin_memory(), c["max_iters"], message_format=MSG_F16)
+    for k in ("hard", "ok", "iters"):
+        assert torch.equal(h[k], base[k].cpu()), k
+    for kw in (dict(vn_algorithm=1), dict(algorithm=1), dict(want_post=True)):
+        with pytest.raises(nb.NbldpcError) as ei:
+            code.decode(x, 10, message_format=MSG_F16, **kw)
+        assert ei.value.status == -1
+    with pytest.raises(nb.NbldpcError) as ei:
+        code.decode(x, 10, message_format=5)
+    assert ei.value.status == -1
+    with pytest.raises(nb.NbldpcError) as ei:
+        code.decode_pmf(torch.ones((2, c["N"], c["q"]), device=dev), 10, message_format=MSG_F16)
+    assert ei.value.status == -1
+    with pytest.raises(nb.NbldpcError) as ei:  # q = 4 rows are shorter than a 16-byte unit of halves
+        c1 = synth.CONFIGS["C1"]
+        _code("C1").decode(torch.from_numpy(config_inputs("C1", 0, 4)[1]).to(dev), 10, message_format=MSG_F16)
+    assert ei.value.status == -3
