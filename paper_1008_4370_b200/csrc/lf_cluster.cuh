@@ -324,7 +324,9 @@ __device__ __forceinline__ int ppos(int z) {
 // F16 = true: messages stored in HBM / L2 as IEEE half (sign | -log2|x|), the paper's reduced-precision
 // motivation: half the message bytes.  The staged rows are halves;
 // a float work row per team takes the transposition, the decision's D and the check node's scatter.
-template <int MB, int NTHR, bool PMF = false, bool F16 = false>
+// KP > 0: the code's edge-slot stride kpad, known at compile time with full CTAs (NTHR threads,
+// NTHR / (KP TT) checks each), so that the chunk geometry constant-folds; 0: taken from P.
+template <int MB, int NTHR, bool PMF = false, bool F16 = false, int KP = 0>
 #ifndef NB_CLUSTER_MINB
 #define NB_CLUSTER_MINB 2
 #endif
@@ -338,14 +340,14 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   const CodeDev& cd = P.code;
   const WorkDev& ws = P.ws;
   const int tid = threadIdx.x;
-  const int nthr = blockDim.x;
+  const int nthr = KP ? NTHR : (int)blockDim.x;
   const int lane = tid & 31;
   const uint32_t rank = cluster_rank();
   const uint32_t csz = cluster_nrank();
   const int clid = (int)cluster_id();
   const int ncl = (int)cluster_count();
-  const int TPC = P.tpc;
-  const int CPC = P.checks_per_cta;
+  const int TPC = KP ? KP * TT : P.tpc;
+  const int CPC = KP ? NTHR / (KP * TT) : P.checks_per_cta;
   const int KT = TPC / TT;                       // teams per check (incl. padding teams)
   const int nch = ((int)P.chunks - (int)rank + (int)csz - 1) / (int)csz;  // my chunks: rank + k*csz
   // independent groups of GT = max(32, TPC) threads (a warp, or one check): each runs its own stage

@@ -80,6 +80,7 @@ struct nbldpc_code_s {
   // launch geometry of the cluster kernel (NBLDPC_VN_SEPARABLE): TPC a power of two, clusters of
   // p_cs CTAs per frame, p_ncl clusters resident
   int p_tpc = 1, p_cpc = 1, p_groups = 1, p_block = 32, p_big = 0, p_cs = 1, p_ncl = 1, p_recs = 0;
+  int p_kp = 0;  // > 0: the plain LLR launch uses the compile-time-geometry instantiation (KP = kpad)
   size_t p_smem = 0;
 };
 
@@ -207,6 +208,40 @@ void* persist_kernel_ptr_t(int m, int big) {
   return nullptr;
 }
 // pmf = 1: the nbldpc_decode_pmf variant (probability-domain variable node)
+// the plain LLR kernel with the chunk geometry at compile time (KP = kpad, full CTAs)
+template <int MB, int KP>
+void* cluster_kp_fn() {
+  constexpr int TT = MB <= 4 ? 1 : (1 << MB) / 16;
+  if constexpr (KP * TT > 512) {
+    return nullptr;
+  } else {
+    return reinterpret_cast<void*>(&nb::lf_cluster_kernel<MB, (KP * TT > 256 ? 512 : 256), false, false, KP>);
+  }
+}
+template <int MB>
+void* cluster_kp_m(int kpad) {
+  switch (kpad) {
+    case 4: return cluster_kp_fn<MB, 4>();
+    case 8: return cluster_kp_fn<MB, 8>();
+    case 16: return cluster_kp_fn<MB, 16>();
+    case 32: return cluster_kp_fn<MB, 32>();
+  }
+  return nullptr;
+}
+void* persist_kp_ptr(int m, int kpad) {
+  switch (m) {
+    case 1: return cluster_kp_m<1>(kpad);
+    case 2: return cluster_kp_m<2>(kpad);
+    case 3: return cluster_kp_m<3>(kpad);
+    case 4: return cluster_kp_m<4>(kpad);
+    case 5: return cluster_kp_m<5>(kpad);
+    case 6: return cluster_kp_m<6>(kpad);
+    case 7: return cluster_kp_m<7>(kpad);
+    case 8: return cluster_kp_m<8>(kpad);
+  }
+  return nullptr;
+}
+
 // pmf = 1: the nbldpc_decode_pmf variant; f16 = 1: half-precision messages (NBLDPC_MSG_F16)
 void* persist_kernel_ptr(int m, int big, int pmf = 0, int f16 = 0) {
   if (f16) return pmf ? nullptr : persist_kernel_ptr_t<false, true>(m, big);
@@ -242,7 +277,8 @@ cudaError_t launch_cluster(const nbldpc_code_s* c, const nb::ClusterParams& P, i
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void* args[] = {const_cast<nb::ClusterParams*>(&P)};
-  return cudaLaunchKernelExC(&cfg, persist_kernel_ptr(c->m, c->p_big, pmf, f16), args);
+  void* fn = (c->p_kp && !pmf && !f16) ? persist_kp_ptr(c->m, c->p_kp) : persist_kernel_ptr(c->m, c->p_big, pmf, f16);
+  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a property of the kernel (one instantiation per
@@ -260,16 +296,19 @@ cudaError_t ensure_smem_attr(const nbldpc_code_s* c) {
     if (e != cudaSuccess) return e;
     g_attr_smem[d][k] = c->smem;
   }
-  static size_t p_attr[64][54] = {};
-  for (int var = 0; var < 3; ++var) {  // plain, pmf, f16
+  static size_t p_attr[64][18 * 4 + 32] = {};
+  for (int var = 0; var < 4; ++var) {  // plain, pmf, f16, compile-time geometry
     const int pmf = var == 1, f16 = var == 2;
-    void* fn = persist_kernel_ptr(c->m, c->p_big, pmf, f16);
+    void* fn = var == 3 ? (c->p_kp ? persist_kp_ptr(c->m, c->p_kp) : nullptr) : persist_kernel_ptr(c->m, c->p_big, pmf, f16);
     if (!fn) continue;
     if (c->p_cs > 8) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;
     }
-    const int d = c->device & 63, k = (c->m * 2 + c->p_big) * 3 + var;
+    // one cache slot per kernel: (m, big, variant), or (m, kpad) for the compile-time-geometry one
+    int k = (c->m * 2 + c->p_big) * 4 + var;
+    if (var == 3) k = 18 * 4 + (c->m - 1) * 4 + (c->p_kp == 4 ? 0 : c->p_kp == 8 ? 1 : c->p_kp == 16 ? 2 : 3);
+    const int d = c->device & 63;
     if (p_attr[d][k] < c->p_smem) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->p_smem);
       if (e != cudaSuccess) return e;
@@ -1008,6 +1047,10 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
       if (v >= 1 && v <= 16 && c->p_groups % v == 0) cs = v;
     }
     c->p_cs = cs;
+    // full CTAs (NTHR threads of checks of kpad teams): the geometry is a compile-time constant
+    if (c->p_block == (tpc > 256 ? 512 : 256) && c->p_cpc * tpc == c->p_block && !getenv("NBLDPC_NO_KP") &&
+        persist_kp_ptr(m, kpad) != nullptr)
+      c->p_kp = kpad;
     const int kt = tpc / tt;
     c->p_recs = ((c->p_groups + cs - 1) / cs) * c->p_cpc * kt;
     c->p_smem = ((size_t)(c->p_block / tt) * persist_team_words(m) + (size_t)c->p_cpc * q) * sizeof(float) +
@@ -1031,7 +1074,8 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int ncl = 0;
-    if (cudaError_t e = cudaOccupancyMaxActiveClusters(&ncl, persist_kernel_ptr(m, c->p_big), &cfg)) return bail(e);
+    void* fn = c->p_kp ? persist_kp_ptr(m, c->p_kp) : persist_kernel_ptr(m, c->p_big);
+    if (cudaError_t e = cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg)) return bail(e);
     if (ncl < 1) {
       nbldpc_destroy(c);
       return NBLDPC_ERR_UNSUPPORTED;
