@@ -346,6 +346,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   const uint32_t csz = cluster_nrank();
   const int clid = (int)cluster_id();
   const int ncl = (int)cluster_count();
+  const int KPAD = KP ? KP : cd.kpad;  // edge-slot stride per check
   const int TPC = KP ? KP * TT : P.tpc;
   const int CPC = KP ? NTHR / (KP * TT) : P.checks_per_cta;
   const int KT = TPC / TT;                       // teams per check (incl. padding teams)
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
     const int c = ((int)rank + kc * (int)csz) * CPC + l;
     EdgeRec rr{-1, 0};
     if (c < cd.M && jj < cd.k_max) {
-      const EdgeDev* ep = cd.edges + (size_t)c * cd.kpad + jj;
+      const EdgeDev* ep = cd.edges + (size_t)c * KPAD + jj;
       if (ep->var >= 0) {
         rr.partner_a = (ep->partner << 9) | ((int)cd.edges[ep->partner].h << 1) | (ep->is_a ? 1 : 0);
         rr.var_h = ((uint32_t)ep->var << 8) | ep->h;
@@ -531,14 +532,27 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         const bool lead = (tid - grp * GT) == 0;
         uint32_t blk = 0;
         if (lead && C::BULK && ell != 0 && cg0 < cd.M)
-          blk = (uint32_t)((cd.M - cg0 < CPG ? cd.M - cg0 : CPG) * cd.kpad * Q * (F16 ? 2 : 4));
+          blk = (uint32_t)((cd.M - cg0 < CPG ? cd.M - cg0 : CPG) * KPAD * Q * (F16 ? 2 : 4));
         if (act && !C::BULK && ell != 0) {
-          const float* sp = Win + ((size_t)((((int)rank + kc * (int)csz) * CPC + lc) * cd.kpad + j)) * Q;
+          const float* sp = Win + ((size_t)((((int)rank + kc * (int)csz) * CPC + lc) * KPAD + j)) * Q;
           float* dst = GST + b * GBLK + trow * C::QS;
 #pragma unroll
           for (int r = 0; r < Q; ++r) dst[r] = __ldcg(sp + r);
         }
+#ifdef NB_TT_BULK
         if (act && !C::THREG && !PMF) tx += 32;
+#else
+        // the team's channel-term row by two LDGSTS tracked by the same mbarrier (the pending count
+        // is raised before this thread's own arrival, so the phase waits for them): a bulk copy from a
+        // divergent thread would cost a uniform-register waterfall loop over the warp's team leaders
+        if (act && !C::THREG && !PMF) {
+          const float* srcT = Tt + (size_t)(rr.var_h >> 8) * 8;
+          float* dstT = THB + b * nteams * 8;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dstT)), "l"(srcT) : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dstT + 4)), "l"(srcT + 4) : "memory");
+          asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(&gmbar[b])) : "memory");
+        }
+#endif
         tx += blk;
         mbar_arrive_tx(&gmbar[b], tx);
         // the block in pieces of <= NB_BLK_PIECE bytes (several TMA transfers in flight)
@@ -546,17 +560,19 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #define NB_BLK_PIECE 16384
 #endif
         if constexpr (F16) {
-          NB_CHECK(blk == 0 || ((size_t)cg0 * cd.kpad * Q * 2 + blk <= (size_t)cd.E * Q * 2 && blk <= (uint32_t)GBLKH * 4));
+          NB_CHECK(blk == 0 || ((size_t)cg0 * KPAD * Q * 2 + blk <= (size_t)cd.E * Q * 2 && blk <= (uint32_t)GBLKH * 4));
           for (uint32_t o = 0; o < blk; o += NB_BLK_PIECE)
-            bulk_g2s(GST + b * GBLKH + o / 4, WinH + (size_t)cg0 * cd.kpad * Q + o / 2,
+            bulk_g2s(GST + b * GBLKH + o / 4, WinH + (size_t)cg0 * KPAD * Q + o / 2,
                      blk - o < NB_BLK_PIECE ? blk - o : NB_BLK_PIECE, &gmbar[b]);
         } else {
-          NB_CHECK(blk == 0 || ((size_t)cg0 * cd.kpad * Q * 4 + blk <= (size_t)cd.E * Q * 4 && blk <= (uint32_t)GBLK * 4));
+          NB_CHECK(blk == 0 || ((size_t)cg0 * KPAD * Q * 4 + blk <= (size_t)cd.E * Q * 4 && blk <= (uint32_t)GBLK * 4));
           for (uint32_t o = 0; o < blk; o += NB_BLK_PIECE)
-            bulk_g2s(GST + b * GBLK + o / 4, Win + (size_t)cg0 * cd.kpad * Q + o / 4,
+            bulk_g2s(GST + b * GBLK + o / 4, Win + (size_t)cg0 * KPAD * Q + o / 4,
                      blk - o < NB_BLK_PIECE ? blk - o : NB_BLK_PIECE, &gmbar[b]);
         }
+#ifdef NB_TT_BULK
         if (act && !C::THREG && !PMF) bulk_g2s(THB + b * nteams * 8, Tt + (size_t)(rr.var_h >> 8) * 8, 32, &gmbar[b]);
+#endif
       };
       // channel-term row of chunk kc's variable, prefetched into registers one chunk ahead
       auto th_load = [&](int kc, float4 (&dst)[2]) {
@@ -588,7 +604,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         if (in_check) rr = recs[(kc * CPC + lc) * KT + j];
         const bool active = cvalid && rr.partner_a >= 0;
         const bool is_a = active && (rr.partner_a & 1);
-        const int e = c * cd.kpad + j;
+        const int e = c * KPAD + j;
         const int var = (int)(rr.var_h >> 8);
         // my row: the message consumed by edge e (F32; it doubles as the work row), or (F16) the half
         // stage row sth, read only in phase A, and the float work row
@@ -1093,7 +1109,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
       if (ell >= 1) {
         // my checks' syndromes s_c = XOR of the contribution bytes on their kpad edge slots
         int bad = 0;
-        const int kp = cd.kpad;
+        const int kp = KPAD;
         for (int i = tid; i < nch * CPC; i += nthr) {
           const int kc = i / CPC, l = i - kc * CPC;
           const int c = ((int)rank + kc * (int)csz) * CPC + l;
