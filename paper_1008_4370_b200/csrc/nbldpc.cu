@@ -812,6 +812,55 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   return NBLDPC_OK;
 }
 
+// Which edge of a degree-2 variable evaluates its tentative decision ("is_a") is free: both give
+// M_v = P^0 (*) W_a (*) W_b.  The kernels run an edge team per 32 / TT consecutive edge slots in a
+// warp, and a warp with no deciding edge skips the decision (warp-uniform branch) while a warp with
+// any pays it in full.  So choose the deciding warps as a small vertex cover of the graph whose nodes
+// are warps and whose edges are variables (greedy: repeatedly the warp covering most uncovered
+// variables), and let each variable decide in a covering warp.
+void assign_decision_owners(std::vector<EdgeDev>& edges, int E, int tt) {
+  const int per = 32 / tt;  // edge slots per warp
+  const int nw = (E + per - 1) / per;
+  std::vector<int> deg(nw, 0);
+  for (int e = 0; e < E; ++e)
+    if (edges[e].var >= 0 && edges[e].is_a) {
+      deg[e / per]++;
+      deg[edges[e].partner / per]++;
+    }
+  std::vector<char> covered_var(E, 0), in_cover(nw, 0);  // indexed by the variable's first edge slot
+  std::vector<std::vector<int>> bucket(2 * per + 1);
+  for (int w = 0; w < nw; ++w) bucket[std::min(deg[w], 2 * per)].push_back(w);
+  int top = 2 * per;
+  while (true) {
+    while (top > 0 && bucket[top].empty()) --top;
+    if (top == 0) break;
+    const int w = bucket[top].back();
+    bucket[top].pop_back();
+    if (in_cover[w] || std::min(deg[w], 2 * per) != top) continue;  // stale entry
+    in_cover[w] = 1;
+    for (int e = w * per; e < std::min(E, (w + 1) * per); ++e) {
+      if (edges[e].var < 0) continue;
+      const int a = edges[e].is_a ? e : edges[e].partner;  // the variable's key slot
+      if (covered_var[a]) continue;
+      covered_var[a] = 1;
+      const int o = (e == a ? edges[a].partner : a) / per;  // the other warp loses this variable
+      if (!in_cover[o] && deg[o] > 0) {
+        deg[o]--;
+        bucket[std::min(deg[o], 2 * per)].push_back(o);
+      }
+    }
+    deg[w] = 0;
+  }
+  for (int e = 0; e < E; ++e) {
+    if (edges[e].var < 0 || !edges[e].is_a) continue;
+    const int b = edges[e].partner;
+    if (!in_cover[e / per] && in_cover[b / per]) {  // hand the decision to the covering warp
+      edges[e].is_a = 0;
+      edges[b].is_a = 1;
+    }
+  }
+}
+
 bool gf_tables(int m, uint32_t poly, std::vector<int>& ex, std::vector<int>& lg) {
   const int q = 1 << m;
   if ((poly >> m) != 1u) return false;
@@ -939,6 +988,7 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
       ea.plogh = ed.logh;
     }
   }
+  if (colw2 && !getenv("NBLDPC_FIRST_EDGE_DECIDES")) assign_decision_owners(edges, E, tt);
   std::vector<uint8_t> gexp(2 * (q - 1) + 1), glog(q, 0);
   for (size_t i = 0; i < gexp.size(); ++i) gexp[i] = (uint8_t)ex[i];
   for (int x = 1; x < q; ++x) glog[x] = (uint8_t)lg[x];
