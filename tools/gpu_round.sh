@@ -1,9 +1,10 @@
-# tests (all), bench (default), launch list + one full ncu capture of the bench's kernel
+# round evidence: tests (all), smoke, bench (default), launch list + one full ncu capture of the bench's kernel
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
-timeout -s KILL 1500 python -m pytest tests -m gpu -q -rf > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -8 gpurun_out/pytest_gpu.log
+timeout -s KILL 1500 python -m pytest tests -m gpu -q -rf > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -3 gpurun_out/pytest_gpu.log
 timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?"; cat gpurun_out/smoke.log
-timeout -s KILL 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench exit $?"; cat gpurun_out/bench.log
+timeout -s KILL 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench exit $?"; tail -1 gpurun_out/bench.log | cut -c1-400
 B="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
 timeout -s KILL 300 $B > gpurun_out/plain.log 2>&1 && \
-timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches exit $?"
-timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:lf_cluster -s 3 -c 1 -o gpurun_out/bench_full $B > gpurun_out/ncu_full.log 2>&1; echo "ncu full exit $?"
+timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launch.log 2>&1 && \
+timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:lf_cluster -s 3 -c 1 -o gpurun_out/bench_full $B > gpurun_out/ncu_full.log 2>&1
+echo "ncu exit $?"
