@@ -318,3 +318,32 @@ def test_irregular_check_degrees_and_cycle_codes(dev, vn):
         same = ((out["hard"].cpu().numpy() == ref["hard"]).all(1) & (out["ok"].cpu().numpy() == ref["ok"])
                 & (out["iters"].cpu().numpy() == ref["iters"]))
         assert same.mean() >= 0.95, (m, degs[:4], same.mean())
+
+
+def test_largest_check_team_and_empty_batches(dev):
+    """The largest geometry (GF(256), k = 32: 512 threads per check, the 512-thread kernel variant)
+    against the oracle, both VN algorithms; an empty batch is rejected as documented (frames >= 1)."""
+    import paper_1008_4370_b200 as nb
+
+    m, N, k = 8, 128, 32
+    M, rows, cols, coeffs = synth.make_regular_code(N, k, m, 777)
+    code = nb.Code(m, 0x11D, M, N, rows, cols, coeffs)
+    ocode = oracle.Code(oracle.Field(m, 0x11D), M, N, rows, cols, coeffs)
+    llr = synth.awgn_llr(N * m, 0, 6, synth.sigma2_for(4.5, 1 - 2 / k), 778)
+    ref = ocode.lf_decode_batch(llr, 15)
+    twin = ocode.lf_decode_batch(llr, 15, f32=True)
+    stable = (ref["hard"] == twin["hard"]).all(1) & (ref["iters"] == twin["iters"])
+    assert stable.sum() >= 4
+    for vn in (0, 1):
+        out = code.decode(torch.from_numpy(llr).to(dev), 15, vn_algorithm=vn)
+        hard, it = out["hard"].cpu().numpy(), out["iters"].cpu().numpy()
+        for f in np.where(stable)[0]:
+            assert np.array_equal(hard[f], ref["hard"][f]) and it[f] == ref["iters"][f], (vn, f)
+    h = torch.zeros((1, N), dtype=torch.uint8, device=dev)
+    o = torch.zeros(1, dtype=torch.uint8, device=dev)
+    i = torch.zeros(1, dtype=torch.int32, device=dev)
+    x = torch.zeros((1, N * m), device=dev)
+    L = nb.lib()
+    assert L.nbldpc_decode(code._h, x.data_ptr(), 0, 10, h.data_ptr(), o.data_ptr(), i.data_ptr(), None) == -1
+    with pytest.raises(ValueError):
+        code.decode(torch.zeros((0, N * m), device=dev), 10)
