@@ -169,7 +169,10 @@ nbldpc_status_t nbldpc_decode_ex(nbldpc_code_t code, const float* llr, int frame
 /* End-to-end variant with HOST buffers: copies llr_host (float32 [frames][N*m], pinned memory
  * recommended) to the device, decodes, copies the results back to the host arrays
  * (hard_host [frames][N], ok_host [frames], iters_host [frames]) and synchronises `stream`
- * before returning.  opts->soft_out / events_out are ignored here. */
+ * before returning.  opts->soft_out / events_out are ignored here.  On the cluster-kernel path the
+ * host-to-device copy runs in up to 16 chunks on an internal copy stream, overlapped with the decode
+ * (the kernel starts after the first chunk; a frame of a later chunk is taken only after its chunk's
+ * arrival flag is raised by a stream memory write).  NBLDPC_NO_OVERLAP=1 in the environment disables it. */
 nbldpc_status_t nbldpc_decode_host(nbldpc_code_t code, const float* llr_host, int frames, int max_iters,
                                    uint8_t* hard_host, uint8_t* ok_host, int32_t* iters_host, void* stream,
                                    const nbldpc_decode_opts_t* opts);

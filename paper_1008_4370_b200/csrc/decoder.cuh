@@ -69,6 +69,9 @@ struct CallDev {            // per-call arguments, written on the stream before 
   float* p0buf;       // nbldpc_decode_pmf: [S][N][q] P_v^0 = WHT(pmf) / sum(pmf) per slot
   float* post_out;    // symbol posterior [frames][N][q] (or NULL), rewritten at every iteration
   uint8_t* map_out;   // symbol-MAP decision [frames][N] (or NULL), idem: the last write is the stopping one
+  const int32_t* chunk_flags;  // nbldpc_decode_host: flag c != 0 once frames [c*chunk_frames, ..) are in HBM
+  int chunk_frames;
+  int pad2;
 };
 
 struct WorkDev {

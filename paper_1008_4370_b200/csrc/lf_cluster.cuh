@@ -455,6 +455,17 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
     } else {
       if (rank == 0 && tid == 0) {
         const int nf = atomicAdd(&ws.glob[0], 1);
+        if (call->chunk_flags != nullptr && nf < call->frames) {
+          // end-to-end decode: this frame's LLRs are still being copied in (nbldpc_decode_host
+          // overlaps the host-to-device copy with the decode); the copy stream raises the flag
+          const int32_t* fl = call->chunk_flags + nf / call->chunk_frames;
+          int v;
+          for (;;) {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(fl) : "memory");
+            if (v != 0) break;
+            __nanosleep(200);
+          }
+        }
         for (uint32_t r = 0; r < csz; ++r) dsmem_st(dsmem_addr(&sh_frame, r), nf);
       }
       cluster_sync_all();

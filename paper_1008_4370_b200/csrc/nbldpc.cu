@@ -5,6 +5,7 @@
 // the per-handle workspace (frame slots resident in L2/HBM), and drives the
 // pass kernel either through a CUDA graph whose WHILE conditional node loops on
 // the device until every frame has stopped, or through a host launch loop.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -33,6 +34,7 @@ constexpr int kPassesPerGraphIter = 8;               // pass kernels per WHILE-b
 constexpr size_t kDefaultSlotBudget = 64ull << 20;  // bytes of slot state kept L2-resident
 constexpr int kBigBlock = 512;                       // block-size variant for k_max * TT > 256
 constexpr int kMaxColWeight = 16;                    // column weights 1..16 (the general kernel)
+constexpr int kMaxChunks = 16;                       // nbldpc_decode_host: host-to-device copy chunks
 
 struct Workspace {
   int S = 0, Y = 1;
@@ -46,6 +48,9 @@ struct Workspace {
   size_t llr_stage_bytes = 0;
   uint8_t* out_stage = nullptr;
   size_t out_stage_bytes = 0;
+  cudaStream_t copy_stream = nullptr;  // nbldpc_decode_host: the host-to-device copies
+  cudaEvent_t ev_start = nullptr, ev_first = nullptr;
+  int32_t* chunk_flags = nullptr;       // [kMaxChunks]
   float* p0buf = nullptr;  // nbldpc_decode_pmf: [S][N][q] channel spectra
   size_t p0buf_bytes = 0;
   void* ls_base = nullptr;  // conventional Log-SP: W [2][S][E][q], L0 [S][N][q], xhat [S][N], counter
@@ -142,6 +147,10 @@ void free_workspace(Workspace& w) {
   if (w.out_stage) cudaFree(w.out_stage);
   if (w.p0buf) cudaFree(w.p0buf);
   if (w.ls_base) cudaFree(w.ls_base);
+  if (w.copy_stream) cudaStreamDestroy(w.copy_stream);
+  if (w.ev_start) cudaEventDestroy(w.ev_start);
+  if (w.ev_first) cudaEventDestroy(w.ev_first);
+  if (w.chunk_flags) cudaFree(w.chunk_flags);
   w = Workspace{};
 }
 
@@ -694,9 +703,10 @@ nbldpc_status_t decode_general(nbldpc_code_s* c, const float* llr, const float* 
 }
 
 // pmf != NULL: nbldpc_decode_pmf (llr unused; the direct kernel with the general channel spectrum)
+// chunk_flags: nbldpc_decode_host's arrival flags (cluster path only; see there)
 nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int max_iters, uint8_t* hard,
                             uint8_t* ok, int32_t* iters, cudaStream_t st, const nbldpc_decode_opts_t* opts,
-                            const float* pmf = nullptr) {
+                            const float* pmf = nullptr, const int32_t* chunk_flags = nullptr, int chunk_frames = 0) {
   int mode = 0, early = 1, slots = 0, use_graph = 0, direct = 0;
   float* soft = nullptr;
   int32_t* events = nullptr;
@@ -765,6 +775,10 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   }
   call.post_out = post;
   call.map_out = xmap;
+  if (!direct) {
+    call.chunk_flags = chunk_flags;
+    call.chunk_frames = chunk_frames;
+  }
   call.llr = llr;
   call.hard = hard;
   call.ok = ok;
@@ -1252,9 +1266,56 @@ nbldpc_status_t nbldpc_decode_host(nbldpc_code_t c, const float* llr_host, int f
     o.soft_out = nullptr;
     o.events_out = nullptr;
   }
-  NB_TRY(cudaMemcpyAsync(w.llr_stage, llr_host, llr_bytes, cudaMemcpyHostToDevice, st));
-  nbldpc_status_t rs = decode_impl(c, w.llr_stage, frames, max_iters, hard_d, ok_d, it_d, st, &o);
-  if (rs != NBLDPC_OK) return rs;
+  // The cluster path overlaps the host-to-device copy with the decode: the LLRs go over in chunks on
+  // a copy stream, each followed by a stream write of its arrival flag (no SM needed, so it cannot
+  // wait behind the persistent kernel), and the kernel starts after the first chunk; a cluster that
+  // takes a frame of a later chunk waits for that chunk's flag (ld.acquire.gpu).
+  using write_value_fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  static write_value_fn write_value = nullptr;
+  static bool write_value_probed = false;
+  if (!write_value_probed) {
+    write_value_probed = true;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      write_value = reinterpret_cast<write_value_fn>(fn);
+    cudaGetLastError();
+  }
+  const bool cluster_path = c->colw2 && o.algorithm == NBLDPC_ALG_LOG_FOURIER && o.vn_algorithm == NBLDPC_VN_SEPARABLE &&
+                            !o.symbol_post_out && !o.symbol_map_out;
+  const int chunk = std::max(c->p_ncl, (frames + kMaxChunks - 1) / kMaxChunks);
+  const int nchunk = (frames + chunk - 1) / chunk;
+  if (cluster_path && write_value && nchunk >= 2 && !getenv("NBLDPC_NO_OVERLAP")) {
+    if (!w.copy_stream) NB_TRY(cudaStreamCreateWithFlags(&w.copy_stream, cudaStreamNonBlocking));
+    if (!w.ev_start) NB_TRY(cudaEventCreateWithFlags(&w.ev_start, cudaEventDisableTiming));
+    if (!w.ev_first) NB_TRY(cudaEventCreateWithFlags(&w.ev_first, cudaEventDisableTiming));
+    if (!w.chunk_flags) NB_TRY(cudaMalloc(&w.chunk_flags, kMaxChunks * sizeof(int32_t)));
+    NB_TRY(cudaEventRecord(w.ev_start, st));  // the previous work on st (readers of llr_stage) is done first
+    NB_TRY(cudaStreamWaitEvent(w.copy_stream, w.ev_start, 0));
+    NB_TRY(cudaMemsetAsync(w.chunk_flags, 0, kMaxChunks * sizeof(int32_t), w.copy_stream));
+    const size_t row = (size_t)c->N * c->m;
+    for (int k = 0; k < nchunk; ++k) {
+      const int f0 = k * chunk, nf = std::min(chunk, frames - f0);
+      NB_TRY(cudaMemcpyAsync(w.llr_stage + (size_t)f0 * row, llr_host + (size_t)f0 * row, (size_t)nf * row * sizeof(float),
+                             cudaMemcpyHostToDevice, w.copy_stream));
+      if (write_value(reinterpret_cast<CUstream>(w.copy_stream), reinterpret_cast<CUdeviceptr>(w.chunk_flags + k), 1,
+                      CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+        return NBLDPC_ERR_CUDA;
+      if (k == 0) NB_TRY(cudaEventRecord(w.ev_first, w.copy_stream));
+    }
+    NB_TRY(cudaStreamWaitEvent(st, w.ev_first, 0));
+    nbldpc_status_t rs = decode_impl(c, w.llr_stage, frames, max_iters, hard_d, ok_d, it_d, st, &o, nullptr,
+                                     w.chunk_flags, chunk);
+    if (rs != NBLDPC_OK) {
+      cudaStreamSynchronize(w.copy_stream);
+      return rs;
+    }
+  } else {
+    NB_TRY(cudaMemcpyAsync(w.llr_stage, llr_host, llr_bytes, cudaMemcpyHostToDevice, st));
+    nbldpc_status_t rs = decode_impl(c, w.llr_stage, frames, max_iters, hard_d, ok_d, it_d, st, &o);
+    if (rs != NBLDPC_OK) return rs;
+  }
   NB_TRY(cudaMemcpyAsync(hard_host, hard_d, (size_t)frames * c->N, cudaMemcpyDeviceToHost, st));
   NB_TRY(cudaMemcpyAsync(ok_host, ok_d, frames, cudaMemcpyDeviceToHost, st));
   NB_TRY(cudaMemcpyAsync(iters_host, it_d, (size_t)frames * 4, cudaMemcpyDeviceToHost, st));
