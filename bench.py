@@ -274,7 +274,7 @@ def main():
     M, rows, cols, coeffs = synth.config_code(cfg["name"])
     code = nb.Code(cfg["m"], cfg["poly"], M, cfg["N"], rows, cols, coeffs)
     pmf_in = args.input == "pmf"
-    vn = 1 if args.symbol_out else args.vn  # the symbol outputs run the slot-pass kernel
+    vn = 1 if (args.symbol_out and pmf_in) else args.vn  # pmf + symbol outputs run the slot-pass kernel
     llr_np = channel_input(cfg, args.input, args.point, args.ebn0, f0, f1 - f0)
     llr_host = torch.from_numpy(llr_np).pin_memory()
     llr = llr_host.to(dev)

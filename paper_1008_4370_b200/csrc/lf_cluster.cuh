@@ -326,7 +326,9 @@ __device__ __forceinline__ int ppos(int z) {
 // a float work row per team takes the transposition, the decision's D and the check node's scatter.
 // KP > 0: the code's edge-slot stride kpad, known at compile time with full CTAs (NTHR threads,
 // NTHR / (KP TT) checks each), so that the chunk geometry constant-folds; 0: taken from P.
-template <int MB, int NTHR, bool PMF = false, bool F16 = false, int KP = 0>
+// SYM = true: also the symbol-level decision at every iteration, written to the
+// frame's output rows: mu_v = WHT(raw) . WHT(W_e) in the phase-B coordinates (M_v = raw (*) W_e).
+template <int MB, int NTHR, bool PMF = false, bool F16 = false, int KP = 0, bool SYM = false>
 #ifndef NB_CLUSTER_MINB
 #define NB_CLUSTER_MINB 2
 #endif
@@ -898,6 +900,50 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               for (int b = 0; b <= MB; ++b) mf[b] = acc[b].x + acc[b].y;
             } else {
               mf[0] = x[0] * d[0];
+            }
+          }
+          if constexpr (SYM) {
+            // symbol posterior and MAP: every lane runs the transforms (full-warp shuffles)
+            float a[R], bq[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) a[r] = is_a ? x[r] : 0.0f;
+            if constexpr (TT > 1) {
+#pragma unroll
+              for (int ch = 0; ch < 4; ++ch) {
+                const float4 v4 = is_a ? *reinterpret_cast<const float4*>(DB + db_word(t, 4 * ch)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                bq[4 * ch] = v4.x; bq[4 * ch + 1] = v4.y; bq[4 * ch + 2] = v4.z; bq[4 * ch + 3] = v4.w;
+              }
+            } else {
+#pragma unroll
+              for (int r = 0; r < R; ++r) bq[r] = is_a ? DB[r] : 0.0f;
+            }
+            wht_phase_b<MB, R, LR, LJ, TT>(a, t);
+            wht_phase_b<MB, R, LR, LJ, TT>(bq, t);
+            float tot = 0.0f, best = 0.0f;
+            int bx = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              a[r] = fmaxf(a[r] * bq[r], 0.0f);  // mu >= 0; rounding residues clamp to 0
+              tot += a[r];
+              if (r == 0 || a[r] > best || (a[r] == best && zr[r] < bx)) { best = a[r]; bx = zr[r]; }
+            }
+            if constexpr (TT > 1) {
+#pragma unroll
+              for (int off = TT / 2; off >= 1; off >>= 1) {
+                tot += __shfl_xor_sync(0xffffffffu, tot, off);
+                const float ob = __shfl_xor_sync(0xffffffffu, best, off);
+                const int ox = __shfl_xor_sync(0xffffffffu, bx, off);
+                if (ob > best || (ob == best && ox < bx)) { best = ob; bx = ox; }
+              }
+            }
+            if (is_a) {
+              const float inv = tot > 0.0f ? 1.0f / tot : 0.0f;
+              if (call->post_out) {
+                float* dst = call->post_out + ((size_t)f * cd.N + var) * Q;
+#pragma unroll
+                for (int r = 0; r < R; ++r) dst[zr[r]] = a[r] * inv;
+              }
+              if (call->map_out && t == 0) call->map_out[(size_t)f * cd.N + var] = (uint8_t)bx;
             }
           }
           // signs of M(0) and M(alpha^i) over the team (bit i of sbits = [M(.) < 0], index 0 = M(0))

@@ -251,8 +251,35 @@ void* persist_kp_ptr(int m, int kpad) {
   return nullptr;
 }
 
-// pmf = 1: the nbldpc_decode_pmf variant; f16 = 1: half-precision messages (NBLDPC_MSG_F16)
-void* persist_kernel_ptr(int m, int big, int pmf = 0, int f16 = 0) {
+// the LLR kernel with the symbol-level outputs (SYM)
+template <int MB, int NTHR>
+void* cluster_sym_fn() { return reinterpret_cast<void*>(&nb::lf_cluster_kernel<MB, NTHR, false, false, 0, true>); }
+void* persist_sym_ptr(int m, int big) {
+  switch (m * 2 + (big ? 1 : 0)) {
+    case 2: return cluster_sym_fn<1, 256>();
+    case 3: return cluster_sym_fn<1, 512>();
+    case 4: return cluster_sym_fn<2, 256>();
+    case 5: return cluster_sym_fn<2, 512>();
+    case 6: return cluster_sym_fn<3, 256>();
+    case 7: return cluster_sym_fn<3, 512>();
+    case 8: return cluster_sym_fn<4, 256>();
+    case 9: return cluster_sym_fn<4, 512>();
+    case 10: return cluster_sym_fn<5, 256>();
+    case 11: return cluster_sym_fn<5, 512>();
+    case 12: return cluster_sym_fn<6, 256>();
+    case 13: return cluster_sym_fn<6, 512>();
+    case 14: return cluster_sym_fn<7, 256>();
+    case 15: return cluster_sym_fn<7, 512>();
+    case 16: return cluster_sym_fn<8, 256>();
+    case 17: return cluster_sym_fn<8, 512>();
+  }
+  return nullptr;
+}
+
+// pmf = 1: the nbldpc_decode_pmf variant; f16 = 1: half-precision messages (NBLDPC_MSG_F16);
+// sym = 1: the symbol-output variant (LLR input)
+void* persist_kernel_ptr(int m, int big, int pmf = 0, int f16 = 0, int sym = 0) {
+  if (sym) return (pmf || f16) ? nullptr : persist_sym_ptr(m, big);
   if (f16) return pmf ? nullptr : persist_kernel_ptr_t<false, true>(m, big);
   return pmf ? persist_kernel_ptr_t<true, false>(m, big) : persist_kernel_ptr_t<false, false>(m, big);
 }
@@ -272,7 +299,7 @@ int persist_team_words(int m) {
 }
 
 cudaError_t launch_cluster(const nbldpc_code_s* c, const nb::ClusterParams& P, int ncl, cudaStream_t st, int pmf = 0,
-                           int f16 = 0) {
+                           int f16 = 0, int sym = 0) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(ncl * c->p_cs));
   cfg.blockDim = dim3((unsigned)c->p_block);
@@ -286,7 +313,8 @@ cudaError_t launch_cluster(const nbldpc_code_s* c, const nb::ClusterParams& P, i
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void* args[] = {const_cast<nb::ClusterParams*>(&P)};
-  void* fn = (c->p_kp && !pmf && !f16) ? persist_kp_ptr(c->m, c->p_kp) : persist_kernel_ptr(c->m, c->p_big, pmf, f16);
+  void* fn = (c->p_kp && !pmf && !f16 && !sym) ? persist_kp_ptr(c->m, c->p_kp)
+                                               : persist_kernel_ptr(c->m, c->p_big, pmf, f16, sym);
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
@@ -305,18 +333,19 @@ cudaError_t ensure_smem_attr(const nbldpc_code_s* c) {
     if (e != cudaSuccess) return e;
     g_attr_smem[d][k] = c->smem;
   }
-  static size_t p_attr[64][18 * 4 + 32] = {};
-  for (int var = 0; var < 4; ++var) {  // plain, pmf, f16, compile-time geometry
-    const int pmf = var == 1, f16 = var == 2;
-    void* fn = var == 3 ? (c->p_kp ? persist_kp_ptr(c->m, c->p_kp) : nullptr) : persist_kernel_ptr(c->m, c->p_big, pmf, f16);
+  static size_t p_attr[64][18 * 5 + 32] = {};
+  for (int var = 0; var < 5; ++var) {  // plain, pmf, f16, compile-time geometry, symbol outputs
+    const int pmf = var == 1, f16 = var == 2, sym = var == 4;
+    void* fn = var == 3 ? (c->p_kp ? persist_kp_ptr(c->m, c->p_kp) : nullptr)
+                        : persist_kernel_ptr(c->m, c->p_big, pmf, f16, sym);
     if (!fn) continue;
     if (c->p_cs > 8) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;
     }
     // one cache slot per kernel: (m, big, variant), or (m, kpad) for the compile-time-geometry one
-    int k = (c->m * 2 + c->p_big) * 4 + var;
-    if (var == 3) k = 18 * 4 + (c->m - 1) * 4 + (c->p_kp == 4 ? 0 : c->p_kp == 8 ? 1 : c->p_kp == 16 ? 2 : 3);
+    int k = (c->m * 2 + c->p_big) * 5 + var;
+    if (var == 3) k = 18 * 5 + (c->m - 1) * 4 + (c->p_kp == 4 ? 0 : c->p_kp == 8 ? 1 : c->p_kp == 16 ? 2 : 3);
     const int d = c->device & 63;
     if (p_attr[d][k] < c->p_smem) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->p_smem);
@@ -747,7 +776,7 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
     if ((soft && !is_device_ptr(soft)) || (events && !is_device_ptr(events))) return NBLDPC_ERR_INVALID_ARGUMENT;
     return decode_general(c, llr, pmf, frames, max_iters, hard, ok, iters, early, soft, events, post, xmap, st);
   }
-  if ((post || xmap) && direct == 0) direct = 1;  // the symbol decision lives in the pass kernel
+  if ((post || xmap) && direct == 0 && pmf) direct = 1;  // pmf + symbol outputs: the pass kernel
   if (pmf && direct) direct = 2;                   // the pass kernel's pmf variant
   if (slots < 0) return NBLDPC_ERR_INVALID_ARGUMENT;
   if ((soft && !is_device_ptr(soft)) || (events && !is_device_ptr(events))) return NBLDPC_ERR_INVALID_ARGUMENT;
@@ -801,7 +830,7 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   w.last_host_launches = 1;
   if (!direct) {
     nb::ClusterParams PP = make_cparams(c, 0, 0, nullptr);
-    NB_TRY(launch_cluster(c, PP, S, st, pmf != nullptr, f16));
+    NB_TRY(launch_cluster(c, PP, S, st, pmf != nullptr, f16, (post || xmap) ? 1 : 0));
     w.last_graph = 0;
     w.last_host_launches = 2;
     return NBLDPC_OK;

@@ -188,8 +188,11 @@ POST_CASES = [
 ]
 
 
+@pytest.mark.parametrize("vn", [0, 1])
 @pytest.mark.parametrize("name,kind,pt,F,nsample", POST_CASES)
-def test_symbol_posterior_and_map_parity(dev, name, kind, pt, F, nsample):
+def test_symbol_posterior_and_map_parity(dev, name, kind, pt, F, nsample, vn):
+    # LLR input: vn 0 the cluster kernel's symbol-output variant, vn 1 the slot-pass kernel;
+    # pmf input: the pass kernel either way
     # symbol-level TENTATIVE DECISION at the stopping iteration (reading R24):
     # per frame the posterior is within 1e-4 of the fp64 oracle or no further than twice the
     # oracle's own fp32 twin (the message state carries fp32 rounding into an uncertain posterior),
@@ -203,8 +206,8 @@ def test_symbol_posterior_and_map_parity(dev, name, kind, pt, F, nsample):
         plain = code.decode_pmf(torch.from_numpy(x).to(dev), c["max_iters"], vn_algorithm=1)
     else:
         _, x, _ = config_inputs(name, 0, F, point=pt)
-        out = code.decode(torch.from_numpy(x).to(dev), c["max_iters"], want_post=True)
-        plain = code.decode(torch.from_numpy(x).to(dev), c["max_iters"], vn_algorithm=1)
+        out = code.decode(torch.from_numpy(x).to(dev), c["max_iters"], want_post=True, vn_algorithm=vn)
+        plain = code.decode(torch.from_numpy(x).to(dev), c["max_iters"], vn_algorithm=vn)
     for k in ("hard", "ok", "iters"):  # the symbol outputs do not perturb the decode
         assert torch.equal(out[k], plain[k]), k
     idx = np.sort(np.random.default_rng(3).choice(F, nsample, replace=False))
