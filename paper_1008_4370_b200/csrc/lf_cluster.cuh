@@ -1070,11 +1070,21 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           if constexpr (TT > 1) __syncwarp();  // transposition / DB reads of X done
           if (cvalid) {
             // scatter: X_e(pi_e^-1 z) = U_e(z) = T_e(.); padding teams hold the neutral message
+#ifdef NB_SMEM_GENERIC
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
               st[oidx[r]] = __uint_as_float(up[r]);
             }
+#else
+            // 32-bit shared-window addresses: one LEA per entry instead of an IMAD + IADD3 pair
+            const uint32_t st_s = smem_u32(st);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(st_s + ((uint32_t)oidx[r] << 2)), "r"(up[r]) : "memory");
+            }
+#endif
           }
           check_sync(lc, TPC);
           switch (JPT) {
@@ -1087,10 +1097,18 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           check_sync(lc, TPC);
           if (active) {
             float out[R];
+#ifndef NB_SMEM_GENERIC
+            const uint32_t tot_s = smem_u32(TOT);
+#endif
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
+#ifdef NB_SMEM_GENERIC
               const float xt = TOT[oidx[r]];
+#else
+              float xt;
+              asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xt) : "r"(tot_s + ((uint32_t)oidx[r] << 2)) : "memory");
+#endif
               const float mg = fabsf(xt) - __uint_as_float(up[r] & ~kSign);  // >= 0 up to rounding
               out[r] = __uint_as_float((__float_as_uint(mg) & ~kSign) | ((__float_as_uint(xt) ^ up[r]) & kSign));
             }
