@@ -347,3 +347,26 @@ def test_largest_check_team_and_empty_batches(dev):
     assert L.nbldpc_decode(code._h, x.data_ptr(), 0, 10, h.data_ptr(), o.data_ptr(), i.data_ptr(), None) == -1
     with pytest.raises(ValueError):
         code.decode(torch.zeros((0, N * m), device=dev), 10)
+
+
+def test_saturated_and_erased_channels(dev):
+    """Degenerate channels through the hot path: saturated LLRs (|L| = 1e4, tanh = +-1 exactly) decode
+    the sent codeword at the first iteration; all-zero LLRs (an erasure channel, uniform prior) make
+    every message neutral, so the decision is the all-zero word, a codeword, at iteration 1 -- the same
+    as the oracle in both cases."""
+    name = "C3"
+    c = synth.CONFIGS[name]
+    _, _, xs = config_inputs(name, 0, 8)
+    bits = synth.symbols_to_bits(xs, c["m"]).astype(np.float32)
+    sat = (1.0 - 2.0 * bits) * 1.0e4
+    era = np.zeros_like(sat)
+    code = gpu_code(name)
+    ocode = oracle_code(name)
+    for llr, want in ((sat, xs.astype(np.uint8)), (era, np.zeros_like(xs, dtype=np.uint8))):
+        for vn in (0, 1):
+            out = code.decode(torch.from_numpy(np.ascontiguousarray(llr)).to(dev), c["max_iters"], vn_algorithm=vn,
+                              want_events=True)
+            assert (out["iters"] == 1).all() and (out["ok"] == 1).all()
+            assert np.array_equal(out["hard"].cpu().numpy(), want)
+        ref = ocode.lf_decode_batch(llr, c["max_iters"])
+        assert np.array_equal(ref["hard"], want) and (ref["iters"] == 1).all()
