@@ -79,7 +79,11 @@ struct CCfg {
   static constexpr int THW = THREG ? 0 : 8;          // channel-term floats per team and stage buffer
   // shared memory per team (floats): message row x 2 stage buffers (+ channel terms x 2); the consumed
   // row doubles as the transposition buffer, the decision buffer and the check node's scatter target
-  static constexpr int TEAMW = 2 * QS + 2 * THW;
+#ifndef NB_NSTAGE
+#define NB_NSTAGE 2
+#endif
+  static constexpr int NS = NB_NSTAGE;               // stage buffers per group (chunks in flight + 1)
+  static constexpr int TEAMW = NS * QS + NS * THW;
 };
 
 // Message storage ("reader-ordered rows"): row r holds the message CONSUMED by edge slot r, i.e. the
@@ -337,7 +341,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   constexpr int Q = C::Q, R = C::R, TT = C::TT, LR = C::LR, LJ = C::LJ, CH = C::CH;
   extern __shared__ __align__(16) float smem[];
   __shared__ int sh_frame, sh_flag[2], sh_bad;
-  __shared__ __align__(8) uint64_t sh_mbar[16];  // [group][buffer]: the group's teams arrive, bulk copies complete_tx
+  __shared__ __align__(8) uint64_t sh_mbar[8 * C::NS];  // [group][buffer]: the group's teams arrive, bulk copies complete_tx
 
   const CodeDev& cd = P.code;
   const WorkDev& ws = P.ws;
@@ -358,7 +362,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   const int GT = TPC > 32 ? TPC : 32;
   const int ngrp = nthr / GT;
   const int grp = threadIdx.x / GT;
-  uint64_t* const gmbar = &sh_mbar[2 * grp];
+  constexpr int NS = C::NS;
+  uint64_t* const gmbar = &sh_mbar[NS * grp];
   auto group_sync = [&]() {
     if (GT == 32) {
       __syncwarp();
@@ -379,13 +384,13 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   const int TG = GT / TT;                        // teams per group
   const int CPG = GT / TPC;                      // checks per group
   const int GBLK = TG * C::QS;                   // one stage buffer of a group (floats)
-  float* const GST = smem + grp * 2 * GBLK;      // the group's stage buffers
+  float* const GST = smem + grp * NS * GBLK;     // the group's stage buffers
   const int trow = team - grp * TG;              // my team's row within a group stage buffer
   // F16: the group's region holds two stage buffers of half rows (GBLKH floats each) and the float
   // work rows (GBLK floats), the same bytes as two float stage buffers
   const int GBLKH = GBLK / 2;
-  float* const WK = F16 ? GST + 2 * GBLKH + trow * C::QS : nullptr;  // my work row
-  float* const THB = smem + nteams * 2 * C::QS + team * 8;  // + b * nteams * 8 (wide teams only)
+  float* const WK = F16 ? GST + NS * GBLKH + trow * C::QS : nullptr;  // my work row
+  float* const THB = smem + nteams * NS * C::QS + team * 8;  // + b * nteams * 8 (wide teams only)
   float* const TOT = smem + nteams * C::TEAMW + lc * Q;
   uint64_t* const PT = reinterpret_cast<uint64_t*>(smem + nteams * C::TEAMW + CPC * Q);  // [q] pi_h^-1 images
   EdgeRec* const recs = reinterpret_cast<EdgeRec*>(PT + Q);
@@ -397,7 +402,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   const int JPT = KT / SPLIT;
   const int wgrp = pck / SPLIT;
   const int jbase = (pck % SPLIT) * JPT;
-  const int gbase = in_check ? (int)(GST - smem) + (F16 ? 2 * GBLKH : 0) + ((lc - grp * CPG) * KT + jbase) * C::QS + wgrp
+  const int gbase = in_check ? (int)(GST - smem) + (F16 ? NS * GBLKH : 0) + ((lc - grp * CPG) * KT + jbase) * C::QS + wgrp
                              : 0;  // + buf * GBLK (F32: the consumed stage rows; F16: the work rows)
   // my phase-B z's
   int zr[R];
@@ -428,8 +433,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
     sh_flag[0] = 0;
     sh_flag[1] = 0;
     for (int gg = 0; gg < ngrp; ++gg) {
-      mbar_init(&sh_mbar[2 * gg], (uint32_t)(GT / TT));
-      mbar_init(&sh_mbar[2 * gg + 1], (uint32_t)(GT / TT));
+      for (int b = 0; b < NS; ++b) mbar_init(&sh_mbar[NS * gg + b], (uint32_t)(GT / TT));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -600,12 +604,12 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
       };
 
       int buf = 0;
-      if (nch > 0) stage(0, 0);
+      for (int k0 = 0; k0 < NS - 1 && k0 < nch; ++k0) stage(k0, k0);  // prologue: NS - 1 chunks in flight
       float4 thn[2];
       th_load(0, thn);
 #pragma unroll 1
       for (int kc = 0; kc < nch; ++kc) {
-        if (kc + 1 < nch) stage(kc + 1, buf ^ 1);
+        if (kc + NS - 1 < nch) stage(kc + NS - 1, buf == 0 ? NS - 1 : buf - 1);
         const float4 thc[2] = {thn[0], thn[1]};
         th_load(kc + 1, thn);
         mbar_wait(&gmbar[buf], (mb_parity >> buf) & 1u);
@@ -1171,7 +1175,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         // generic-proxy writes to this stage buffer (DB) are ordered before its next bulk fill
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         group_sync();  // the group's buffers of this chunk are free
-        buf ^= 1;
+        buf = buf + 1 == NS ? 0 : buf + 1;
       }
       cp_async_wait<0>();
       if (step) break;
