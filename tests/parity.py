@@ -85,3 +85,20 @@ def stable_frames(ocode, llr, max_iters, mode=0):
     b = ocode.lf_decode_batch(llr, max_iters, mode=mode, f32=True)
     stable = (a["hard"] == b["hard"]).all(1) & (a["ok"] == b["ok"]) & (a["iters"] == b["iters"])
     return a, stable
+
+
+def fail_trajectory_stable(decode, x_row, max_iters, **kw):
+    """Reading R20 for a frame the oracle does not converge on (ok = 0 at max_iters): its f64 and
+    f32 trajectories must also agree at max_iters - 5 and max_iters - 10 iterations before it counts
+    as stable -- a chaotic non-converged frame can coincide at the last iteration by chance (C5 at
+    4.5 dB: frame 1999 agrees at 50 and 49 iterations, differs by 2 symbols at 30, 40 and 45).
+    ``decode`` is the oracle's batch decode (lf_decode_batch, lf_decode_batch_pmf or ls_decode_batch)."""
+    for it in (max_iters - 5, max_iters - 10):
+        if it < 1:
+            continue
+        a = decode(x_row[None], it, early_stop=False, **kw)
+        b = decode(x_row[None], it, early_stop=False, f32=True, **kw)
+        if not np.array_equal(a["hard"][0], b["hard"][0]):
+            return False
+    return True
+

@@ -12,7 +12,7 @@ torch = pytest.importorskip("torch")
 import oracle
 import synth
 from helpers import DEFAULT_POLY
-from parity import config_inputs, oracle_code
+from parity import config_inputs, fail_trajectory_stable, oracle_code
 
 pytestmark = pytest.mark.gpu
 
@@ -38,6 +38,8 @@ def _compare(ocode, out, x, idx, max_iters, pmf=False):
         for n, b in enumerate(bad):
             stable = (np.array_equal(twin["hard"][n], ref["hard"][b]) and twin["ok"][n] == ref["ok"][b]
                       and twin["iters"][n] == ref["iters"][b])
+            if stable and ref["ok"][b] == 0:
+                stable = fail_trajectory_stable(ocode.ls_decode_batch, x[idx][b], max_iters, pmf=pmf)
             assert not stable, (f"stable frame {idx[b]} differs: gpu iters {it[b]} ok {ok[b]} vs oracle "
                                 f"{ref['iters'][b]} {ref['ok'][b]}, {int((hard[b] != ref['hard'][b]).sum())} symbols")
             unstable += 1

@@ -13,7 +13,8 @@ torch = pytest.importorskip("torch")
 
 import oracle
 import synth
-from parity import (config_inputs, message_mismatch, oracle_code, oracle_to_packed, packed_to_oracle)
+from parity import (config_inputs, fail_trajectory_stable, message_mismatch, oracle_code, oracle_to_packed,
+                    packed_to_oracle)
 
 pytestmark = pytest.mark.gpu
 
@@ -53,6 +54,8 @@ def compare_decode(name, gpu_out, llr_np, idx, max_iters, mode=0):
         for n, b in enumerate(bad):
             oracle_stable = (np.array_equal(twin["hard"][n], ref["hard"][b]) and twin["ok"][n] == ref["ok"][b]
                              and twin["iters"][n] == ref["iters"][b])
+            if oracle_stable and ref["ok"][b] == 0:
+                oracle_stable = fail_trajectory_stable(ocode.lf_decode_batch, sub[b], max_iters, mode=mode)
             assert not oracle_stable, (
                 f"{name}: stable frame {idx[b]} differs: gpu iters {it[b]} ok {ok[b]} vs oracle "
                 f"{ref['iters'][b]} {ref['ok'][b]}, {int((hard[b] != ref['hard'][b]).sum())} symbols")

@@ -11,7 +11,7 @@ torch = pytest.importorskip("torch")
 
 import synth
 from helpers import bit_prior
-from parity import config_inputs, oracle_code
+from parity import config_inputs, fail_trajectory_stable, oracle_code
 
 pytestmark = pytest.mark.gpu
 
@@ -54,6 +54,8 @@ def _compare(name, out, pmf, idx, max_iters):
         for n, b in enumerate(bad):
             stable = (np.array_equal(twin["hard"][n], ref["hard"][b]) and twin["ok"][n] == ref["ok"][b]
                       and twin["iters"][n] == ref["iters"][b])
+            if stable and ref["ok"][b] == 0:
+                stable = fail_trajectory_stable(ocode.lf_decode_batch_pmf, pmf[idx][b], max_iters)
             assert not stable, (f"{name}: stable frame {idx[b]} differs: gpu iters {it[b]} ok {ok[b]} vs "
                                 f"oracle {ref['iters'][b]} {ref['ok'][b]}")
             unstable += 1
