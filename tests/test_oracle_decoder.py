@@ -237,3 +237,21 @@ def test_f32_twin_tracks_f64_on_c1():
     b = code.lf_decode_batch(llr, c["max_iters"], f32=True)
     same = (a["hard"] == b["hard"]).all(1) & (a["ok"] == b["ok"]) & (a["iters"] == b["iters"])
     assert same.mean() > 0.9
+
+
+try:
+    from hypothesis import given, settings, strategies as st
+
+    @settings(max_examples=25, deadline=None, derandomize=True)
+    @given(m=st.integers(1, 4), k=st.sampled_from([3, 4, 6]), half_n=st.integers(3, 8), seed=st.integers(0, 10**6),
+           mu=st.floats(-1.0, 2.5), sd=st.floats(0.3, 3.0))
+    def test_lf_equals_sp_random_codes(m, k, half_n, seed, mu, sd):
+        # PAPER.md:329-330 on randomly drawn (2,k) codes, fields and channels: O-LF's messages are the
+        # WHT of O-SP's, edge by edge, for three iterations
+        N = half_n * k
+        M, rows, cols, coeffs = synth.make_regular_code(N, k, m, seed)
+        code = oracle.Code(oracle.Field(m, DEFAULT_POLY[m]), M, N, rows, cols, coeffs)
+        llr = np.random.default_rng(seed).normal(mu, sd, N * m)
+        _sp_lf_agreement(code, llr, iters=3, tol=1e-8)
+except ImportError:  # pragma: no cover
+    pass
