@@ -1,6 +1,7 @@
 /*
  * nbldpc.h -- C-ABI of the B200-native (sm_100a) batched Log-Fourier SP decoder
- * for (j=2,k)-regular non-binary LDPC codes over GF(2^m), arXiv:1008.4370.
+ * for (j=2,k)-regular non-binary LDPC codes over GF(2^m), arXiv:1008.4370 (and, beyond the
+ * paper's (2,k) codes, any column weight 1..16; plus the conventional Log-SP it compares with).
  *
  * The decoder runs the paper's Log-Fourier sum-product iteration
  * (section 3.2): messages are 2^m-point Walsh-Hadamard spectra
@@ -37,8 +38,9 @@ typedef enum {
                                        coefficient not in [1, 2^m-1], frames < 1, max_iters < 1,
                                        host pointer where a device pointer is required (or vice versa) */
   NBLDPC_ERR_NOT_PRIMITIVE = -2,    /* prim_poly not of degree m, or alpha's period != 2^m - 1 */
-  NBLDPC_ERR_UNSUPPORTED = -3,      /* a column weight != 2, duplicate (row, col), a row degree < 2,
-                                       or a row degree too large for one thread block */
+  NBLDPC_ERR_UNSUPPORTED = -3,      /* a column weight outside 1..16, duplicate (row, col), a row degree
+                                       < 2, a row degree too large for one thread block, or an option
+                                       combination a code does not support (see the options) */
   NBLDPC_ERR_CUDA = -4,             /* a CUDA runtime call failed */
   NBLDPC_ERR_OUT_OF_MEMORY = -5     /* device or pinned host allocation failed */
 } nbldpc_status_t;
