@@ -145,6 +145,13 @@ nbldpc_status_t nbldpc_code_info(nbldpc_code_t code, int* m, int* M, int* N, int
 /* Device bytes the decoder keeps per resident frame slot (messages, channel terms, estimates). */
 size_t nbldpc_slot_bytes(nbldpc_code_t code);
 
+/* Device bytes of the workspace a default nbldpc_decode of `frames` frames keeps on this handle
+ * (the resident slots times nbldpc_slot_bytes, plus the per-call control block); 0 for a NULL code,
+ * frames < 1, or a code with a column weight other than 2 (its general kernel sizes a workspace per
+ * call from the occupancy).  The workspace is allocated by the first decode and reused while it is large
+ * enough; it is released by nbldpc_destroy. */
+size_t nbldpc_workspace_bytes(nbldpc_code_t code, int frames);
+
 /* Number of kernels the most recent decode on this handle launched (setup, pass and control
  * kernels).  Synchronises the stream of that decode.  0 before the first decode. */
 nbldpc_status_t nbldpc_last_decode_launches(nbldpc_code_t code, long long* launches);

@@ -70,6 +70,7 @@ def lib():
         "nbldpc_last_cuda_error": (ctypes.c_char_p, []),
         "nbldpc_code_info": (i32, [vp, vp, vp, vp, vp, vp]),
         "nbldpc_slot_bytes": (sz, [vp]),
+        "nbldpc_workspace_bytes": (sz, [vp, i32]),
         "nbldpc_last_decode_launches": (i32, [vp, ctypes.POINTER(ctypes.c_longlong)]),
         "nbldpc_decode": (i32, [vp, vp, i32, i32, vp, vp, vp, vp]),
         "nbldpc_decode_ex": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, ctypes.POINTER(_Opts)]),
@@ -145,6 +146,10 @@ class Code:
     @property
     def slot_bytes(self) -> int:
         return int(self._L.nbldpc_slot_bytes(self._h))
+
+    def workspace_bytes(self, frames: int) -> int:
+        """Device bytes of the workspace a default decode of ``frames`` frames keeps (nbldpc_workspace_bytes)."""
+        return int(self._L.nbldpc_workspace_bytes(self._h, int(frames)))
 
     def _opts(self, syndrome_mode=0, early_stop=True, soft=None, events=None, slots=0, use_graph=0, vn_algorithm=0,
               post=None, xmap=None, algorithm=0, message_format=0):

@@ -1212,6 +1212,15 @@ nbldpc_status_t nbldpc_code_info(nbldpc_code_t c, int* m, int* M, int* N, int* E
 
 size_t nbldpc_slot_bytes(nbldpc_code_t c) { return c ? slot_bytes_of(c) : 0; }
 
+size_t nbldpc_workspace_bytes(nbldpc_code_t c, int frames) {
+  if (!c || frames < 1) return 0;
+  // the default path: the cluster kernel keeps one slot per resident cluster (decode_impl);
+  // codes with a column weight != 2 run the general kernel (two message sets + estimates per slot)
+  if (!c->colw2) return 0;  // allocated per call by decode_general, sized by occupancy
+  const size_t S = (size_t)std::min(c->p_ncl, frames);
+  return S * slot_bytes_of(c) + sizeof(CallDev) + 16 * sizeof(int32_t);
+}
+
 nbldpc_status_t nbldpc_last_decode_launches(nbldpc_code_t c, long long* launches) {
   if (!c || !launches) return NBLDPC_ERR_INVALID_ARGUMENT;
   std::lock_guard<std::mutex> lk(c->mu);

@@ -211,6 +211,16 @@ def test_invariance_slots_graph_batch(dev):
         assert torch.equal(again[k], base[k])
 
 
+def test_workspace_accounting(dev):
+    code = gpu_code("C2")
+    sb = code.slot_bytes
+    c = synth.CONFIGS["C2"]
+    assert sb >= 2 * code.E * c["q"] * 4  # the two message sets of a resident frame
+    w1, wbig = code.workspace_bytes(1), code.workspace_bytes(1 << 20)
+    assert sb <= w1 < 2 * sb and wbig > w1 and (wbig - w1) % sb == 0
+    assert code.workspace_bytes(0) == 0
+
+
 def test_decode_host_matches_device(dev):
     name = "C5"
     c = synth.CONFIGS[name]

@@ -92,6 +92,7 @@ def test_null_handles_are_rejected(L):
     assert L.nbldpc_decode(None, None, 1, 1, None, None, None, None) == -1
     assert L.nbldpc_code_info(None, None, None, None, None, None) == -1
     assert L.nbldpc_slot_bytes(None) == 0
+    assert L.nbldpc_workspace_bytes(None, 10) == 0
     n = ctypes.c_longlong()
     assert L.nbldpc_last_decode_launches(None, ctypes.byref(n)) == -1
 
