@@ -120,8 +120,17 @@ __global__ void __launch_bounds__(256) ls_frame_kernel(LsParams P) {
     float l[R];
     const float* l0 = L0 + (size_t)ed.var * Q + t * R;
     const float* wi = Win + (size_t)ed.partner * Q + t * R;
+    if constexpr (R >= 4) {  // 16-byte loads of the two rows
 #pragma unroll
-    for (int r = 0; r < R; ++r) l[r] = l0[r] + (first ? 0.0f : wi[r]);
+      for (int c4 = 0; c4 < R / 4; ++c4) {
+        const float4 a = reinterpret_cast<const float4*>(l0)[c4];
+        const float4 w = first ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<const float4*>(wi)[c4];
+        l[4 * c4] = a.x + w.x; l[4 * c4 + 1] = a.y + w.y; l[4 * c4 + 2] = a.z + w.z; l[4 * c4 + 3] = a.w + w.w;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) l[r] = l0[r] + (first ? 0.0f : wi[r]);
+    }
     float mx = l[0];
 #pragma unroll
     for (int r = 1; r < R; ++r) mx = fmaxf(mx, l[r]);
@@ -141,8 +150,17 @@ __global__ void __launch_bounds__(256) ls_frame_kernel(LsParams P) {
     mx = team_max<TT>(mx, tmask);
     const float lmx = mx > 0.0f ? lg2a(mx) : 0.0f;
     float* dst = Wout + (size_t)e * Q + t * R;
+    float o[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) dst[r] = v[r] > 0.0f ? lg2a(v[r]) - lmx : -kFloor;
+    for (int r = 0; r < R; ++r) o[r] = v[r] > 0.0f ? lg2a(v[r]) - lmx : -kFloor;
+    if constexpr (R >= 4) {
+#pragma unroll
+      for (int c4 = 0; c4 < R / 4; ++c4)
+        reinterpret_cast<float4*>(dst)[c4] = make_float4(o[4 * c4], o[4 * c4 + 1], o[4 * c4 + 2], o[4 * c4 + 3]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) dst[r] = o[r];
+    }
   };
   auto team_sync = [&]() {
     if constexpr (TT > 1) __syncwarp(tmask);  // a one-thread team owns its vectors alone
@@ -241,11 +259,23 @@ __global__ void __launch_bounds__(256) ls_frame_kernel(LsParams P) {
           const float* wb = Wout + (size_t)ed.partner * Q + t * R;
           float best = -3.0e38f;
           int bx = 0;
+          float mu[R];
+          if constexpr (R >= 4) {
 #pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const float mu = l0[r] + wa[r] + wb[r];
-            if (mu > best) { best = mu; bx = t * R + r; }
+            for (int c4 = 0; c4 < R / 4; ++c4) {
+              const float4 a = reinterpret_cast<const float4*>(l0)[c4];
+              const float4 b = reinterpret_cast<const float4*>(wa)[c4];
+              const float4 d = reinterpret_cast<const float4*>(wb)[c4];
+              mu[4 * c4] = a.x + b.x + d.x; mu[4 * c4 + 1] = a.y + b.y + d.y;
+              mu[4 * c4 + 2] = a.z + b.z + d.z; mu[4 * c4 + 3] = a.w + b.w + d.w;
+            }
+          } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) mu[r] = l0[r] + wa[r] + wb[r];
           }
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (mu[r] > best) { best = mu[r]; bx = t * R + r; }
 #pragma unroll
           for (int off = TT / 2; off >= 1; off >>= 1) {
             const float ob = __shfl_xor_sync(tmask, best, off);
