@@ -891,6 +891,8 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
 #undef NB_TH
 }
 
+// the small control kernels are defined in nbldpc.cu's translation unit only (NB_CONTROL_KERNELS)
+#ifdef NB_CONTROL_KERNELS
 __global__ void nb_setup_kernel(WorkDev ws, CallDev call) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) {
@@ -946,5 +948,6 @@ __global__ void nb_control_kernel(int32_t* glob, cudaGraphConditionalHandle h) {
     if (*(volatile const int32_t*)&glob[1] == 0) cudaGraphSetConditional(h, 0);
   }
 }
+#endif  // NB_CONTROL_KERNELS
 
 }  // namespace nb

@@ -1,0 +1,39 @@
+// k_other.cu -- the Log-SP comparison kernel and the general-column-weight kernel families
+#include "kernels.h"
+#include "lf_general.cuh"
+#include "logsp.cuh"
+
+namespace nbk {
+template <int MB>
+void* ls_fn() { return reinterpret_cast<void*>(&nb::ls_frame_kernel<MB>); }
+void* ls_kernel_ptr(int m) {
+  switch (m) {
+    case 1: return ls_fn<1>();
+    case 2: return ls_fn<2>();
+    case 3: return ls_fn<3>();
+    case 4: return ls_fn<4>();
+    case 5: return ls_fn<5>();
+    case 6: return ls_fn<6>();
+    case 7: return ls_fn<7>();
+    case 8: return ls_fn<8>();
+  }
+  return nullptr;
+}
+
+template <int MB>
+void* gen_fn() { return reinterpret_cast<void*>(&nb::lfg_frame_kernel<MB>); }
+void* gen_kernel_ptr(int m) {
+  switch (m) {
+    case 1: return gen_fn<1>();
+    case 2: return gen_fn<2>();
+    case 3: return gen_fn<3>();
+    case 4: return gen_fn<4>();
+    case 5: return gen_fn<5>();
+    case 6: return gen_fn<6>();
+    case 7: return gen_fn<7>();
+    case 8: return gen_fn<8>();
+  }
+  return nullptr;
+}
+
+}  // namespace nbk

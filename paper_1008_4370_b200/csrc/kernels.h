@@ -1,0 +1,15 @@
+// kernels.h -- host-side entry points to the kernel families (one translation unit each, so that
+// the library builds in parallel).  Each returns the kernel for the given field degree and variant,
+// or nullptr when that variant does not exist.
+#pragma once
+
+namespace nbk {
+void* pass_kernel_ptr(int m, int big, int direct);  // k_pass.cu: nb_pass_kernel (0 separable, 1 direct, 2 pmf)
+void* persist_plain_ptr(int m, int big);            // k_cluster.cu: lf_cluster_kernel, LLR input
+void* persist_pmf_ptr(int m, int big);              // k_cluster_pmf.cu: the symbol-pmf variant
+void* persist_f16_ptr(int m, int big);              // k_cluster_f16.cu: half-precision messages (m >= 3)
+void* persist_kp_ptr(int m, int kpad);              // k_cluster_kp.cu: compile-time chunk geometry
+void* persist_sym_ptr(int m, int big);              // k_cluster_sym.cu: symbol-level outputs
+void* ls_kernel_ptr(int m);                         // k_other.cu: the conventional Log-SP kernel
+void* gen_kernel_ptr(int m);                        // k_other.cu: the general-column-weight kernel
+}  // namespace nbk

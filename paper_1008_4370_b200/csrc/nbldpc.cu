@@ -17,9 +17,11 @@
 #include <vector>
 
 #include "../../include/nbldpc.h"
+#define NB_CONTROL_KERNELS  // the setup / control kernels live in this translation unit
 #include "decoder.cuh"
 #include "logsp.cuh"
 #include "lf_general.cuh"
+#include "kernels.h"
 #include "lf_cluster.cuh"
 
 using nb::CallDev;
@@ -154,134 +156,15 @@ void free_workspace(Workspace& w) {
   w = Workspace{};
 }
 
-template <int MB, int MAXB, bool DIRECT, bool PMF>
-void* pass_fn() { return reinterpret_cast<void*>(&nb::nb_pass_kernel<MB, MAXB, DIRECT, PMF>); }
-
-template <bool DIRECT, bool PMF>
-void* pass_kernel_ptr_t(int m, int big) {
-  switch (m * 2 + (big ? 1 : 0)) {
-    case 2: return pass_fn<1, 256, DIRECT, PMF>();
-    case 3: return pass_fn<1, kBigBlock, DIRECT, PMF>();
-    case 4: return pass_fn<2, 256, DIRECT, PMF>();
-    case 5: return pass_fn<2, kBigBlock, DIRECT, PMF>();
-    case 6: return pass_fn<3, 256, DIRECT, PMF>();
-    case 7: return pass_fn<3, kBigBlock, DIRECT, PMF>();
-    case 8: return pass_fn<4, 256, DIRECT, PMF>();
-    case 9: return pass_fn<4, kBigBlock, DIRECT, PMF>();
-    case 10: return pass_fn<5, 256, DIRECT, PMF>();
-    case 11: return pass_fn<5, kBigBlock, DIRECT, PMF>();
-    case 12: return pass_fn<6, 256, DIRECT, PMF>();
-    case 13: return pass_fn<6, kBigBlock, DIRECT, PMF>();
-    case 14: return pass_fn<7, 256, DIRECT, PMF>();
-    case 15: return pass_fn<7, kBigBlock, DIRECT, PMF>();
-    case 16: return pass_fn<8, 256, DIRECT, PMF>();
-    case 17: return pass_fn<8, kBigBlock, DIRECT, PMF>();
-  }
-  return nullptr;
-}
-// direct = 1: the paper's q^2-term convolution; 0: separable butterflies;
-// 2: the direct convolution with the channel spectrum of a general pmf (nbldpc_decode_pmf)
-void* pass_kernel_ptr(int m, int big, int direct) {
-  if (direct == 2) return pass_kernel_ptr_t<true, true>(m, big);
-  return direct ? pass_kernel_ptr_t<true, false>(m, big) : pass_kernel_ptr_t<false, false>(m, big);
-}
-
-template <int MB, int NTHR, bool PMF, bool F16>
-void* cluster_fn() {
-  if constexpr (F16 && (PMF || MB < 3)) {  // half messages: LLR input, q >= 8 (16-byte row units)
-    return nullptr;
-  } else {
-    return reinterpret_cast<void*>(&nb::lf_cluster_kernel<MB, NTHR, PMF, F16>);
-  }
-}
-template <bool PMF, bool F16>
-void* persist_kernel_ptr_t(int m, int big) {
-  switch (m * 2 + (big ? 1 : 0)) {
-    case 2: return cluster_fn<1, 256, PMF, F16>();
-    case 3: return cluster_fn<1, 512, PMF, F16>();
-    case 4: return cluster_fn<2, 256, PMF, F16>();
-    case 5: return cluster_fn<2, 512, PMF, F16>();
-    case 6: return cluster_fn<3, 256, PMF, F16>();
-    case 7: return cluster_fn<3, 512, PMF, F16>();
-    case 8: return cluster_fn<4, 256, PMF, F16>();
-    case 9: return cluster_fn<4, 512, PMF, F16>();
-    case 10: return cluster_fn<5, 256, PMF, F16>();
-    case 11: return cluster_fn<5, 512, PMF, F16>();
-    case 12: return cluster_fn<6, 256, PMF, F16>();
-    case 13: return cluster_fn<6, 512, PMF, F16>();
-    case 14: return cluster_fn<7, 256, PMF, F16>();
-    case 15: return cluster_fn<7, 512, PMF, F16>();
-    case 16: return cluster_fn<8, 256, PMF, F16>();
-    case 17: return cluster_fn<8, 512, PMF, F16>();
-  }
-  return nullptr;
-}
-// pmf = 1: the nbldpc_decode_pmf variant (probability-domain variable node)
-// the plain LLR kernel with the chunk geometry at compile time (KP = kpad, full CTAs)
-template <int MB, int KP>
-void* cluster_kp_fn() {
-  constexpr int TT = MB <= 4 ? 1 : (1 << MB) / 16;
-  if constexpr (KP * TT > 512) {
-    return nullptr;
-  } else {
-    return reinterpret_cast<void*>(&nb::lf_cluster_kernel<MB, (KP * TT > 256 ? 512 : 256), false, false, KP>);
-  }
-}
-template <int MB>
-void* cluster_kp_m(int kpad) {
-  switch (kpad) {
-    case 4: return cluster_kp_fn<MB, 4>();
-    case 8: return cluster_kp_fn<MB, 8>();
-    case 16: return cluster_kp_fn<MB, 16>();
-    case 32: return cluster_kp_fn<MB, 32>();
-  }
-  return nullptr;
-}
-void* persist_kp_ptr(int m, int kpad) {
-  switch (m) {
-    case 1: return cluster_kp_m<1>(kpad);
-    case 2: return cluster_kp_m<2>(kpad);
-    case 3: return cluster_kp_m<3>(kpad);
-    case 4: return cluster_kp_m<4>(kpad);
-    case 5: return cluster_kp_m<5>(kpad);
-    case 6: return cluster_kp_m<6>(kpad);
-    case 7: return cluster_kp_m<7>(kpad);
-    case 8: return cluster_kp_m<8>(kpad);
-  }
-  return nullptr;
-}
-
-// the LLR kernel with the symbol-level outputs (SYM)
-template <int MB, int NTHR>
-void* cluster_sym_fn() { return reinterpret_cast<void*>(&nb::lf_cluster_kernel<MB, NTHR, false, false, 0, true>); }
-void* persist_sym_ptr(int m, int big) {
-  switch (m * 2 + (big ? 1 : 0)) {
-    case 2: return cluster_sym_fn<1, 256>();
-    case 3: return cluster_sym_fn<1, 512>();
-    case 4: return cluster_sym_fn<2, 256>();
-    case 5: return cluster_sym_fn<2, 512>();
-    case 6: return cluster_sym_fn<3, 256>();
-    case 7: return cluster_sym_fn<3, 512>();
-    case 8: return cluster_sym_fn<4, 256>();
-    case 9: return cluster_sym_fn<4, 512>();
-    case 10: return cluster_sym_fn<5, 256>();
-    case 11: return cluster_sym_fn<5, 512>();
-    case 12: return cluster_sym_fn<6, 256>();
-    case 13: return cluster_sym_fn<6, 512>();
-    case 14: return cluster_sym_fn<7, 256>();
-    case 15: return cluster_sym_fn<7, 512>();
-    case 16: return cluster_sym_fn<8, 256>();
-    case 17: return cluster_sym_fn<8, 512>();
-  }
-  return nullptr;
-}
+using nbk::pass_kernel_ptr;
+using nbk::persist_kp_ptr;
 
 // pmf = 1: the nbldpc_decode_pmf variant; f16 = 1: half-precision messages (NBLDPC_MSG_F16);
 // sym = 1: the symbol-output variant (LLR input)
 void* persist_kernel_ptr(int m, int big, int pmf = 0, int f16 = 0, int sym = 0) {
-  if (sym) return (pmf || f16) ? nullptr : persist_sym_ptr(m, big);
-  if (f16) return pmf ? nullptr : persist_kernel_ptr_t<false, true>(m, big);
-  return pmf ? persist_kernel_ptr_t<true, false>(m, big) : persist_kernel_ptr_t<false, false>(m, big);
+  if (sym) return (pmf || f16) ? nullptr : nbk::persist_sym_ptr(m, big);
+  if (f16) return pmf ? nullptr : nbk::persist_f16_ptr(m, big);
+  return pmf ? nbk::persist_pmf_ptr(m, big) : nbk::persist_plain_ptr(m, big);
 }
 // shared-memory words per edge team of the cluster kernel (nb::CCfg<m>::TEAM)
 int persist_team_words(int m) {
@@ -574,21 +457,7 @@ int default_slots(const nbldpc_code_s* c, int frames) {
 }
 
 // ---- conventional Log-SP (NBLDPC_ALG_LOG_SP): one CTA per frame, persistent
-template <int MB>
-void* ls_fn() { return reinterpret_cast<void*>(&nb::ls_frame_kernel<MB>); }
-void* ls_kernel_ptr(int m) {
-  switch (m) {
-    case 1: return ls_fn<1>();
-    case 2: return ls_fn<2>();
-    case 3: return ls_fn<3>();
-    case 4: return ls_fn<4>();
-    case 5: return ls_fn<5>();
-    case 6: return ls_fn<6>();
-    case 7: return ls_fn<7>();
-    case 8: return ls_fn<8>();
-  }
-  return nullptr;
-}
+using nbk::ls_kernel_ptr;
 
 nbldpc_status_t decode_logsp(nbldpc_code_s* c, const float* llr, const float* pmf, int frames, int max_iters,
                              uint8_t* hard, uint8_t* ok, int32_t* iters, int early, cudaStream_t st) {
@@ -650,21 +519,7 @@ nbldpc_status_t decode_logsp(nbldpc_code_s* c, const float* llr, const float* pm
 }
 
 // ---- any column weight (NBLDPC_VN_GENERAL, lf_general.cuh): one CTA per frame, persistent
-template <int MB>
-void* gen_fn() { return reinterpret_cast<void*>(&nb::lfg_frame_kernel<MB>); }
-void* gen_kernel_ptr(int m) {
-  switch (m) {
-    case 1: return gen_fn<1>();
-    case 2: return gen_fn<2>();
-    case 3: return gen_fn<3>();
-    case 4: return gen_fn<4>();
-    case 5: return gen_fn<5>();
-    case 6: return gen_fn<6>();
-    case 7: return gen_fn<7>();
-    case 8: return gen_fn<8>();
-  }
-  return nullptr;
-}
+using nbk::gen_kernel_ptr;
 
 nbldpc_status_t decode_general(nbldpc_code_s* c, const float* llr, const float* pmf, int frames, int max_iters,
                                uint8_t* hard, uint8_t* ok, int32_t* iters, int early, float* soft, int32_t* events,
