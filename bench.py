@@ -314,7 +314,20 @@ def main():
 
     # end to end through the host-buffer C-ABI entry (H2D + decode + D2H inside the timed region)
     e2e_ms, e2e_iters, d2h = 0.0, 0, F * cfg["N"] + F + 4 * F
-    if not args.no_e2e and (pmf_in or args.symbol_out):
+    if not args.no_e2e and pmf_in and not args.symbol_out:
+        # through the host-buffer C-ABI entry (pinned pmfs -> device -> decode -> host outputs, all timed)
+        hkw = dict(slots=args.slots, vn_algorithm=vn, algorithm=kw["algorithm"])
+        code.decode_pmf_host(llr_host, cfg["max_iters"], **hkw)
+        barrier()
+        for _ in range(args.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            hout = code.decode_pmf_host(llr_host, cfg["max_iters"], **hkw)
+            e2e_ms += 1e3 * (time.perf_counter() - t0)
+            e2e_iters += int(hout["iters"].sum())
+        barrier()
+    elif not args.no_e2e and (pmf_in or args.symbol_out):
         # through the Python binding: pinned H2D copy of the inputs, decode, D2H of every output
         if args.symbol_out:
             d2h += F * cfg["N"] * (4 * cfg["q"] + 1)

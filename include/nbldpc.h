@@ -206,6 +206,12 @@ nbldpc_status_t nbldpc_decode_pmf(nbldpc_code_t code, const float* pmf, int fram
                                   uint8_t* hard_symbols, uint8_t* syndrome_ok, int32_t* iters_used, void* stream,
                                   const nbldpc_decode_opts_t* opts);
 
+/* nbldpc_decode_pmf with HOST buffers, as nbldpc_decode_host: pmf_host float32 [frames][N][2^m] (pinned
+ * recommended), results to the host arrays; the copy overlaps the decode on the cluster-kernel path. */
+nbldpc_status_t nbldpc_decode_pmf_host(nbldpc_code_t code, const float* pmf_host, int frames, int max_iters,
+                                       uint8_t* hard_host, uint8_t* ok_host, int32_t* iters_host, void* stream,
+                                       const nbldpc_decode_opts_t* opts);
+
 /* One Log-Fourier iteration from a given state (step-parity tests; not on the hot path).
  * Requires every row of H to have the same degree k, a power of two >= 4 (else
  * NBLDPC_ERR_UNSUPPORTED): then the decoder's internal edge slots coincide with canonical order.

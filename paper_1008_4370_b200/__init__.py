@@ -76,6 +76,7 @@ def lib():
         "nbldpc_decode_ex": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, ctypes.POINTER(_Opts)]),
         "nbldpc_decode_host": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, ctypes.POINTER(_Opts)]),
         "nbldpc_decode_pmf": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, ctypes.POINTER(_Opts)]),
+        "nbldpc_decode_pmf_host": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, ctypes.POINTER(_Opts)]),
         "nbldpc_step": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, i32, vp]),
     }
     for name, (res, args) in sig.items():
@@ -249,6 +250,30 @@ class Code:
                                         out["ok"].data_ptr(), out["iters"].data_ptr(), _stream(stream),
                                         ctypes.byref(o))
         _check(st, "nbldpc_decode_host")
+        return out
+
+    def decode_pmf_host(self, pmf_host, max_iters: int, *, slots: int = 0, vn_algorithm: int = 0, out=None,
+                        stream=None, algorithm: int = 0):
+        """End-to-end pmf decode from HOST memory (nbldpc_decode_pmf_host): pmf_host float32 [F, N, q]."""
+        import torch
+
+        if isinstance(pmf_host, np.ndarray):
+            pmf_host = torch.from_numpy(np.ascontiguousarray(pmf_host, np.float32))
+        if pmf_host.is_cuda or pmf_host.dtype != torch.float32 or not pmf_host.is_contiguous():
+            raise ValueError("pmf_host must be a contiguous host float32 tensor")
+        F = pmf_host.numel() // (self.N * self.q)
+        if F * self.N * self.q != pmf_host.numel() or F < 1:
+            raise ValueError("pmf size is not a multiple of N*q")
+        if out is None:
+            pin = pmf_host.is_pinned()
+            out = {"hard": torch.empty((F, self.N), dtype=torch.uint8, pin_memory=pin),
+                   "ok": torch.empty(F, dtype=torch.uint8, pin_memory=pin),
+                   "iters": torch.empty(F, dtype=torch.int32, pin_memory=pin)}
+        o = self._opts(0, True, None, None, slots, 0, vn_algorithm, algorithm=algorithm)
+        st = self._L.nbldpc_decode_pmf_host(self._h, pmf_host.data_ptr(), F, int(max_iters), out["hard"].data_ptr(),
+                                            out["ok"].data_ptr(), out["iters"].data_ptr(), _stream(stream),
+                                            ctypes.byref(o))
+        _check(st, "nbldpc_decode_pmf_host")
         return out
 
     def step(self, llr, iter_: int, w_in=None, want_u=False, want_soft=False, vn_algorithm: int = 0, stream=None):

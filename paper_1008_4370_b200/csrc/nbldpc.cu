@@ -1119,9 +1119,14 @@ nbldpc_status_t nbldpc_decode(nbldpc_code_t c, const float* llr, int frames, int
   return nbldpc_decode_ex(c, llr, frames, max_iters, hard, ok, iters, stream, nullptr);
 }
 
-nbldpc_status_t nbldpc_decode_host(nbldpc_code_t c, const float* llr_host, int frames, int max_iters,
-                                   uint8_t* hard_host, uint8_t* ok_host, int32_t* iters_host, void* stream,
-                                   const nbldpc_decode_opts_t* opts) {
+}  // extern "C"
+
+namespace {
+// nbldpc_decode_host / nbldpc_decode_pmf_host: in_host is float32 [frames][N*m] LLRs or, with is_pmf,
+// [frames][N][q] symbol pmfs
+nbldpc_status_t decode_host_impl(nbldpc_code_t c, const float* llr_host, int is_pmf, int frames, int max_iters,
+                                 uint8_t* hard_host, uint8_t* ok_host, int32_t* iters_host, void* stream,
+                                 const nbldpc_decode_opts_t* opts) {
   if (!c || frames < 1 || max_iters < 1 || !llr_host || !hard_host || !ok_host || !iters_host)
     return NBLDPC_ERR_INVALID_ARGUMENT;
   if (is_device_ptr(llr_host) || is_device_ptr(hard_host)) return NBLDPC_ERR_INVALID_ARGUMENT;
@@ -1130,7 +1135,8 @@ nbldpc_status_t nbldpc_decode_host(nbldpc_code_t c, const float* llr_host, int f
   NB_TRY(cudaSetDevice(c->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   Workspace& w = c->ws;
-  const size_t llr_bytes = (size_t)frames * c->N * c->m * sizeof(float);
+  const size_t row = (size_t)c->N * (is_pmf ? c->q : c->m);  // floats per frame
+  const size_t llr_bytes = (size_t)frames * row * sizeof(float);
   const size_t out_bytes = align_up((size_t)frames * c->N, 256) + align_up(frames, 256) + (size_t)frames * 4;
   if (w.llr_stage_bytes < llr_bytes) {
     cudaStreamSynchronize(st);
@@ -1187,7 +1193,6 @@ nbldpc_status_t nbldpc_decode_host(nbldpc_code_t c, const float* llr_host, int f
     NB_TRY(cudaEventRecord(w.ev_start, st));  // the previous work on st (readers of llr_stage) is done first
     NB_TRY(cudaStreamWaitEvent(w.copy_stream, w.ev_start, 0));
     NB_TRY(cudaMemsetAsync(w.chunk_flags, 0, kMaxChunks * sizeof(int32_t), w.copy_stream));
-    const size_t row = (size_t)c->N * c->m;
     for (int k = 0; k < nchunk; ++k) {
       const int f0 = k * chunk, nf = std::min(chunk, frames - f0);
       NB_TRY(cudaMemcpyAsync(w.llr_stage + (size_t)f0 * row, llr_host + (size_t)f0 * row, (size_t)nf * row * sizeof(float),
@@ -1198,15 +1203,16 @@ nbldpc_status_t nbldpc_decode_host(nbldpc_code_t c, const float* llr_host, int f
       if (k == 0) NB_TRY(cudaEventRecord(w.ev_first, w.copy_stream));
     }
     NB_TRY(cudaStreamWaitEvent(st, w.ev_first, 0));
-    nbldpc_status_t rs = decode_impl(c, w.llr_stage, frames, max_iters, hard_d, ok_d, it_d, st, &o, nullptr,
-                                     w.chunk_flags, chunk);
+    nbldpc_status_t rs = decode_impl(c, is_pmf ? nullptr : w.llr_stage, frames, max_iters, hard_d, ok_d, it_d, st, &o,
+                                     is_pmf ? w.llr_stage : nullptr, w.chunk_flags, chunk);
     if (rs != NBLDPC_OK) {
       cudaStreamSynchronize(w.copy_stream);
       return rs;
     }
   } else {
     NB_TRY(cudaMemcpyAsync(w.llr_stage, llr_host, llr_bytes, cudaMemcpyHostToDevice, st));
-    nbldpc_status_t rs = decode_impl(c, w.llr_stage, frames, max_iters, hard_d, ok_d, it_d, st, &o);
+    nbldpc_status_t rs = decode_impl(c, is_pmf ? nullptr : w.llr_stage, frames, max_iters, hard_d, ok_d, it_d, st, &o,
+                                     is_pmf ? w.llr_stage : nullptr);
     if (rs != NBLDPC_OK) return rs;
   }
   NB_TRY(cudaMemcpyAsync(hard_host, hard_d, (size_t)frames * c->N, cudaMemcpyDeviceToHost, st));
@@ -1214,6 +1220,21 @@ nbldpc_status_t nbldpc_decode_host(nbldpc_code_t c, const float* llr_host, int f
   NB_TRY(cudaMemcpyAsync(iters_host, it_d, (size_t)frames * 4, cudaMemcpyDeviceToHost, st));
   NB_TRY(cudaStreamSynchronize(st));
   return NBLDPC_OK;
+}
+}  // namespace
+
+extern "C" {
+
+nbldpc_status_t nbldpc_decode_host(nbldpc_code_t c, const float* llr_host, int frames, int max_iters,
+                                   uint8_t* hard_host, uint8_t* ok_host, int32_t* iters_host, void* stream,
+                                   const nbldpc_decode_opts_t* opts) {
+  return decode_host_impl(c, llr_host, 0, frames, max_iters, hard_host, ok_host, iters_host, stream, opts);
+}
+
+nbldpc_status_t nbldpc_decode_pmf_host(nbldpc_code_t c, const float* pmf_host, int frames, int max_iters,
+                                       uint8_t* hard_host, uint8_t* ok_host, int32_t* iters_host, void* stream,
+                                       const nbldpc_decode_opts_t* opts) {
+  return decode_host_impl(c, pmf_host, 1, frames, max_iters, hard_host, ok_host, iters_host, stream, opts);
 }
 
 nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int iter, const float* w_in, float* w_out,

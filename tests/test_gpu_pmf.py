@@ -235,3 +235,17 @@ def test_symbol_posterior_and_map_parity(dev, name, kind, pt, F, nsample, vn):
         assert np.array_equal(xmap[n][clear], ref["map"][n][clear])
     assert checked >= max(1, (len(idx) * 3) // 4)
     assert eg_tot <= max(1e-4 * checked, 1.25 * et_tot)
+
+
+def test_pmf_host_entry_matches_device(dev):
+    # nbldpc_decode_pmf_host (chunked copy overlapped with the decode) = the device entry
+    name = "C2"
+    c = synth.CONFIGS[name]
+    pmf, _ = _pmf_inputs(name, 640, 0.5)
+    code = gpu_code(name)
+    d = code.decode_pmf(torch.from_numpy(pmf).to(dev), c["max_iters"])
+    for vn in (0, 1):
+        h = code.decode_pmf_host(torch.from_numpy(pmf).pin_memory(), c["max_iters"], vn_algorithm=vn)
+        ref = d if vn == 0 else code.decode_pmf(torch.from_numpy(pmf).to(dev), c["max_iters"], vn_algorithm=1)
+        for k in ("hard", "ok", "iters"):
+            assert torch.equal(ref[k].cpu(), h[k]), (vn, k)
