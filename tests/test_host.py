@@ -93,6 +93,12 @@ def test_null_handles_are_rejected(L):
     assert L.nbldpc_code_info(None, None, None, None, None, None) == -1
     assert L.nbldpc_slot_bytes(None) == 0
     assert L.nbldpc_workspace_bytes(None, 10) == 0
+    # every decode entry point rejects a NULL handle before touching the device
+    assert L.nbldpc_decode_ex(None, None, 1, 1, None, None, None, None, None) == -1
+    assert L.nbldpc_decode_pmf(None, None, 1, 1, None, None, None, None, None) == -1
+    assert L.nbldpc_decode_host(None, None, 1, 1, None, None, None, None, None) == -1
+    assert L.nbldpc_decode_pmf_host(None, None, 1, 1, None, None, None, None, None) == -1
+    assert L.nbldpc_step(None, None, 1, 0, None, None, None, None, None, 0, None) == -1
     n = ctypes.c_longlong()
     assert L.nbldpc_last_decode_launches(None, ctypes.byref(n)) == -1
 
