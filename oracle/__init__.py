@@ -79,6 +79,7 @@ def _lib():
                 "or_boxplus": (None, [i32, dp, dp, dp, dp, dp, dp]),
                 "or_gamma_inv": (ctypes.c_double, [i32, ctypes.c_double]),
                 "or_channel_prior": (None, [i32, dp, dp]),
+                "or_round_half": (ctypes.c_double, [ctypes.c_double]),
                 "or_code_new": (vp, [vp, i32, i32, i32, dp, dp, dp]),
                 "or_code_free": (None, [vp]),
                 "or_code_E": (i32, [vp]),
@@ -98,7 +99,8 @@ def _lib():
                 sig["or_lf_decode" + sfx] = (None, [vp, dp, i32, i32, i32, dp, dp, dp, dp, dp])
                 sig["or_lf_decode_batch" + sfx] = (None, [vp, dp, i32, i32, i32, i32, dp, dp, dp, dp, dp, i32])
                 sig["or_lf_decode_batch_ex" + sfx] = (None, [vp, dp, i32, i32, i32, i32, i32, dp, dp, dp, dp, dp, dp,
-                                                               dp, i32])
+                                                               dp, i32, i32])
+                sig["or_lf_store_half" + sfx] = (None, [ctypes.c_size_t, dp, dp])
                 sig["or_lf_symbol_posterior" + sfx] = (None, [vp, dp, dp, dp, dp, dp, dp])
                 sig["or_lf_init_pmf" + sfx] = (None, [vp, dp, dp, dp])
                 sig["or_ls_init" + sfx] = (None, [vp, dp, dp])
@@ -237,6 +239,11 @@ def boxplus(s1, l1, s2, l2):
     return so, lo
 
 
+def round_half(v: float) -> float:
+    """IEEE binary16 rounding (the oracle's own, written from the format's definition)."""
+    return float(_lib().or_round_half(float(v)))
+
+
 def channel_prior(llr) -> np.ndarray:
     llr = _f64(llr)
     out = np.zeros(1 << llr.size)
@@ -369,7 +376,7 @@ class Code:
         getattr(self._L, "or_lf_symbol_posterior" + sfx)(self._h, _p(S0), _p(L0), _p(Ws), _p(Wl), _p(post), _p(xmap))
         return post, xmap
 
-    def _decode_batch(self, inp, is_pmf, max_iters, mode, early_stop, want_soft, want_post, nthreads, f32):
+    def _decode_batch(self, inp, is_pmf, max_iters, mode, early_stop, want_soft, want_post, nthreads, f32, half=False):
         dt, sfx = self._real(f32)
         row = self.N * (self.q if is_pmf else self.m)
         inp = np.ascontiguousarray(inp, np.float32).reshape(-1, row)
@@ -385,7 +392,7 @@ class Code:
         opt = lambda a: _p(a) if a is not None else None  # noqa: E731
         getattr(self._L, "or_lf_decode_batch_ex" + sfx)(
             self._h, _p(inp), int(bool(is_pmf)), F, int(max_iters), int(mode), int(bool(early_stop)), _p(x), _p(ok),
-            _p(it), opt(soft), _p(ev), opt(post), opt(xmap), int(nt),
+            _p(it), opt(soft), _p(ev), opt(post), opt(xmap), int(bool(half)), int(nt),
         )
         out = {"hard": x.astype(np.uint8), "ok": ok.astype(np.uint8), "iters": it, "events": ev}
         if soft is not None:
@@ -448,10 +455,21 @@ class Code:
 
     def lf_decode_batch(self, llr, max_iters: int, mode: int = EXACT, early_stop: bool = True,
                         want_soft: bool = False, nthreads: int | None = None, f32: bool = False,
-                        want_post: bool = False):
+                        want_post: bool = False, half: bool = False):
         """Decode F frames (llr float32 [F][N*m]); returns dict of numpy arrays (hard, ok, iters,
-        events; soft [F][N*m]; post [F][N][q] and map [F][N] at the stopping iteration)."""
-        return self._decode_batch(llr, False, max_iters, mode, early_stop, want_soft, want_post, nthreads, f32)
+        events; soft [F][N*m]; post [F][N][q] and map [F][N] at the stopping iteration).
+        half=True: O-LF-half, the stored messages rounded to the half-precision format after every
+        check node (lf_store_half; reading R26)."""
+        return self._decode_batch(llr, False, max_iters, mode, early_stop, want_soft, want_post, nthreads, f32, half)
+
+    def lf_store_half(self, Ws, Wl, f32=False):
+        """The O-LF-half storage rule applied to a message array (sign, ln): -log2|x| rounded to IEEE
+        binary16.  Returns new arrays."""
+        dt, sfx = self._real(f32)
+        s = np.ascontiguousarray(Ws, np.uint8).copy()
+        l = np.ascontiguousarray(Wl, dt).copy()
+        getattr(self._L, "or_lf_store_half" + sfx)(l.size, _p(s), _p(l))
+        return s, l
 
     def lf_decode_batch_pmf(self, pmf, max_iters: int, mode: int = EXACT, early_stop: bool = True,
                             nthreads: int | None = None, f32: bool = False, want_soft: bool = False,

@@ -442,6 +442,28 @@ void or_sp_posterior(const or_code* c, const double* p0, const double* w, double
 }
 
 /* ------------------------------------------------------------------ */
+/* IEEE 754 binary16 rounding, written out from the format's           */
+/* definition: 1 sign bit, 5 exponent bits (bias 15), 10 fraction bits; */
+/* normal numbers 2^-14 .. 65504, subnormals with the quantum 2^-24;   */
+/* round to nearest, ties to even; overflow to infinity.  It is the    */
+/* storage rule of the half-precision message format (O-LF-half,       */
+/* SURVEY 8(f) row 4, the quantisation motivation of PAPER.md:57-71;   */
+/* reading R26): not part of the paper's arithmetic.                   */
+/* ------------------------------------------------------------------ */
+double or_round_half(double v) {
+  if (v != v || v == 0.0 || isinf(v)) return v;
+  double a = fabs(v);
+  int e;
+  frexp(a, &e);          /* a = f 2^e, f in [0.5, 1): the leading bit weighs 2^(e-1) */
+  int lead = e - 1;
+  if (lead < -14) lead = -14;             /* subnormals: all share the quantum 2^-24 */
+  double quantum = ldexp(1.0, lead - 10); /* 10 fraction bits below the leading bit */
+  double r = nearbyint(a / quantum) * quantum; /* default rounding mode: ties to even */
+  if (r > 65504.0) r = INFINITY;
+  return v < 0 ? -r : r;
+}
+
+/* ------------------------------------------------------------------ */
 /* O-LF: the paper's Log-Fourier SP, double and a   */
 /* float32 diagnostic twin generated from lf_body.inc.                 */
 /* ------------------------------------------------------------------ */
