@@ -80,6 +80,7 @@ def _lib():
                 "or_gamma_inv": (ctypes.c_double, [i32, ctypes.c_double]),
                 "or_channel_prior": (None, [i32, dp, dp]),
                 "or_round_half": (ctypes.c_double, [ctypes.c_double]),
+                "or_round_half_mode": (ctypes.c_double, [ctypes.c_double, i32]),
                 "or_code_new": (vp, [vp, i32, i32, i32, dp, dp, dp]),
                 "or_code_free": (None, [vp]),
                 "or_code_E": (i32, [vp]),
@@ -239,9 +240,10 @@ def boxplus(s1, l1, s2, l2):
     return so, lo
 
 
-def round_half(v: float) -> float:
-    """IEEE binary16 rounding (the oracle's own, written from the format's definition)."""
-    return float(_lib().or_round_half(float(v)))
+def round_half(v: float, toward_zero: bool = False) -> float:
+    """IEEE binary16 rounding (the oracle's own, written from the format's definition): to nearest
+    (ties to even), or toward zero."""
+    return float(_lib().or_round_half_mode(float(v), 2 if toward_zero else 1))
 
 
 def channel_prior(llr) -> np.ndarray:
@@ -392,7 +394,7 @@ class Code:
         opt = lambda a: _p(a) if a is not None else None  # noqa: E731
         getattr(self._L, "or_lf_decode_batch_ex" + sfx)(
             self._h, _p(inp), int(bool(is_pmf)), F, int(max_iters), int(mode), int(bool(early_stop)), _p(x), _p(ok),
-            _p(it), opt(soft), _p(ev), opt(post), opt(xmap), int(bool(half)), int(nt),
+            _p(it), opt(soft), _p(ev), opt(post), opt(xmap), (2 if half == "rz" else int(bool(half))), int(nt),
         )
         out = {"hard": x.astype(np.uint8), "ok": ok.astype(np.uint8), "iters": it, "events": ev}
         if soft is not None:
@@ -459,7 +461,8 @@ class Code:
         """Decode F frames (llr float32 [F][N*m]); returns dict of numpy arrays (hard, ok, iters,
         events; soft [F][N*m]; post [F][N][q] and map [F][N] at the stopping iteration).
         half=True: O-LF-half, the stored messages rounded to the half-precision format after every
-        check node (lf_store_half; reading R26)."""
+        check node (lf_store_half; reading R26); half="rz": the same store rounding toward zero (a
+        diagnostic second rounding of the format, for the stable-frame classification of the F16 path)."""
         return self._decode_batch(llr, False, max_iters, mode, early_stop, want_soft, want_post, nthreads, f32, half)
 
     def lf_store_half(self, Ws, Wl, f32=False):

@@ -450,7 +450,10 @@ void or_sp_posterior(const or_code* c, const double* p0, const double* w, double
 /* SURVEY 8(f) row 4, the quantisation motivation of PAPER.md:57-71;   */
 /* reading R26): not part of the paper's arithmetic.                   */
 /* ------------------------------------------------------------------ */
-double or_round_half(double v) {
+/* mode 1: round to nearest, ties to even (the format's default rounding, the storage rule); mode 2:
+ * round toward zero -- used only as a second, equally valid rounding of the same format, to tell
+ * frames whose outcome depends on how stored values round (tests/test_gpu_f16.py) */
+double or_round_half_mode(double v, int mode) {
   if (v != v || v == 0.0 || isinf(v)) return v;
   double a = fabs(v);
   int e;
@@ -458,10 +461,11 @@ double or_round_half(double v) {
   int lead = e - 1;
   if (lead < -14) lead = -14;             /* subnormals: all share the quantum 2^-24 */
   double quantum = ldexp(1.0, lead - 10); /* 10 fraction bits below the leading bit */
-  double r = nearbyint(a / quantum) * quantum; /* default rounding mode: ties to even */
-  if (r > 65504.0) r = INFINITY;
+  double r = (mode == 2 ? floor(a / quantum) : nearbyint(a / quantum)) * quantum; /* nearbyint: ties to even */
+  if (r > 65504.0) r = mode == 2 ? 65504.0 : INFINITY;
   return v < 0 ? -r : r;
 }
+double or_round_half(double v) { return or_round_half_mode(v, 1); }
 
 /* ------------------------------------------------------------------ */
 /* O-LF: the paper's Log-Fourier SP, double and a   */

@@ -31,6 +31,18 @@ def test_round_half_matches_ieee_binary16():
     assert np.array_equal(got, want), vals[got != want][:5]
 
 
+def test_round_half_toward_zero():
+    """The diagnostic second rounding: the largest binary16 value not above |v| in magnitude."""
+    rng = np.random.default_rng(8)
+    vals = np.exp2(rng.uniform(-26, 16, 5000))
+    for v in vals:
+        r = oracle.round_half(v, toward_zero=True)
+        assert r <= v and float(np.float16(r)) == r  # representable, not above
+        up = float(np.nextafter(np.float16(r), np.float16(np.inf)))
+        assert up > v or up == r  # the next binary16 value is above v
+        assert oracle.round_half(-v, toward_zero=True) == -r
+
+
 def test_store_half_is_the_rounding_rule_entrywise():
     """On messages the oracle's check node produces (C2 and a GF(256) code), lf_store_half writes
     ln' = -ln 2 * fp16(-ln / ln 2) with the sign kept, and leaves zeros (the floor) alone."""
