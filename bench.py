@@ -3,14 +3,19 @@
 
 A "step" is one nbldpc_decode of the whole batch: every frame of the workload runs
 the full hot path (channel spectrum, variable node, tentative decision, check node,
-syndrome, early termination) until it stops.  Workload at N=1: BASELINE.json
-configs[1] (C2: GF(64), (2,4)-regular, N=1024, 4096 all-zero-codeword frames,
-BPSK/AWGN Eb/N0 = 1.0 dB, 50 iterations with early stop), synthetic seeded inputs.
+syndrome, early termination) until it stops.  Workload (default): BASELINE.json
+configs[3], the configuration the metric "(1/2/4/8 B200)" is quoted on -- C4: GF(256),
+(2,16)-regular, N=2048, a global batch of 16,384 all-zero-codeword frames, BPSK/AWGN
+Eb/N0 = 3.5 dB, 30 iterations with early stop; synthetic seeded inputs.  --config picks
+another BASELINE config (C1..C5), --point a C5 Eb/N0 point.
 
 metric = sum_f K_bits * iters_used_f / T  (decoded info bits per second per iteration),
-K_bits = N m (1 - 2/k).  Multi-GPU (torchrun): weak scaling, each rank decodes its own
-4096-frame shard (global frame indices rank*F ..), NCCL only for the final counter /
-timing reductions.  L2 is flushed (256 MiB write) before every timed step.
+K_bits = N m (1 - 2/k).  Multi-GPU (torchrun): strong scaling by default -- the config's
+fixed global batch in chunk-aligned contiguous shards (shard.frame_range); --scaling weak
+gives every rank F frames.  No collective in the loop; one NCCL all-reduce of the counter
+vector (frames, converged, frame / symbol / bit errors against the sent codeword,
+undetected errors, iterations, numerical events) and one MAX of the device times after
+it.  L2 is flushed (256 MiB write) before every timed step.
 
 --impl reference times the CPU oracle (oracle/, fp64, OpenMP over frames) on a bounded
 sample of the same workload; it is the base contract's reference arm for this tier.
@@ -67,7 +72,10 @@ def per_frame_iter(cfg, vn, inp="llr", symbol_out=False, algorithm="lf", msg="f3
         # backward), each input exponentiated twice and each output's log once; messages + lambda^0
         Mc = E // cfg["k"]
         return 3 * E * q, Mc * 3 * (cfg["k"] - 2) * q * q, 2 * E * q * 4 + 4 * N * q + N
-    mufu = 2 * E * q + N * q                        # ex2 of every VN input entry, lg2 of every output, ex2 of W_a
+    # SFU ops: the packed-log format (f16 messages) takes an ex2 of every VN input entry, an lg2 of every
+    # output and an ex2 of every W_a entry of the decision; the f32 hot path stores linear messages
+    # at q >= 128 and needs one reciprocal per edge (the normalisation) only
+    mufu = (2 * E * q + N * q) if (msg == "f16" or cfg["m"] < 7) else E
     if inp == "pmf":  # probability-domain VN: 2 WHTs (m q add/sub each) and a product per entry
         fma = E * q * (2 * m + 1) + N * (m + 1) * q
     else:             # VN (separable / direct) + decision points
@@ -174,23 +182,37 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_oracle_run(cfg, point, frame0, nframes, threads=None, inp="llr", ebn0=None, symbol_out=False, algorithm="lf"):
-    """Times the oracle (as it stands) on frames frame0.. of the workload; returns (value, seconds, iters)."""
+# oracle cost is ~E q^2 exponentials per frame-iteration: cap the iterations of the CPU samples of the
+# GF(256) configs so that a sample stays within seconds (measured: C4 4.9 s, C3 1.4 s, C2 0.2 s, C5 0.08 s
+# per frame-iteration per core); the metric counts the iterations actually run
+ORACLE_ITER_CAP = {"C3": 2, "C4": 1}
+
+
+def cpu_oracle_run(cfg, point, frame0, nframes, threads=None, inp="llr", ebn0=None, symbol_out=False, algorithm="lf",
+                   max_iters=None):
+    """Times the oracle (as it stands) on frames frame0.. of the workload; returns (value, seconds, iters, threads)."""
     import oracle
 
     M, rows, cols, coeffs = synth.config_code(cfg["name"])
     code = oracle.Code(oracle.Field(cfg["m"], cfg["poly"]), M, cfg["N"], rows, cols, coeffs)
     x = channel_input(cfg, inp, point, ebn0, frame0, nframes)
     nt = threads or os.cpu_count() or 1
+    iters = max_iters or cfg["max_iters"]
     t0 = time.perf_counter()
     if algorithm == "logsp":
-        r = code.ls_decode_batch(x, cfg["max_iters"], pmf=inp == "pmf", nthreads=nt)
+        r = code.ls_decode_batch(x, iters, pmf=inp == "pmf", nthreads=nt)
     else:
         dec = code.lf_decode_batch_pmf if inp == "pmf" else code.lf_decode_batch
-        r = dec(x, cfg["max_iters"], nthreads=nt, want_post=symbol_out)
+        r = dec(x, iters, nthreads=nt, want_post=symbol_out)
     dt = time.perf_counter() - t0
     it = int(r["iters"].sum())
     return info_bits(cfg) * it / dt, dt, it, nt
+
+
+def oracle_sample(cfg, nframes, iters_cap):
+    cap = min(cfg["max_iters"], iters_cap or ORACLE_ITER_CAP.get(cfg["name"], cfg["max_iters"]))
+    return cap, (f"{nframes} frames of the workload, at most {cap} of its {cfg['max_iters']} iterations each"
+                 + (" (the fp64 oracle costs seconds per frame-iteration here)" if cap < cfg["max_iters"] else ""))
 
 
 def run_reference(args, cfg):
@@ -198,10 +220,13 @@ def run_reference(args, cfg):
     if rank != 0:
         return 0
     vals, dts = [], []
-    nframes = args.ref_frames
+    cores = os.cpu_count() or 1
+    nframes = args.ref_frames or min(32, max(8, cores))
+    cap, sample = oracle_sample(cfg, nframes, args.ref_iters)
+    nt = cores
     for i in range(args.warmup + args.steps):
         v, dt, it, nt = cpu_oracle_run(cfg, args.point, i * nframes, nframes, inp=args.input, ebn0=args.ebn0,
-                                       symbol_out=args.symbol_out, algorithm=args.algorithm)
+                                       symbol_out=args.symbol_out, algorithm=args.algorithm, max_iters=cap)
         if i >= args.warmup:
             vals.append(v)
             dts.append(dt)
@@ -210,11 +235,11 @@ def run_reference(args, cfg):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(dts) / len(dts),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(cfg, args.point, args.input, args.ebn0), "frames_per_step": nframes,
-                   "sample": f"{nframes} frames per step (frames i*{nframes}.. of the seeded stream)"},
+                   "sample": f"each step: {sample} (frames i*{nframes}.. of the seeded stream)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nt, "kind": "oracle",
-                         "sample": f"{nframes} frames per step x {args.steps} steps, fp64 C oracle, OpenMP"},
+                         "sample": f"{sample}, x {args.steps} steps, fp64 C oracle, OpenMP over frames"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -227,9 +252,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4",
+                    help="BASELINE.json config (default C4, the 1/2/4/8-GPU configuration the metric is quoted on)")
     ap.add_argument("--point", type=int, default=0)
-    ap.add_argument("--frames", type=int, default=0, help="frames per rank (default: the config's)")
+    ap.add_argument("--frames", type=int, default=0,
+                    help="strong scaling: the global batch (default: the config's); weak: frames per rank")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's fixed global batch split over the ranks (default); weak: F per rank")
     ap.add_argument("--slots", type=int, default=0)
     ap.add_argument("--graph", type=int, default=0, help="direct path only: 0 graph, -1 host loop")
     ap.add_argument("--vn", type=int, default=0,
@@ -242,8 +271,9 @@ def main():
                     help="lf: Log-Fourier SP (the hot path); logsp: the conventional Log-SP it is compared with")
     ap.add_argument("--msg", default="f32", choices=["f32", "f16"],
                     help="message storage: f32 (default) or f16 (half the message bytes; evaluated by FER)")
-    ap.add_argument("--ref-frames", type=int, default=32)
-    ap.add_argument("--cpu-frames", type=int, default=64)
+    ap.add_argument("--ref-frames", type=int, default=0, help="reference arm: frames per step (default: cores)")
+    ap.add_argument("--ref-iters", type=int, default=0, help="reference arm: iteration cap (default per config)")
+    ap.add_argument("--cpu-frames", type=int, default=0, help="cpu_baseline sample frames (default: cores)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--traffic", default=os.path.join(ROOT, "profiles", "traffic.json"))
@@ -269,19 +299,25 @@ def main():
 
     import paper_1008_4370_b200 as nb
 
-    F = args.frames or cfg["frames"]
-    f0, f1 = shard.frame_range(rank, world, F)
+    Fcfg = args.frames or cfg["frames"]
+    f0, f1 = shard.frame_range(rank, world, Fcfg, args.scaling)
+    F = f1 - f0
+    if F < 1:
+        raise SystemExit(f"rank {rank}: empty shard of {Fcfg} frames over {world} ranks")
+    global_frames = Fcfg if args.scaling == "strong" else Fcfg * world
     M, rows, cols, coeffs = synth.config_code(cfg["name"])
     code = nb.Code(cfg["m"], cfg["poly"], M, cfg["N"], rows, cols, coeffs)
     pmf_in = args.input == "pmf"
     vn = 1 if (args.symbol_out and pmf_in) else args.vn  # pmf + symbol outputs run the slot-pass kernel
-    llr_np = channel_input(cfg, args.input, args.point, args.ebn0, f0, f1 - f0)
+    llr_np = channel_input(cfg, args.input, args.point, args.ebn0, f0, F)
     llr_host = torch.from_numpy(llr_np).pin_memory()
     llr = llr_host.to(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
+    logsp = args.algorithm == "logsp"
     kw = dict(slots=args.slots, use_graph=args.graph, want_post=args.symbol_out, vn_algorithm=vn,
-              algorithm=1 if args.algorithm == "logsp" else 0, message_format=1 if args.msg == "f16" else 0)
+              algorithm=1 if logsp else 0, message_format=1 if args.msg == "f16" else 0,
+              want_events=not logsp)
     decode = code.decode_pmf if pmf_in else code.decode
 
     def barrier():
@@ -297,7 +333,8 @@ def main():
     clocks = ClockSampler(local)
     clocks.start()
     barrier()
-    step_ms, iters_sum, launches, ok_sum = [], 0, 0, 0
+    step_ms, launches = [], 0
+    cnt = {k: 0 for k in shard.COUNTERS}
     for _ in range(args.steps):
         flush.fill_(1)  # L2 flush (untimed)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -306,14 +343,19 @@ def main():
         e1.record(stream)
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
-        iters_sum += int(out["iters"].sum().item())
-        ok_sum += int(out["ok"].sum().item())
+        # outside the timed region: counters against the sent (all-zero) codeword
+        for k, v in shard.error_counts(out["hard"], out["ok"], None, out.get("events")).items():
+            cnt[k] += v
+        cnt["frame_iters"] += int(out["iters"].to(torch.int64).sum().item())
         launches += code.last_decode_launches()
     barrier()
     clk = clocks.stop()
+    cnt["launches"] = launches
+    my_iters = cnt["frame_iters"]
 
     # end to end through the host-buffer C-ABI entry (H2D + decode + D2H inside the timed region)
     e2e_ms, e2e_iters, d2h = 0.0, 0, F * cfg["N"] + F + 4 * F
+    hkw = {k: v for k, v in kw.items() if k not in ("want_post", "want_events")}
     if not args.no_e2e and pmf_in and not args.symbol_out:
         # through the host-buffer C-ABI entry (pinned pmfs -> device -> decode -> host outputs, all timed)
         hkw = dict(slots=args.slots, vn_algorithm=vn, algorithm=kw["algorithm"])
@@ -348,22 +390,20 @@ def main():
                 e2e_iters += int(host_out["iters"].sum())
         barrier()
     elif not args.no_e2e:
-        kw.pop("want_post")
-        code.decode_host(llr_host, cfg["max_iters"], **kw)
+        code.decode_host(llr_host, cfg["max_iters"], **hkw)
         barrier()
         for _ in range(args.steps):
             flush.fill_(1)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            hout = code.decode_host(llr_host, cfg["max_iters"], **kw)
+            hout = code.decode_host(llr_host, cfg["max_iters"], **hkw)
             e2e_ms += 1e3 * (time.perf_counter() - t0)
             e2e_iters += int(hout["iters"].sum())
         barrier()
+    cnt["e2e_frame_iters"] = e2e_iters
 
-    cnt, tim = shard.reduce_stats(
-        {"frame_iters": iters_sum, "ok": ok_sum, "frames": F * args.steps, "launches": launches,
-         "e2e_frame_iters": e2e_iters},
-        {"ms": sum(step_ms), "e2e_ms": e2e_ms}, dist, device=dev)
+    # ONE all-reduce of the counter vector (SUM) and one of the device times (MAX) -- SURVEY.md 8(e)
+    cnt, tim = shard.reduce_stats(cnt, {"ms": sum(step_ms), "e2e_ms": e2e_ms}, dist, device=dev)
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -374,46 +414,56 @@ def main():
     if os.path.exists(args.traffic):
         try:
             key = (f"{cfg['name']}:vn{vn}" + (":pmf" if pmf_in else "") + (":sym" if args.symbol_out else "")
-                   + (":f16" if args.msg == "f16" else "") + (":logsp" if args.algorithm == "logsp" else ""))
+                   + (":f16" if args.msg == "f16" else "") + (":logsp" if logsp else ""))
             traffic = json.load(open(args.traffic)).get(key)
         except (OSError, ValueError):
             traffic = None
     # this rank's kernel: its frame-iterations over its own device time
-    roof = roofline(cfg, vn, iters_sum, sum(step_ms) * 1e-3, traffic, args.input, args.symbol_out, args.algorithm,
+    roof = roofline(cfg, vn, my_iters, sum(step_ms) * 1e-3, traffic, args.input, args.symbol_out, args.algorithm,
                     args.msg)
     roof["kernel"] = ("lf_cluster_kernel (one launch per step + a 1-block setup kernel; "
                       "CUDA events around the step)") if vn == 0 else "nb_pass_kernel (slot passes)"
-    if args.algorithm == "logsp":
+    if logsp:
         roof["kernel"] = "ls_frame_kernel (conventional Log-SP, one CTA per frame; one launch per step)"
     elif vn == 2 or cfg["j"] != 2:
         roof["kernel"] = "lfg_frame_kernel (general column weight, one CTA per frame; one launch per step)"
+    nfr = cnt["frames"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": warm, "ms_per_step": tim["ms"] / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_name(cfg, args.point, args.input, args.ebn0), "frames_per_gpu": F,
-                   "global_frames": F * world, "N": cfg["N"], "q": cfg["q"], "k": cfg["k"],
+                   "global_frames": global_frames, "N": cfg["N"], "q": cfg["q"], "k": cfg["k"],
                    "max_iters": cfg["max_iters"], "vn_algorithm": ["separable", "direct", "general"][vn],
                    "column_weight": cfg["j"],
                    "input": args.input, "symbol_outputs": bool(args.symbol_out), "algorithm": args.algorithm,
                    "messages": args.msg,
-                   "parallelism": f"frames sharded over {world} GPU(s), no collective in the loop",
+                   "parallelism": (f"{args.scaling} scaling: {global_frames} frames in chunk-aligned contiguous "
+                                   f"shards over {world} GPU(s), no collective in the loop, one NCCL all-reduce "
+                                   f"of the counter vector after it"),
                    "l2": "flushed (256 MiB write) before every timed step",
-                   "slots": args.slots or "default", "mean_iters": cnt["frame_iters"] / cnt["frames"],
-                   "frame_error_rate": 1.0 - cnt["ok"] / cnt["frames"]},
+                   "slots": args.slots or "default", "mean_iters": cnt["frame_iters"] / nfr,
+                   "codeword": "all-zero (sent codeword for the error counts)",
+                   "frame_error_rate": cnt["frame_err"] / nfr,
+                   "symbol_error_rate": cnt["sym_err"] / (nfr * cfg["N"]),
+                   "bit_error_rate": cnt["bit_err"] / (nfr * cfg["N"] * cfg["m"]),
+                   "undetected_frames": cnt["undetected"], "syndrome_fail_rate": 1.0 - cnt["ok"] / nfr,
+                   "numeric_events": cnt["events"], "frames_decoded": nfr},
         "roofline": roof,
         "gpu_launches": int(cnt["launches"]),
         "clocks": clk,
     }
     if not args.no_e2e:
         line["e2e"] = {"value": info_bits(cfg) * cnt["e2e_frame_iters"] / (tim["e2e_ms"] * 1e-3), "unit": UNIT,
-                       "h2d_bytes_per_step": int(llr_np.nbytes), "d2h_bytes_per_step": int(d2h)}
+                       "h2d_bytes_per_step": int(llr_np.nbytes) * world, "d2h_bytes_per_step": int(d2h) * world}
     if not args.no_cpu_baseline and world == 1:
-        v, dt, it, nt = cpu_oracle_run(cfg, args.point, 0, args.cpu_frames, inp=args.input, ebn0=args.ebn0,
-                                       symbol_out=args.symbol_out, algorithm=args.algorithm)
+        n = args.cpu_frames or (os.cpu_count() or 1)
+        cap, sample = oracle_sample(cfg, n, 0 if cfg["name"] != "C4" else 2)
+        v, dt, it, nt = cpu_oracle_run(cfg, args.point, 0, n, inp=args.input, ebn0=args.ebn0,
+                                       symbol_out=args.symbol_out, algorithm=args.algorithm, max_iters=cap)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": nt, "kind": "oracle",
-                                "sample": f"first {args.cpu_frames} frames of the workload, {it} frame-iterations, "
-                                          f"{dt:.1f} s, fp64 C oracle with OpenMP over frames"}
+                                "sample": f"first {sample}: {it} frame-iterations, {dt:.1f} s, fp64 C oracle with "
+                                          f"OpenMP over frames"}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -104,12 +104,24 @@ typedef struct {
                                stopping iteration */
   uint8_t* symbol_map_out;  /* device, [frames][N] or NULL: argmax_x mu_v(x), ties -> lowest x
                                (the paper's symbol-level TENTATIVE DECISION) */
-  /* Either symbol output selects the direct kernel (NBLDPC_VN_DIRECT): the symbol decision is
-   * evaluated at every iteration (the stopping one is not known in advance; 2 WHTs of size 2^m per
-   * variable) and written to the frame's output rows each time, so the last write is the
-   * stopping iteration's.  The output rows hold intermediate values until the decode completes. */
+  /* The symbol decision is evaluated at every iteration (the stopping one is not known in advance;
+   * 2 WHTs of size 2^m per variable) and written to the frame's output rows each time, so the last
+   * write is the stopping iteration's; the rows hold intermediate values until the decode completes.
+   * With LLR input it runs inside the cluster kernel (its symbol-output variant, NBLDPC_VN_SEPARABLE);
+   * with symbol-pmf input (nbldpc_decode_pmf) it selects the slot-pass kernel (NBLDPC_VN_DIRECT). */
   int algorithm;     /* nbldpc_algorithm_t, default NBLDPC_ALG_LOG_FOURIER */
   int message_format; /* nbldpc_message_format_t, default NBLDPC_MSG_F32 */
+  /* --- since round 2 (callers built against the older, shorter struct keep working: fields past
+   *     their struct_size read as zero) --- */
+  void* workspace;        /* DEVICE, 256-byte aligned, or NULL (default: the handle's own workspace).
+                             Caller-provided workspace of at least nbldpc_workspace_bytes(code, frames)
+                             bytes for nbldpc_decode_ex with LLR input on the cluster kernel
+                             (NBLDPC_VN_SEPARABLE, column weight 2); other entry points / paths return
+                             NBLDPC_ERR_UNSUPPORTED.  The caller owns it; it must not be used by another
+                             decode until this one completes on `stream`.  A decode with its own
+                             workspace writes nothing of the handle and takes no handle lock, so decodes
+                             with distinct workspaces may run concurrently on distinct streams. */
+  size_t workspace_bytes; /* size of `workspace` (NBLDPC_ERR_INVALID_ARGUMENT if too small) */
 } nbldpc_decode_opts_t;
 
 /* Builds a code from H given as nnz (row, col, coefficient) triplets in any order.
@@ -118,17 +130,26 @@ typedef struct {
  *   M, N      : H is M x N
  *   rows, cols, coeffs : HOST arrays of length nnz, 0-based indices, coefficients in [1, 2^m-1]
  *   out       : receives the handle (caller owns it; release with nbldpc_destroy)
- * Every column must have 1..16 nonzeros in distinct rows and every row at least two.  Column weight 2
+ * Every column must have 1..16 nonzeros in distinct rows and every row at least two; row degree times
+ * max(1, 2^m/16) must not exceed 512 (one check per thread block).  Column weight 2
  * everywhere (the (2,k) codes of PAPER.md:36-41) runs the Log-Fourier cluster kernel; any other column
  * weight ("the extension ... is straightforward") runs NBLDPC_VN_GENERAL, for which
  * nbldpc_step and NBLDPC_ALG_LOG_SP are unavailable (NBLDPC_ERR_UNSUPPORTED).  The handle copies H, builds its device tables (GF tables, canonical edge list,
  * Fourier permutation bases) on the CUDA device current at the call, and is
- * immutable afterwards.  Decoding must happen on that device. */
+ * immutable afterwards.  Decoding must happen on that device.
+ * Length: each CTA of the cluster kernel keeps 8-byte records of its share of the edge slots in shared
+ * memory; long codes get larger clusters (up to 16 CTAs per frame).  A code whose share still exceeds
+ * the 227 KB of shared memory (about E * 2^m > 16 * 227 KB * 2^m / 8 bytes of edge records, i.e. tens
+ * of thousands of symbols) is accepted and decoded by the general-column-weight kernel (same results
+ * up to rounding); nbldpc_step with NBLDPC_VN_SEPARABLE, NBLDPC_MSG_F16 and caller workspaces are then
+ * NBLDPC_ERR_UNSUPPORTED.  Edge slots must fit 22 bits (M * kpad < 2^22, kpad = the next power of two
+ * >= max(4, largest row degree)). */
 nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int nnz, const int32_t* rows,
                                    const int32_t* cols, const uint16_t* coeffs, nbldpc_code_t* out);
 
-/* Releases the handle and everything it allocated.  NULL is a no-op.  The caller must make sure no
- * decode using the handle is still running (synchronise the streams first). */
+/* Releases the handle and everything it allocated.  NULL is a no-op.  Waits (host side) for the last
+ * decode that used the handle's own workspace to complete before releasing it; decodes that ran with a
+ * caller-provided workspace must have completed (synchronise their streams first). */
 void nbldpc_destroy(nbldpc_code_t code);
 
 /* Human-readable text of a status (static storage). */
@@ -146,10 +167,13 @@ nbldpc_status_t nbldpc_code_info(nbldpc_code_t code, int* m, int* M, int* N, int
 size_t nbldpc_slot_bytes(nbldpc_code_t code);
 
 /* Device bytes of the workspace a default nbldpc_decode of `frames` frames keeps on this handle
- * (the resident slots times nbldpc_slot_bytes, plus the per-call control block); 0 for a NULL code,
- * frames < 1, or a code with a column weight other than 2 (its general kernel sizes a workspace per
- * call from the occupancy).  The workspace is allocated by the first decode and reused while it is large
- * enough; it is released by nbldpc_destroy. */
+ * (min(frames, resident clusters) slots of about nbldpc_slot_bytes each, plus the per-call control
+ * block) -- also the size a caller-provided nbldpc_decode_opts_t::workspace needs; 0 for a NULL code,
+ * frames < 1, or a code the cluster kernel does not run (column weight other than 2, or too long, see
+ * nbldpc_code_create: the general kernel sizes a workspace per call from the occupancy).  The handle's
+ * workspace is allocated by the first decode and re-carved when the slot count changes, stream-ordered
+ * on the decode's stream (cudaFreeAsync / cudaMallocAsync after the handle's previous decode, wherever
+ * it ran -- no device-wide synchronisation); it is released by nbldpc_destroy. */
 size_t nbldpc_workspace_bytes(nbldpc_code_t code, int frames);
 
 /* Number of kernels the most recent decode on this handle launched (setup, pass and control
@@ -166,7 +190,9 @@ nbldpc_status_t nbldpc_last_decode_launches(nbldpc_code_t code, long long* launc
  *   stream       : cudaStream_t (NULL = legacy default stream)
  * Stream-ordered: returns after enqueueing; outputs are valid when `stream` reaches that point.
  * Results depend only on (code, llr row, max_iters, options), not on frames, batching or slots.
- * Calls sharing one handle must be ordered on one stream (they share the handle's workspace). */
+ * Calls sharing one handle's workspace are serialised by a lock and by stream order (a decode whose
+ * slot count differs re-carves the workspace after the previous one completes, stream-ordered); give
+ * each concurrent stream its own nbldpc_decode_opts_t::workspace to overlap decodes of one handle. */
 nbldpc_status_t nbldpc_decode(nbldpc_code_t code, const float* llr, int frames, int max_iters,
                               uint8_t* hard_symbols, uint8_t* syndrome_ok, int32_t* iters_used, void* stream);
 
@@ -227,6 +253,13 @@ nbldpc_status_t nbldpc_decode_pmf_host(nbldpc_code_t code, const float* pmf_host
  * nbldpc_decode.  Stream-ordered. */
 nbldpc_status_t nbldpc_step(nbldpc_code_t code, const float* llr, int frames, int iter, const float* w_in,
                             float* w_out, float* u_out, uint8_t* hard, float* soft, int vn_algorithm, void* stream);
+
+/* nbldpc_step for symbol-pmf input (the Log-Fourier cluster kernel's pmf variant, NBLDPC_VN_SEPARABLE):
+ * pmf as for nbldpc_decode_pmf (DEVICE, float32 [frames][N][2^m], 16-byte aligned, rows scaled to
+ * probabilities); the other arguments as nbldpc_step.  Same code requirements;
+ * NBLDPC_ERR_UNSUPPORTED where the cluster kernel does not run the code. */
+nbldpc_status_t nbldpc_step_pmf(nbldpc_code_t code, const float* pmf, int frames, int iter, const float* w_in,
+                                float* w_out, float* u_out, uint8_t* hard, float* soft, void* stream);
 
 #ifdef __cplusplus
 }

@@ -42,7 +42,8 @@ class _Opts(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_size_t), ("syndrome_mode", ctypes.c_int), ("no_early_stop", ctypes.c_int),
                 ("soft_out", ctypes.c_void_p), ("events_out", ctypes.c_void_p), ("slots", ctypes.c_int),
                 ("use_graph", ctypes.c_int), ("vn_algorithm", ctypes.c_int), ("symbol_post_out", ctypes.c_void_p),
-                ("symbol_map_out", ctypes.c_void_p), ("algorithm", ctypes.c_int), ("message_format", ctypes.c_int)]
+                ("symbol_map_out", ctypes.c_void_p), ("algorithm", ctypes.c_int), ("message_format", ctypes.c_int),
+                ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t)]
 
 
 def header_symbols() -> list[str]:
@@ -78,6 +79,7 @@ def lib():
         "nbldpc_decode_pmf": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, ctypes.POINTER(_Opts)]),
         "nbldpc_decode_pmf_host": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, ctypes.POINTER(_Opts)]),
         "nbldpc_step": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, i32, vp]),
+        "nbldpc_step_pmf": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -153,7 +155,7 @@ class Code:
         return int(self._L.nbldpc_workspace_bytes(self._h, int(frames)))
 
     def _opts(self, syndrome_mode=0, early_stop=True, soft=None, events=None, slots=0, use_graph=0, vn_algorithm=0,
-              post=None, xmap=None, algorithm=0, message_format=0):
+              post=None, xmap=None, algorithm=0, message_format=0, workspace=None):
         o = _Opts()
         o.struct_size = ctypes.sizeof(_Opts)
         o.syndrome_mode = int(syndrome_mode)
@@ -167,6 +169,9 @@ class Code:
         o.symbol_map_out = _ptr(xmap)
         o.algorithm = int(algorithm)
         o.message_format = int(message_format)
+        if workspace is not None:
+            o.workspace = workspace.data_ptr()
+            o.workspace_bytes = workspace.numel() * workspace.element_size()
         return o
 
     def _outputs(self, F, dev, want_soft, want_events, want_post):
@@ -186,10 +191,11 @@ class Code:
 
     def decode(self, llr, max_iters: int, *, syndrome_mode: int = 0, early_stop: bool = True, want_soft=False,
                want_events=False, want_post=False, slots: int = 0, use_graph: int = 0, vn_algorithm: int = 0, out=None,
-               stream=None, algorithm: int = 0, message_format: int = 0):
+               stream=None, algorithm: int = 0, message_format: int = 0, workspace=None):
         """Decode frames. ``llr``: CUDA float32 tensor [F, N*m].  Returns a dict of CUDA tensors
         (hard uint8 [F,N], ok uint8 [F], iters int32 [F], optional soft float32 [F,N*m], events int32 [F],
-        post float32 [F,N,q] symbol posterior and map uint8 [F,N] symbol-MAP decision)."""
+        post float32 [F,N,q] symbol posterior and map uint8 [F,N] symbol-MAP decision).
+        ``workspace``: optional caller-owned CUDA tensor of >= workspace_bytes(F) bytes (256-byte aligned)."""
         import torch
 
         if not (llr.is_cuda and llr.dtype == torch.float32 and llr.is_contiguous()):
@@ -200,7 +206,7 @@ class Code:
         if out is None:
             out = self._outputs(F, llr.device, want_soft, want_events, want_post)
         o = self._opts(syndrome_mode, early_stop, out.get("soft"), out.get("events"), slots, use_graph, vn_algorithm,
-                       out.get("post"), out.get("map"), algorithm, message_format)
+                       out.get("post"), out.get("map"), algorithm, message_format, workspace)
         st = self._L.nbldpc_decode_ex(self._h, llr.data_ptr(), F, int(max_iters), out["hard"].data_ptr(),
                                       out["ok"].data_ptr(), out["iters"].data_ptr(), _stream(stream),
                                       ctypes.byref(o))
@@ -290,4 +296,19 @@ class Code:
         st = self._L.nbldpc_step(self._h, llr.data_ptr(), F, int(iter_), _ptr(w_in), w_out.data_ptr(), _ptr(u_out),
                                  hard.data_ptr(), _ptr(soft), int(vn_algorithm), _stream(stream))
         _check(st, "nbldpc_step")
+        return {"w": w_out, "u": u_out, "hard": hard, "soft": soft}
+
+    def step_pmf(self, pmf, iter_: int, w_in=None, want_u=False, want_soft=False, stream=None):
+        """nbldpc_step from symbol pmfs [F, N, q] (the cluster kernel's pmf variant; parity tests)."""
+        import torch
+
+        F = pmf.numel() // (self.N * self.q)
+        dev = pmf.device
+        w_out = torch.empty((F, self.E, self.q), dtype=torch.float32, device=dev)
+        u_out = torch.empty_like(w_out) if want_u else None
+        hard = torch.empty((F, self.N), dtype=torch.uint8, device=dev)
+        soft = torch.empty((F, self.N * self.m), dtype=torch.float32, device=dev) if want_soft else None
+        st = self._L.nbldpc_step_pmf(self._h, pmf.data_ptr(), F, int(iter_), _ptr(w_in), w_out.data_ptr(), _ptr(u_out),
+                                     hard.data_ptr(), _ptr(soft), _stream(stream))
+        _check(st, "nbldpc_step_pmf")
         return {"w": w_out, "u": u_out, "hard": hard, "soft": soft}

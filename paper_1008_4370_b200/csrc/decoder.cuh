@@ -135,6 +135,123 @@ __device__ __forceinline__ float pack(float mag, uint32_t sign) {
   return __uint_as_float(__float_as_uint(mag) | (sign & kSign));
 }
 
+// ---- the tentative decision in fp64 (soft outputs, reading R22)
+// M_v(z) = sum_y raw(y) D(z ^ y) at z = 0 and z = alpha^i, raw = P^0 (*) B, computed
+// in fp64 from the stored (packed fp32) spectra B = W_e' and D = W_e of the deciding edge.  The fp32
+// evaluation is accurate enough for the hard bits (their signs) but not for the posterior
+// log-magnitudes ln|M(alpha^i)/M(0)| where P^0 (*) B cancels strongly: the result can be 1e5 times
+// more sensitive than its inputs, so even the fp32 rounding of Gamma^-1 (2^-24 relative) moves it by
+// 5e-3 (measured at GF(256); tools/soft_bar.py).  Hence Gamma^-1 itself is evaluated in fp64 (lin64)
+// and every later operation too.  Used only when soft outputs are requested (decode soft_out,
+// nbldpc_step), never on the plain hot path (a separate kernel instantiation).
+//
+// Gamma^-1 of a packed entry (sign | -log2|x|) in fp64: 2^-mag = 2^-n e^{-g ln 2}, n = floor(mag),
+// g = mag - n (exact), e^y by its Taylor series to degree 17 (|y| < ln 2: truncation < 2e-18).
+__device__ __forceinline__ double lin64(float p) {
+  const float mag = fabsf(p);
+  if (!(mag < 1022.0f)) return 0.0;  // below the normal doubles (the oracle's floor is 2^-1075)
+  const int n = (int)mag;
+  const double y = -((double)mag - (double)n) * 0.6931471805599453094172321;
+  constexpr double c[18] = {1.0, 1.0, 1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120, 1.0 / 720, 1.0 / 5040, 1.0 / 40320,
+                            1.0 / 362880, 1.0 / 3628800, 1.0 / 39916800, 1.0 / 479001600, 1.0 / 6227020800.0,
+                            1.0 / 87178291200.0, 1.0 / 1307674368000.0, 1.0 / 20922789888000.0,
+                            1.0 / 355687428096000.0};
+  double e = c[17];
+#pragma unroll
+  for (int k = 16; k >= 0; --k) e = fma(e, y, c[k]);
+  const double r = e * __hiloint2double((1023 - n) << 20, 0);
+  return (__float_as_uint(p) & 0x80000000u) ? -r : r;
+}
+
+// Layout: phase A -- lane t of a team of TT = 2^(MB-LR) contiguous lanes holds z = R t + r, r < R;
+// bpk / dpk are those R entries of B and D as stored (packed), plin (PMF) the pmf p_v(z).  PMF:
+// raw = WHT(p . WHT(B)) / q (a general symbol pmf), else raw = (x)_i (1, t_i) applied to B (the
+// separable channel spectrum, th[i] = tanh(L_i / 2)).  Returns the team totals md[0..MB] in every lane;
+// lanes of non-deciding teams pass zero spectra.
+template <int MB, int LR, bool PMF>
+__device__ __noinline__ void decision_f64(const float* bpk, const float* dpk, const float* plin, const float* th,
+                                          int t, double* md) {
+  constexpr int R = 1 << LR;
+  constexpr int TT = 1 << (MB - LR);
+  double x[R], d[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    x[r] = lin64(bpk[r]);
+    d[r] = lin64(dpk[r]);
+  }
+  auto wht64 = [&]() {
+#pragma unroll
+    for (int b = 0; b < LR; ++b)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (!(r & (1 << b))) {
+          const double u = x[r], w = x[r | (1 << b)];
+          x[r] = u + w;
+          x[r | (1 << b)] = u - w;
+        }
+#pragma unroll
+    for (int b = LR; b < MB; ++b) {
+      const int off = 1 << (b - LR);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double o = __shfl_xor_sync(0xffffffffu, x[r], off);
+        x[r] = (t & off) ? o - x[r] : x[r] + o;
+      }
+    }
+  };
+  if constexpr (PMF) {
+    wht64();
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r] *= (double)plin[r];
+    wht64();  // q raw: the factor q cancels in every ratio and sign
+  } else {
+#pragma unroll
+    for (int b = 0; b < LR; ++b) {
+      const double tb = (double)th[b];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (!(r & (1 << b))) {
+          const double u = x[r], w = x[r | (1 << b)];
+          x[r] = fma(tb, w, u);
+          x[r | (1 << b)] = fma(tb, u, w);
+        }
+    }
+#pragma unroll
+    for (int b = LR; b < MB; ++b) {
+      const double tb = (double)th[b];
+      const int off = 1 << (b - LR);
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r] = fma(tb, __shfl_xor_sync(0xffffffffu, x[r], off), x[r]);
+    }
+  }
+#pragma unroll
+  for (int b = 0; b <= MB; ++b) md[b] = 0.0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    md[0] = fma(x[r], d[r], md[0]);
+#pragma unroll
+    for (int b = 0; b < LR; ++b) md[b + 1] = fma(x[r], d[r ^ (1 << b)], md[b + 1]);
+  }
+#pragma unroll
+  for (int b = LR; b < MB; ++b) {
+    const int off = 1 << (b - LR);
+#pragma unroll
+    for (int r = 0; r < R; ++r) md[b + 1] = fma(x[r], __shfl_xor_sync(0xffffffffu, d[r], off), md[b + 1]);
+  }
+  if constexpr (TT > 1) {
+#pragma unroll
+    for (int off = TT / 2; off >= 1; off >>= 1)
+#pragma unroll
+      for (int b = 0; b <= MB; ++b) md[b] += __shfl_xor_sync(0xffffffffu, md[b], off);
+  }
+}
+
+// ln|M(alpha^b) / M(0)| from fp64 totals (a ratio below 2^-126 is reported as ln 2^-126)
+__device__ __forceinline__ float soft_ratio(double mb, double m0) {
+  const double r = fabs(mb) / fabs(m0);
+  return __logf((float)fmax(r, 1.1754944e-38));
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
@@ -639,6 +756,19 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
 #pragma unroll
           for (int b = 0; b <= MB; ++b) mv[b] += __shfl_xor_sync(0xffffffffu, mv[b], off);
       }
+      if (want_soft) {
+        // soft outputs: the whole decision in fp64 from the linear spectra (decision_f64, reading R22)
+        float bl[R], dl[R], pl[PMF ? R : 1];
+        const float* Wc = ws.W + ((size_t)(ell & 1) * ws.S + s) * EQ;  // this pass's input messages (packed)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int z = t * R + r;
+          bl[r] = is_a ? __ldcg(Wc + (size_t)ed.partner * Q + z) : 1000.0f;  // 1000: Gamma^-1 = 0
+          dl[r] = is_a ? __ldcg(Wc + (size_t)e * Q + z) : 1000.0f;
+          if constexpr (PMF) pl[r] = is_a ? p0[r] : 0.0f;
+        }
+        decision_f64<MB, LR, PMF>(bl, dl, pl, th, t, mv);
+      }
       const uint32_t s0z = mv[0] < 0.0 ? 1u : 0u;  // sgn_GF2 M(0); an exact zero has sign 0
       if (is_a && t == 0) {
         int x = 0;
@@ -656,10 +786,8 @@ __global__ void __launch_bounds__(MAXB, (MAXB <= 256 ? 2 : 1)) nb_pass_kernel(Pa
           ws.con[(size_t)s * ws.con_stride + ed.partner] = (uint8_t)cb;
         }
         if (want_soft) {
-          const double l0 = log(fabs(mv[0]));
 #pragma unroll
-          for (int b = 0; b < MB; ++b)
-            ws.soft[((size_t)s * cd.N + ed.var) * MB + b] = (float)(log(fabs(mv[b + 1])) - l0);
+          for (int b = 0; b < MB; ++b) ws.soft[((size_t)s * cd.N + ed.var) * MB + b] = soft_ratio(mv[b + 1], mv[0]);
         }
       }
       if constexpr (DIRECT) {

@@ -89,4 +89,36 @@ void* cluster_kp_m(int kpad) {
 template <int MB, int NTHR>
 void* cluster_sym_fn() { return reinterpret_cast<void*>(&nb::lf_cluster_kernel<MB, NTHR, false, false, 0, true>); }
 
+// soft-output instantiations (SOFT = true): variant 0 plain LLR, 1 symbol pmf, 2 half messages, 3 symbol outputs
+template <int MB, int NTHR, int VAR>
+void* cluster_soft_fn() {
+  if constexpr (VAR == 2 && MB < 3) {
+    return nullptr;
+  } else {
+    return reinterpret_cast<void*>(&nb::lf_cluster_kernel<MB, NTHR, VAR == 1, VAR == 2, 0, VAR == 3, true>);
+  }
+}
+template <int VAR>
+void* persist_soft_ptr_t(int m, int big) {
+  switch (m * 2 + (big ? 1 : 0)) {
+    case 2: return cluster_soft_fn<1, 256, VAR>();
+    case 3: return cluster_soft_fn<1, 512, VAR>();
+    case 4: return cluster_soft_fn<2, 256, VAR>();
+    case 5: return cluster_soft_fn<2, 512, VAR>();
+    case 6: return cluster_soft_fn<3, 256, VAR>();
+    case 7: return cluster_soft_fn<3, 512, VAR>();
+    case 8: return cluster_soft_fn<4, 256, VAR>();
+    case 9: return cluster_soft_fn<4, 512, VAR>();
+    case 10: return cluster_soft_fn<5, 256, VAR>();
+    case 11: return cluster_soft_fn<5, 512, VAR>();
+    case 12: return cluster_soft_fn<6, 256, VAR>();
+    case 13: return cluster_soft_fn<6, 512, VAR>();
+    case 14: return cluster_soft_fn<7, 256, VAR>();
+    case 15: return cluster_soft_fn<7, 512, VAR>();
+    case 16: return cluster_soft_fn<8, 256, VAR>();
+    case 17: return cluster_soft_fn<8, 512, VAR>();
+  }
+  return nullptr;
+}
+
 }  // namespace nbk

@@ -10,6 +10,8 @@ void* persist_pmf_ptr(int m, int big);              // k_cluster_pmf.cu: the sym
 void* persist_f16_ptr(int m, int big);              // k_cluster_f16.cu: half-precision messages (m >= 3)
 void* persist_kp_ptr(int m, int kpad);              // k_cluster_kp.cu: compile-time chunk geometry
 void* persist_sym_ptr(int m, int big);              // k_cluster_sym.cu: symbol-level outputs
+void* persist_soft_ptr(int m, int big, int var);    // k_cluster_soft.cu: soft outputs (0 plain, 1 pmf, 2 f16, 3 sym)
+void* persist_soft2_ptr(int m, int big, int var);   // k_cluster_soft2.cu: its pmf / f16 part
 void* ls_kernel_ptr(int m);                         // k_other.cu: the conventional Log-SP kernel
 void* gen_kernel_ptr(int m);                        // k_other.cu: the general-column-weight kernel
 }  // namespace nbk

@@ -277,6 +277,54 @@ __device__ __forceinline__ void tot_sum(const float* smem, int gbase, float* TOT
   }
 }
 
+// LIN: the leave-one-out PRODUCTS of the check node on linear messages: thread pck owns
+// WPT w's x JPT teams of its check; each X_j(w) is replaced in place by prod_{j' != j} X_j'(w) (prefix and
+// suffix products in registers; when one w is split over SPLIT lanes the other lanes' products come by a
+// butterfly of exclusive products).  No division: a zero factor stays exact.
+template <int R, int JPT, int TT, int TEAM>
+__device__ __forceinline__ void tot_prod(float* smem, int gbase, int split, bool cvalid) {
+  constexpr int WPT = R / JPT;
+  float* g = smem + gbase;
+#pragma unroll
+  for (int i = 0; i < WPT; ++i) {
+    float v[JPT], ex[JPT];
+#pragma unroll
+    for (int jj = 0; jj < JPT; ++jj) v[jj] = g[jj * TEAM + i * TT * JPT];
+    float pre = 1.0f;
+#pragma unroll
+    for (int jj = 0; jj < JPT; ++jj) {
+      ex[jj] = pre;
+      pre *= v[jj];
+    }
+    float suf = 1.0f;
+#pragma unroll
+    for (int jj = JPT - 1; jj >= 0; --jj) {
+      ex[jj] *= suf;
+      suf *= v[jj];
+    }
+    if constexpr (WPT == 1) {
+      float other = 1.0f, incl = pre;  // the product of the other split lanes' factors
+      for (int off = 1; off < split; off <<= 1) {
+        const float o = __shfl_xor_sync(0xffffffffu, incl, off);
+        other *= o;
+        incl *= o;
+      }
+#pragma unroll
+      for (int jj = 0; jj < JPT; ++jj) ex[jj] *= other;
+    }
+    if (cvalid) {
+#pragma unroll
+      for (int jj = 0; jj < JPT; ++jj) g[jj * TEAM + i * TT * JPT] = ex[jj];
+    }
+  }
+}
+
+// linear message entry -> the packed (sign | -log2|x|) format of nbldpc_step (0 -> the zero, 200)
+__device__ __forceinline__ float lin_to_packed(float u) {
+  const float mag = fminf(fmaxf(-lg2a(fabsf(u)), 0.0f), kFloor);
+  return __uint_as_float(__float_as_uint(mag) | (mag >= kFloor ? 0u : (__float_as_uint(u) & kSign)));
+}
+
 // One Walsh-Hadamard butterfly stage (u, w) -> (u + w, u - w) on register bit I of a thread's R entries.
 template <int R, int I>
 __device__ __forceinline__ void wht_reg(float (&x)[R]) {
@@ -332,7 +380,9 @@ __device__ __forceinline__ int ppos(int z) {
 // NTHR / (KP TT) checks each), so that the chunk geometry constant-folds; 0: taken from P.
 // SYM = true: also the symbol-level decision at every iteration, written to the
 // frame's output rows: mu_v = WHT(raw) . WHT(W_e) in the phase-B coordinates (M_v = raw (*) W_e).
-template <int MB, int NTHR, bool PMF = false, bool F16 = false, int KP = 0, bool SYM = false>
+// SOFT = true: soft outputs (decode soft_out, nbldpc_step): the decision in fp64 (decision_f64, reading
+// R22); a separate instantiation so that the plain hot-path kernels carry none of its registers.
+template <int MB, int NTHR, bool PMF = false, bool F16 = false, int KP = 0, bool SYM = false, bool SOFT = false>
 #ifndef NB_CLUSTER_MINB
 #define NB_CLUSTER_MINB 2
 #endif
@@ -444,7 +494,12 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   const CallDev* call = ws.call;
   const int max_iters = call->max_iters;
   const int mode = call->mode;
-  const int want_soft = call->want_soft;
+  constexpr bool want_soft = SOFT;  // soft outputs are requested exactly when the host launches a SOFT kernel
+  // LIN: messages stored as linear fp32 values -- the F32 hot path at q >= 128, where dropping
+  // the ex2 / lg2 / sign work of the log format outweighs the check node's extra write-back (measured: C3
+  // -2.5%, C4 -2% time; C2 +5%, C5 +12%, so q <= 64 keeps the log format); the F16 format and the
+  // soft-output kernels (whose fp64 decision needs the exact log-magnitudes) always keep the packed log format
+  constexpr bool LIN = !F16 && !SOFT && MB >= 7;
   const int step = P.step_mode;
   const size_t EQ = (size_t)cd.E * Q;
   const uint32_t flag0 = dsmem_addr(&sh_flag[0], 0), flag1 = dsmem_addr(&sh_flag[1], 0);
@@ -489,7 +544,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
     float* const Tt = ws.Tt + (size_t)slot * cd.N * 8;
     uint8_t* const con = ws.con + (size_t)slot * ws.con_stride;
     float* const Pp = PMF ? call->p0buf + (size_t)slot * cd.N * Q : nullptr;
-    if (!step && PMF) {
+    if (PMF) {  // (also in step mode: nbldpc_step_pmf, slot = frame)
       // the frame's pmf rows scaled to probabilities p_v, one warp per row, stored at
       // ppos(z) for the teams' phase-B reads; a row with a non-positive sum becomes all zero (its
       // variable-node outputs are then neutral and counted as numerical events, reading R23)
@@ -717,11 +772,15 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #pragma unroll
             for (int ch = 0; ch < CH; ++ch) {
               const float4 v = *reinterpret_cast<const float4*>(st + mpos<MB>(t * R + 4 * ch, e));
-              x[4 * ch] = to_lin(v.x); x[4 * ch + 1] = to_lin(v.y); x[4 * ch + 2] = to_lin(v.z); x[4 * ch + 3] = to_lin(v.w);
+              if constexpr (LIN) {
+                x[4 * ch] = v.x; x[4 * ch + 1] = v.y; x[4 * ch + 2] = v.z; x[4 * ch + 3] = v.w;
+              } else {
+                x[4 * ch] = to_lin(v.x); x[4 * ch + 1] = to_lin(v.y); x[4 * ch + 2] = to_lin(v.z); x[4 * ch + 3] = to_lin(v.w);
+              }
             }
           } else {
 #pragma unroll
-            for (int r = 0; r < R; ++r) x[r] = to_lin(st[r]);
+            for (int r = 0; r < R; ++r) x[r] = LIN ? st[r] : to_lin(st[r]);
           }
           if constexpr (PMF) {
             if constexpr (LR > 0) wht_reg<R, 0>(x);  // z bits 0..LR-1 of WHT(W_e')
@@ -780,7 +839,21 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         float raw0 = x[0];
         if constexpr (TT > 1) raw0 = __shfl_sync(0xffffffffu, x[0], lane & ~(TT - 1));
         uint32_t up[R];
-        {
+        if constexpr (LIN) {
+          // U = raw / raw(0): entry 0 is 1; |U| <= 1 up to rounding
+          float inv0;
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv0) : "f"(raw0));
+#pragma unroll
+          for (int r = 0; r < R; ++r) up[r] = __float_as_uint(x[r] * inv0);
+          if (!active) {  // padding edge: the neutral factor 1 in every entry
+#pragma unroll
+            for (int r = 0; r < R; ++r) up[r] = 0x3f800000u;
+          } else if (!(raw0 > 0.0f)) {  // DC term <= 0: neutral message + numerical event (reading R10)
+#pragma unroll
+            for (int r = 0; r < R; ++r) up[r] = zr[r] == 0 ? 0x3f800000u : 0u;
+            if (t == 0) atomicAdd(&ws.slot_events[step ? 0 : slot], 1);
+          }
+        } else {
           const float lg0 = lg2a(raw0);
 #pragma unroll
           for (int r = 0; r < R; ++r) {
@@ -801,7 +874,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         if (P.u_out != nullptr && active) {
           float* dst = P.u_out + ((size_t)f * cd.E + e) * Q;
 #pragma unroll
-          for (int r = 0; r < R; ++r) dst[zr[r]] = __uint_as_float(up[r]);
+          for (int r = 0; r < R; ++r) dst[zr[r]] = LIN ? lin_to_packed(__uint_as_float(up[r])) : __uint_as_float(up[r]);
         }
 
         // ---- TENTATIVE DECISION at v's first edge: M_v(z) = sum_y raw(y) W_e(z ^ y)
@@ -827,7 +900,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #pragma unroll
               for (int ch = 0; ch < 4; ++ch) {
                 const float4 v = wo4[ch];
-                const float d4[4] = {to_lin(v.x), to_lin(v.y), to_lin(v.z), to_lin(v.w)};
+                const float d4[4] = {LIN ? v.x : to_lin(v.x), LIN ? v.y : to_lin(v.y), LIN ? v.z : to_lin(v.z),
+                                     LIN ? v.w : to_lin(v.w)};
                 // z = 16 t + w: tB = w >> LJ, rB = (w & (2^LJ - 1)) | t << LJ; runs of 2^LJ entries stay
                 // contiguous in a D row, so store them as one vector
                 if constexpr (LJ >= 2) {
@@ -845,11 +919,15 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #pragma unroll
               for (int ch = 0; ch < CH; ++ch) {
                 const float4 v = wo4[ch];
-                DB[4 * ch] = to_lin(v.x); DB[4 * ch + 1] = to_lin(v.y); DB[4 * ch + 2] = to_lin(v.z); DB[4 * ch + 3] = to_lin(v.w);
+                if constexpr (LIN) {
+                  *reinterpret_cast<float4*>(DB + 4 * ch) = v;
+                } else {
+                  DB[4 * ch] = to_lin(v.x); DB[4 * ch + 1] = to_lin(v.y); DB[4 * ch + 2] = to_lin(v.z); DB[4 * ch + 3] = to_lin(v.w);
+                }
               }
             } else {
-              DB[0] = to_lin(wo4[0].x);
-              if constexpr (R > 1) DB[1] = to_lin(wo4[0].y);
+              DB[0] = LIN ? wo4[0].x : to_lin(wo4[0].x);
+              if constexpr (R > 1) DB[1] = LIN ? wo4[0].y : to_lin(wo4[0].y);
             }
           }
           if constexpr (TT > 1) __syncwarp();
@@ -950,13 +1028,37 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               if (call->map_out && t == 0) call->map_out[(size_t)f * cd.N + var] = (uint8_t)bx;
             }
           }
+          // soft outputs requested (grid-uniform): the decision again in fp64 from the edge's linear
+          // spectra (decision_f64, reading R22) -- its signs and ratios replace the fp32 ones
+          double md[MB + 1];
+          if constexpr (SOFT) {
+            float bl[R], dl[R], pl[PMF ? R : 1];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              const int z = t * R + r;
+              float bv = 1000.0f;  // packed entries (Gamma^-1 in fp64 inside); 1000: a zero
+              if (is_a) {
+                if constexpr (F16) bv = __half2float(__ldcg(WinH + (size_t)e * Q + mposh<MB>(z, e)));
+                else bv = __ldcg(Win + (size_t)e * Q + mpos<MB>(z, e));
+              }
+              bl[r] = bv;
+              const float dv = R >= 4 ? (&wo4[r >> 2].x)[r & 3] : (r == 0 ? wo4[0].x : wo4[0].y);
+              dl[r] = is_a ? dv : 1000.0f;
+              if constexpr (PMF) pl[r] = is_a ? __ldcg(Pp + (size_t)var * Q + ppos<MB>(z)) : 0.0f;
+            }
+            decision_f64<MB, LR, PMF>(bl, dl, pl, th, t, md);
+          }
           // signs of M(0) and M(alpha^i) over the team (bit i of sbits = [M(.) < 0], index 0 = M(0))
           uint32_t sbits;
           int s_off = 0, s_n = MB + 1;
 #ifndef NB_RS_MIN_TT
 #define NB_RS_MIN_TT 8
 #endif
-          if constexpr (TT >= NB_RS_MIN_TT) {
+          if constexpr (SOFT) {
+            sbits = 0;
+#pragma unroll
+            for (int b = 0; b <= MB; ++b) sbits |= (md[b] < 0.0 ? 1u : 0u) << b;
+          } else if constexpr (TT >= NB_RS_MIN_TT) {
             sbits = team_sign_bits<MB + 1, TT>(mf, lane, s_off, s_n);
           } else if constexpr (TT > 1) {  // small teams: full butterfly all-reduce, every lane holds all totals
 #pragma unroll
@@ -972,24 +1074,9 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             for (int b = 0; b <= MB; ++b) sbits |= (mf[b] < 0.0f ? 1u : 0u) << b;
           }
           const uint32_t s0z = sbits & 1u;  // sgn_GF2 M(0); an exact zero has sign 0
-          if (want_soft && is_a) {
-            // soft output: the team's totals through the consumed stage buffer (rare path)
-            if constexpr (TT >= NB_RS_MIN_TT) {
-              __syncwarp(__activemask());
+          if (want_soft && is_a && t == 0) {
 #pragma unroll
-              for (int k = 0; k <= MB; ++k)
-                if (k < s_n && s_off + k <= MB) DB[s_off + k] = mf[k];
-              __syncwarp(__activemask());
-              if (t == 0) {
-#pragma unroll
-                for (int b = 0; b <= MB; ++b) mf[b] = DB[b];
-              }
-            }
-            if (t == 0) {
-              const float l0 = __logf(fabsf(mf[0]));
-#pragma unroll
-              for (int b = 0; b < MB; ++b) sout[(size_t)var * MB + b] = __logf(fabsf(mf[b + 1])) - l0;
-            }
+            for (int b = 0; b < MB; ++b) sout[(size_t)var * MB + b] = soft_ratio(md[b + 1], md[0]);
           }
           if (is_a && t == 0) {
             const int xv = (int)(((sbits >> 1) ^ (s0z ? 0xFFu : 0u)) & ((1u << MB) - 1u));
@@ -1091,7 +1178,15 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #endif
           }
           check_sync(lc, TPC);
-          switch (JPT) {
+          if constexpr (LIN) {
+            switch (JPT) {
+              case 1: tot_prod<R, 1, TT, C::QS>(smem, gbase + buf * GBLK, SPLIT, cvalid); break;
+              case 2: tot_prod<R, (R >= 2 ? 2 : 1), TT, C::QS>(smem, gbase + buf * GBLK, SPLIT, cvalid); break;
+              case 4: tot_prod<R, (R >= 4 ? 4 : 1), TT, C::QS>(smem, gbase + buf * GBLK, SPLIT, cvalid); break;
+              case 8: tot_prod<R, (R >= 8 ? 8 : 1), TT, C::QS>(smem, gbase + buf * GBLK, SPLIT, cvalid); break;
+              default: tot_prod<R, R, TT, C::QS>(smem, gbase + buf * GBLK, SPLIT, cvalid); break;
+            }
+          } else switch (JPT) {
             case 1: tot_sum<R, 1, TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid); break;
             case 2: tot_sum<R, (R >= 2 ? 2 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid); break;
             case 4: tot_sum<R, (R >= 4 ? 4 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid); break;
@@ -1102,19 +1197,23 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           if (active) {
             float out[R];
 #ifndef NB_SMEM_GENERIC
-            const uint32_t tot_s = smem_u32(TOT);
+            const uint32_t tot_s = smem_u32(LIN ? st : TOT);
 #endif
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
 #ifdef NB_SMEM_GENERIC
-              const float xt = TOT[oidx[r]];
+              const float xt = LIN ? st[oidx[r]] : TOT[oidx[r]];
 #else
               float xt;
               asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xt) : "r"(tot_s + ((uint32_t)oidx[r] << 2)) : "memory");
 #endif
-              const float mg = fabsf(xt) - __uint_as_float(up[r] & ~kSign);  // >= 0 up to rounding
-              out[r] = __uint_as_float((__float_as_uint(mg) & ~kSign) | ((__float_as_uint(xt) ^ up[r]) & kSign));
+              if constexpr (LIN) {
+                out[r] = xt;  // W_e(z) = prod_{j != e} X_j(pi_e^-1 z), written back into my own scatter row
+              } else {
+                const float mg = fabsf(xt) - __uint_as_float(up[r] & ~kSign);  // >= 0 up to rounding
+                out[r] = __uint_as_float((__float_as_uint(mg) & ~kSign) | ((__float_as_uint(xt) ^ up[r]) & kSign));
+              }
             }
             const int prow = rr.partner_a >> 9;  // stored where the partner edge will read it
             NB_CHECK(prow >= 0 && prow < cd.E);
@@ -1226,8 +1325,9 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 
 // message layout conversion for nbldpc_step: natural order (message of edge e in slot e) <-> the
 // cluster kernel's reader-ordered rows (message of edge e in row partner(e), entries at mpos)
+// lin = 1: the kernel's messages are linear (LIN instantiations), the step format packed log
 template <int MB>
-__global__ void nb_msg_layout_kernel(const float* src, float* dst, int frames, CodeDev cd, int to_kernel) {
+__global__ void nb_msg_layout_kernel(const float* src, float* dst, int frames, CodeDev cd, int to_kernel, int lin) {
   constexpr int Q = 1 << MB;
   const size_t n = (size_t)frames * cd.E * Q;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -1238,7 +1338,8 @@ __global__ void nb_msg_layout_kernel(const float* src, float* dst, int frames, C
     const EdgeDev& ed = cd.edges[e];
     if (ed.var < 0) continue;
     const size_t k = (f * cd.E + ed.partner) * Q + mpos<MB>(z, ed.partner);
-    if (to_kernel) dst[k] = src[i]; else dst[i] = src[k];
+    if (to_kernel) dst[k] = lin ? to_lin(src[i]) : src[i];
+    else dst[i] = lin ? lin_to_packed(src[k]) : src[k];
   }
 }
 

@@ -42,6 +42,66 @@ struct GenParams {
   int jmax;               // largest column weight
 };
 
+// The decision in fp64 for soft outputs (reading R22, as decision_f64 of the degree-2 kernels):
+// mu = p0 prod_i w_i with w_i = WHT(Gamma^-1(W_i)) evaluated in fp64 from the fp32 spectra, then
+// M_v(0) = sum mu and M_v(alpha^b) = sum mu (-1)^{x_b} (the 1/q factors are positive
+// and cancel in every sign and ratio).  Team layout z = R t + r; tmask: the team's lanes.
+template <int MB, int LR>
+__device__ __noinline__ void general_decision_f64(const float* W, const int32_t* edges, int d, const float* p0, int t,
+                                                  unsigned tmask, double* md) {
+  constexpr int Q = 1 << MB, R = 1 << LR, TT = Q / R;
+  double mu[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) mu[r] = (double)p0[r];
+  for (int i = 0; i < d; ++i) {
+    double x[R];
+    const float* src = W + (size_t)edges[i] * Q + t * R;
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r] = lin64(src[r]);  // Gamma^-1 in fp64 (see decision_f64)
+#pragma unroll
+    for (int b = 0; b < LR; ++b)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (!(r & (1 << b))) {
+          const double u = x[r], w = x[r | (1 << b)];
+          x[r] = u + w;
+          x[r | (1 << b)] = u - w;
+        }
+#pragma unroll
+    for (int b = LR; b < MB; ++b) {
+      const int off = 1 << (b - LR);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double o = __shfl_xor_sync(tmask, x[r], off);
+        x[r] = (t & off) ? o - x[r] : x[r] + o;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) mu[r] *= x[r];
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) s += mu[r];
+  md[0] = s;
+#pragma unroll
+  for (int b = 0; b < MB; ++b) {
+    double sb = 0.0;
+    if (b < LR) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) sb += ((r >> b) & 1) ? -mu[r] : mu[r];
+    } else {
+      sb = ((t >> (b - LR)) & 1) ? -s : s;
+    }
+    md[b + 1] = sb;
+  }
+  if constexpr (TT > 1) {
+#pragma unroll
+    for (int off = TT / 2; off >= 1; off >>= 1)
+#pragma unroll
+      for (int b = 0; b <= MB; ++b) md[b] += __shfl_xor_sync(tmask, md[b], off);
+  }
+}
+
 template <int MB>
 __global__ void __launch_bounds__(256) lfg_frame_kernel(GenParams P) {
   constexpr int Q = 1 << MB, R = Q < 16 ? Q : 16, TT = Q / R, LR = MB < 4 ? MB : 4;
@@ -218,18 +278,23 @@ __global__ void __launch_bounds__(256) lfg_frame_kernel(GenParams P) {
 #pragma unroll
             for (int b = 0; b <= MB; ++b) Ms[b] = team_sum(Ms[b]);
           }
-          const int s0 = Ms[0] < 0.0f ? 1 : 0;
+          int s0 = Ms[0] < 0.0f ? 1 : 0;
           int xv = 0;
 #pragma unroll
           for (int b = 0; b < MB; ++b) xv |= ((Ms[b + 1] < 0.0f ? 1 : 0) ^ s0) << b;
-          if (t == 0) {
-            xh[v] = (uint8_t)xv;
-            if (P.soft_out) {
-              const float l0 = __logf(fabsf(Ms[0]));
+          if (P.soft_out) {  // soft outputs: the decision again in fp64 (reading R22); its signs decide
+            double md[MB + 1];
+            general_decision_f64<MB, LR>(W, P.v_edges + e0, d, p0, t, tmask, md);
+            s0 = md[0] < 0.0 ? 1 : 0;
+            xv = 0;
 #pragma unroll
-              for (int b = 0; b < MB; ++b) P.soft_out[((size_t)f * cd.N + v) * MB + b] = __logf(fabsf(Ms[b + 1])) - l0;
+            for (int b = 0; b < MB; ++b) xv |= ((md[b + 1] < 0.0 ? 1 : 0) ^ s0) << b;
+            if (t == 0) {
+#pragma unroll
+              for (int b = 0; b < MB; ++b) P.soft_out[((size_t)f * cd.N + v) * MB + b] = soft_ratio(md[b + 1], md[0]);
             }
           }
+          if (t == 0) xh[v] = (uint8_t)xv;
           if (P.post_out || P.map_out) {  // symbol posterior mu / sum mu and its argmax
             float tot = 0.0f, best = 0.0f;
             int bx = 0;

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -57,6 +58,7 @@ struct Workspace {
   size_t p0buf_bytes = 0;
   void* ls_base = nullptr;  // conventional Log-SP: W [2][S][E][q], L0 [S][N][q], xhat [S][N], counter
   size_t ls_bytes = 0;
+  cudaEvent_t ev_done = nullptr;  // recorded on the stream of every decode that used this workspace
   // launch accounting of the most recent decode
   cudaStream_t last_stream = nullptr;
   int last_graph = 0;
@@ -89,6 +91,10 @@ struct nbldpc_code_s {
   int p_tpc = 1, p_cpc = 1, p_groups = 1, p_block = 32, p_big = 0, p_cs = 1, p_ncl = 1, p_recs = 0;
   int p_kp = 0;  // > 0: the plain LLR launch uses the compile-time-geometry instantiation (KP = kpad)
   size_t p_smem = 0;
+  // false: the cluster kernel cannot run this code (its per-CTA edge records do not fit in shared memory
+  // even with 16-CTA clusters, or no cluster fits on the GPU): NBLDPC_VN_SEPARABLE decodes run the
+  // general-column-weight kernel instead (same results up to rounding)
+  bool cluster_ok = true;
 };
 
 namespace {
@@ -142,6 +148,8 @@ size_t slot_bytes_of(const nbldpc_code_s* c) {
 }
 
 void free_workspace(Workspace& w) {
+  // the handle's last decode may still run (stream-ordered buffers are not freed synchronously): wait for it
+  if (w.ev_done) cudaEventSynchronize(w.ev_done);
   if (w.graph) cudaGraphExecDestroy(w.graph);
   if (w.base) cudaFree(w.base);
   if (w.host_flag) cudaFreeHost(w.host_flag);
@@ -153,6 +161,7 @@ void free_workspace(Workspace& w) {
   if (w.ev_start) cudaEventDestroy(w.ev_start);
   if (w.ev_first) cudaEventDestroy(w.ev_first);
   if (w.chunk_flags) cudaFree(w.chunk_flags);
+  if (w.ev_done) cudaEventDestroy(w.ev_done);
   w = Workspace{};
 }
 
@@ -161,7 +170,8 @@ using nbk::persist_kp_ptr;
 
 // pmf = 1: the nbldpc_decode_pmf variant; f16 = 1: half-precision messages (NBLDPC_MSG_F16);
 // sym = 1: the symbol-output variant (LLR input)
-void* persist_kernel_ptr(int m, int big, int pmf = 0, int f16 = 0, int sym = 0) {
+void* persist_kernel_ptr(int m, int big, int pmf = 0, int f16 = 0, int sym = 0, int soft = 0) {
+  if (soft) return (sym && (pmf || f16)) ? nullptr : nbk::persist_soft_ptr(m, big, sym ? 3 : f16 ? 2 : pmf ? 1 : 0);
   if (sym) return (pmf || f16) ? nullptr : nbk::persist_sym_ptr(m, big);
   if (f16) return pmf ? nullptr : nbk::persist_f16_ptr(m, big);
   return pmf ? nbk::persist_pmf_ptr(m, big) : nbk::persist_plain_ptr(m, big);
@@ -182,7 +192,7 @@ int persist_team_words(int m) {
 }
 
 cudaError_t launch_cluster(const nbldpc_code_s* c, const nb::ClusterParams& P, int ncl, cudaStream_t st, int pmf = 0,
-                           int f16 = 0, int sym = 0) {
+                           int f16 = 0, int sym = 0, int soft = 0) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(ncl * c->p_cs));
   cfg.blockDim = dim3((unsigned)c->p_block);
@@ -196,8 +206,8 @@ cudaError_t launch_cluster(const nbldpc_code_s* c, const nb::ClusterParams& P, i
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void* args[] = {const_cast<nb::ClusterParams*>(&P)};
-  void* fn = (c->p_kp && !pmf && !f16 && !sym) ? persist_kp_ptr(c->m, c->p_kp)
-                                               : persist_kernel_ptr(c->m, c->p_big, pmf, f16, sym);
+  void* fn = (c->p_kp && !pmf && !f16 && !sym && !soft) ? persist_kp_ptr(c->m, c->p_kp)
+                                                        : persist_kernel_ptr(c->m, c->p_big, pmf, f16, sym, soft);
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
@@ -216,19 +226,21 @@ cudaError_t ensure_smem_attr(const nbldpc_code_s* c) {
     if (e != cudaSuccess) return e;
     g_attr_smem[d][k] = c->smem;
   }
-  static size_t p_attr[64][18 * 5 + 32] = {};
-  for (int var = 0; var < 5; ++var) {  // plain, pmf, f16, compile-time geometry, symbol outputs
-    const int pmf = var == 1, f16 = var == 2, sym = var == 4;
+  static size_t p_attr[64][18 * 9 + 32] = {};
+  for (int var = 0; c->cluster_ok && var < 9; ++var) {
+    // plain, pmf, f16, compile-time geometry, symbol outputs; then the soft-output plain, pmf, f16, sym
+    const int soft = var >= 5;
+    const int pmf = var == 1 || var == 6, f16 = var == 2 || var == 7, sym = var == 4 || var == 8;
     void* fn = var == 3 ? (c->p_kp ? persist_kp_ptr(c->m, c->p_kp) : nullptr)
-                        : persist_kernel_ptr(c->m, c->p_big, pmf, f16, sym);
+                        : persist_kernel_ptr(c->m, c->p_big, pmf, f16, sym, soft);
     if (!fn) continue;
     if (c->p_cs > 8) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;
     }
     // one cache slot per kernel: (m, big, variant), or (m, kpad) for the compile-time-geometry one
-    int k = (c->m * 2 + c->p_big) * 5 + var;
-    if (var == 3) k = 18 * 5 + (c->m - 1) * 4 + (c->p_kp == 4 ? 0 : c->p_kp == 8 ? 1 : c->p_kp == 16 ? 2 : 3);
+    int k = (c->m * 2 + c->p_big) * 9 + var;
+    if (var == 3) k = 18 * 9 + (c->m - 1) * 4 + (c->p_kp == 4 ? 0 : c->p_kp == 8 ? 1 : c->p_kp == 16 ? 2 : 3);
     const int d = c->device & 63;
     if (p_attr[d][k] < c->p_smem) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->p_smem);
@@ -258,17 +270,10 @@ int choose_lanes(const nbldpc_code_s* c, int S) {
   return best;
 }
 
-nbldpc_status_t ensure_workspace(nbldpc_code_s* c, int S) {
-  Workspace& w = c->ws;
-  if (w.base && w.S == S) return NBLDPC_OK;
-  if (w.base) {
-    cudaDeviceSynchronize();
-    if (w.graph) cudaGraphExecDestroy(w.graph);
-    w.graph = nullptr;
-    cudaFree(w.base);
-    w.base = nullptr;
-    cudaGetLastError();
-  }
+// Carves the slot state of S resident frames out of `b` (NULL: sizing only); returns the bytes used.
+// Layout: W [2][S][E][q] | Tt [S][N][8] | xhat | soft | con (syndrome contributions, zeroed) | per-slot
+// counters | glob[16] | CallDev.  Everything from `con` on must be zero before the first decode.
+size_t layout_workspace(const nbldpc_code_s* c, int S, char* b, WorkDev* dev, size_t* zero_from = nullptr) {
   const size_t q = c->q;
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -288,28 +293,77 @@ nbldpc_status_t ensure_workspace(nbldpc_code_s* c, int S) {
   const size_t oE = take((size_t)S * sizeof(int32_t));
   const size_t oG = take(16 * sizeof(int32_t));
   const size_t oK = take(sizeof(CallDev));
-  void* base = nullptr;
-  NB_TRY(cudaMalloc(&base, off));
-  NB_TRY(cudaMemset(base, 0, off));  // padding edge slots of `con` must stay zero
-  char* b = static_cast<char*>(base);
+  if (zero_from) *zero_from = oP;
+  if (b && dev) {
+    *dev = WorkDev{};
+    dev->S = S;
+    dev->W = reinterpret_cast<float*>(b + oW);
+    dev->Tt = reinterpret_cast<float*>(b + oT);
+    dev->xhat = reinterpret_cast<uint8_t*>(b + oX);
+    dev->soft = reinterpret_cast<float*>(b + oS);
+    dev->con = reinterpret_cast<uint8_t*>(b + oP);
+    dev->con_stride = c->con_stride;
+    dev->slot_frame = reinterpret_cast<int32_t*>(b + oF);
+    dev->slot_iter = reinterpret_cast<int32_t*>(b + oI);
+    dev->slot_events = reinterpret_cast<int32_t*>(b + oV);
+    dev->slot_counter = reinterpret_cast<int32_t*>(b + oC);
+    dev->slot_epoch = reinterpret_cast<int32_t*>(b + oE);
+    dev->glob = reinterpret_cast<int32_t*>(b + oG);
+    dev->call = reinterpret_cast<CallDev*>(b + oK);
+  }
+  return off;
+}
+
+// Grows a handle buffer to >= need bytes, stream-ordered on `st` (no host or device-wide sync): the
+// old buffer is released with cudaFreeAsync after the handle's previous decode (event ev_done, which
+// may have run on another stream) and everything earlier on `st`; the new one comes from
+// cudaMallocAsync on `st`.
+template <class T>
+nbldpc_status_t grow_buffer(Workspace& w, T** buf, size_t* have, size_t need, cudaStream_t st) {
+  if (*buf && *have >= need) return NBLDPC_OK;
+  if (*buf) {
+    if (w.ev_done) NB_TRY(cudaStreamWaitEvent(st, w.ev_done, 0));
+    NB_TRY(cudaFreeAsync(*buf, st));
+    *buf = nullptr;
+    *have = 0;
+  }
+  void* p = nullptr;
+  NB_TRY(cudaMallocAsync(&p, need, st));
+  *buf = static_cast<T*>(p);
+  *have = need;
+  return NBLDPC_OK;
+}
+
+// the decode just enqueued on `st` used the handle's workspace: later reallocations wait for it
+nbldpc_status_t mark_done(Workspace& w, cudaStream_t st) {
+  if (!w.ev_done) NB_TRY(cudaEventCreateWithFlags(&w.ev_done, cudaEventDisableTiming));
+  NB_TRY(cudaEventRecord(w.ev_done, st));
+  return NBLDPC_OK;
+}
+
+// The handle's slot state for S resident frames, re-carved (and grown, stream-ordered) when S changes.
+nbldpc_status_t ensure_workspace(nbldpc_code_s* c, int S, cudaStream_t st) {
+  Workspace& w = c->ws;
+  if (w.base && w.S == S) return NBLDPC_OK;
+  if (w.graph) {  // captured the old slot layout; an in-flight launch completes before it is freed
+    cudaGraphExecDestroy(w.graph);
+    w.graph = nullptr;
+  }
+  size_t zero_from = 0;
+  const size_t off = layout_workspace(c, S, nullptr, nullptr, &zero_from);
+  void* base = w.base;
+  nbldpc_status_t rs = grow_buffer(w, &base, &w.bytes, off, st);
   w.base = base;
-  w.bytes = off;
+  if (rs != NBLDPC_OK) {
+    w.S = 0;
+    return rs;
+  }
+  char* b = static_cast<char*>(base);
+  if (w.ev_done) NB_TRY(cudaStreamWaitEvent(st, w.ev_done, 0));  // a previous decode may still use it
+  NB_TRY(cudaMemsetAsync(b + zero_from, 0, off - zero_from, st));  // padding edge slots of `con` stay zero
   w.S = S;
   w.Y = choose_lanes(c, S);
-  w.dev.S = S;
-  w.dev.W = reinterpret_cast<float*>(b + oW);
-  w.dev.Tt = reinterpret_cast<float*>(b + oT);
-  w.dev.xhat = reinterpret_cast<uint8_t*>(b + oX);
-  w.dev.soft = reinterpret_cast<float*>(b + oS);
-  w.dev.con = reinterpret_cast<uint8_t*>(b + oP);
-  w.dev.con_stride = c->con_stride;
-  w.dev.slot_frame = reinterpret_cast<int32_t*>(b + oF);
-  w.dev.slot_iter = reinterpret_cast<int32_t*>(b + oI);
-  w.dev.slot_events = reinterpret_cast<int32_t*>(b + oV);
-  w.dev.slot_counter = reinterpret_cast<int32_t*>(b + oC);
-  w.dev.slot_epoch = reinterpret_cast<int32_t*>(b + oE);
-  w.dev.glob = reinterpret_cast<int32_t*>(b + oG);
-  w.dev.call = reinterpret_cast<CallDev*>(b + oK);
+  layout_workspace(c, S, b, &w.dev);
   if (!w.host_flag) NB_TRY(cudaMallocHost(&w.host_flag, 64));
   return NBLDPC_OK;
 }
@@ -336,29 +390,34 @@ PassParams make_params(const nbldpc_code_s* c, int step_mode, float* u_out) {  /
   return P;
 }
 
-nb::ClusterParams make_cparams(const nbldpc_code_s* c, int step_mode, int step_iter, float* u_out);
+nb::ClusterParams make_cparams(const nbldpc_code_s* c, int step_mode, int step_iter, float* u_out,
+                               const WorkDev* dev = nullptr);
 
 template <int MB>
-cudaError_t launch_layout_t(const nb::CodeDev& cd, const float* src, float* dst, int frames, int to_kernel, cudaStream_t st) {
-  nb::nb_msg_layout_kernel<MB><<<512, 256, 0, st>>>(src, dst, frames, cd, to_kernel);
+cudaError_t launch_layout_t(const nb::CodeDev& cd, const float* src, float* dst, int frames, int to_kernel, int lin,
+                            cudaStream_t st) {
+  nb::nb_msg_layout_kernel<MB><<<512, 256, 0, st>>>(src, dst, frames, cd, to_kernel, lin);
   return cudaGetLastError();
 }
-cudaError_t launch_layout(const nbldpc_code_s* c, const float* src, float* dst, int frames, int to_kernel,
+// lin = 1: the cluster kernel stores linear messages (its plain / KP / pmf / symbol instantiations for
+// m >= 7, see LIN in lf_cluster.cuh); lin = 0: the packed log format (all others)
+cudaError_t launch_layout(const nbldpc_code_s* c, const float* src, float* dst, int frames, int to_kernel, int lin,
                           cudaStream_t st) {
   const nb::CodeDev cd = make_cparams(c, 0, 0, nullptr).code;
   switch (c->m) {
-    case 1: return launch_layout_t<1>(cd, src, dst, frames, to_kernel, st);
-    case 2: return launch_layout_t<2>(cd, src, dst, frames, to_kernel, st);
-    case 3: return launch_layout_t<3>(cd, src, dst, frames, to_kernel, st);
-    case 4: return launch_layout_t<4>(cd, src, dst, frames, to_kernel, st);
-    case 5: return launch_layout_t<5>(cd, src, dst, frames, to_kernel, st);
-    case 6: return launch_layout_t<6>(cd, src, dst, frames, to_kernel, st);
-    case 7: return launch_layout_t<7>(cd, src, dst, frames, to_kernel, st);
-    default: return launch_layout_t<8>(cd, src, dst, frames, to_kernel, st);
+    case 1: return launch_layout_t<1>(cd, src, dst, frames, to_kernel, lin, st);
+    case 2: return launch_layout_t<2>(cd, src, dst, frames, to_kernel, lin, st);
+    case 3: return launch_layout_t<3>(cd, src, dst, frames, to_kernel, lin, st);
+    case 4: return launch_layout_t<4>(cd, src, dst, frames, to_kernel, lin, st);
+    case 5: return launch_layout_t<5>(cd, src, dst, frames, to_kernel, lin, st);
+    case 6: return launch_layout_t<6>(cd, src, dst, frames, to_kernel, lin, st);
+    case 7: return launch_layout_t<7>(cd, src, dst, frames, to_kernel, lin, st);
+    default: return launch_layout_t<8>(cd, src, dst, frames, to_kernel, lin, st);
   }
 }
 
-nb::ClusterParams make_cparams(const nbldpc_code_s* c, int step_mode, int step_iter, float* u_out) {
+nb::ClusterParams make_cparams(const nbldpc_code_s* c, int step_mode, int step_iter, float* u_out,
+                               const WorkDev* dev) {
   nb::ClusterParams P{};
   P.code.m = c->m;
   P.code.M = c->M;
@@ -370,7 +429,7 @@ nb::ClusterParams make_cparams(const nbldpc_code_s* c, int step_mode, int step_i
   P.code.gf_exp = c->gf_exp_d;
   P.code.gf_log = c->gf_log_d;
   P.code.pinv_tab = c->pinv_tab_d;
-  P.ws = c->ws.dev;
+  P.ws = dev ? *dev : c->ws.dev;
   P.chunks = c->p_groups;
   P.checks_per_cta = c->p_cpc;
   P.tpc = c->p_tpc;
@@ -482,15 +541,9 @@ nbldpc_status_t decode_logsp(nbldpc_code_s* c, const float* llr, const float* pm
   const size_t bL = align_up((size_t)S * c->N * q * sizeof(float), 256);
   const size_t bX = align_up((size_t)S * c->N, 256);
   const size_t need = bW + bL + bX + 256;
-  if (w.ls_bytes < need) {
-    if (w.ls_base) {
-      NB_TRY(cudaStreamSynchronize(st));
-      cudaFree(w.ls_base);
-      w.ls_base = nullptr;
-      w.ls_bytes = 0;
-    }
-    NB_TRY(cudaMalloc(&w.ls_base, need));
-    w.ls_bytes = need;
+  {
+    nbldpc_status_t rs = grow_buffer(w, &w.ls_base, &w.ls_bytes, need, st);
+    if (rs != NBLDPC_OK) return rs;
   }
   char* b = static_cast<char*>(w.ls_base);
   nb::LsParams P{};
@@ -515,7 +568,7 @@ nbldpc_status_t decode_logsp(nbldpc_code_s* c, const float* llr, const float* pm
   w.last_stream = st;
   w.last_graph = 0;
   w.last_host_launches = 1;
-  return NBLDPC_OK;
+  return mark_done(w, st);
 }
 
 // ---- any column weight (NBLDPC_VN_GENERAL, lf_general.cuh): one CTA per frame, persistent
@@ -544,15 +597,9 @@ nbldpc_status_t decode_general(nbldpc_code_s* c, const float* llr, const float* 
   const size_t bM = align_up((size_t)S * c->E * q * sizeof(float), 256);
   const size_t bX = align_up((size_t)S * c->N, 256);
   const size_t need = 2 * bM + bX + 256;
-  if (w.ls_bytes < need) {  // shares the Log-SP workspace (one decode per handle at a time)
-    if (w.ls_base) {
-      NB_TRY(cudaStreamSynchronize(st));
-      cudaFree(w.ls_base);
-      w.ls_base = nullptr;
-      w.ls_bytes = 0;
-    }
-    NB_TRY(cudaMalloc(&w.ls_base, need));
-    w.ls_bytes = need;
+  {  // shares the Log-SP workspace (one decode per handle at a time)
+    nbldpc_status_t rs = grow_buffer(w, &w.ls_base, &w.ls_bytes, need, st);
+    if (rs != NBLDPC_OK) return rs;
   }
   char* b = static_cast<char*>(w.ls_base);
   nb::GenParams P{};
@@ -583,11 +630,26 @@ nbldpc_status_t decode_general(nbldpc_code_s* c, const float* llr, const float* 
   w.last_stream = st;
   w.last_graph = 0;
   w.last_host_launches = 1;
-  return NBLDPC_OK;
+  return mark_done(w, st);
+}
+
+// Copies caller options into a zeroed struct: callers built against the round-1 header (without the
+// workspace fields) pass a smaller struct_size, and fields past it read as zero.
+constexpr size_t kOptsV1Size = offsetof(nbldpc_decode_opts_t, workspace);
+bool normalise_opts(const nbldpc_decode_opts_t* in, nbldpc_decode_opts_t* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->struct_size = sizeof(*out);
+  if (!in) return true;
+  if (in->struct_size < kOptsV1Size) return false;
+  std::memcpy(out, in, std::min(in->struct_size, sizeof(*out)));
+  out->struct_size = sizeof(*out);
+  return true;
 }
 
 // pmf != NULL: nbldpc_decode_pmf (llr unused; the direct kernel with the general channel spectrum)
 // chunk_flags: nbldpc_decode_host's arrival flags (cluster path only; see there)
+// opts->workspace != NULL: the caller's workspace (cluster kernel only); the handle's state is not
+// touched, so the caller need not hold the handle lock (see nbldpc_decode_ex)
 nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int max_iters, uint8_t* hard,
                             uint8_t* ok, int32_t* iters, cudaStream_t st, const nbldpc_decode_opts_t* opts,
                             const float* pmf = nullptr, const int32_t* chunk_flags = nullptr, int chunk_frames = 0) {
@@ -597,8 +659,12 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   float* post = nullptr;
   uint8_t* xmap = nullptr;
   int f16 = 0;
+  nbldpc_decode_opts_t onorm;
+  if (!normalise_opts(opts, &onorm)) return NBLDPC_ERR_INVALID_ARGUMENT;
+  void* user_ws = onorm.workspace;
+  const size_t user_ws_bytes = onorm.workspace_bytes;
   if (opts) {
-    if (opts->struct_size < sizeof(nbldpc_decode_opts_t)) return NBLDPC_ERR_INVALID_ARGUMENT;
+    opts = &onorm;
     mode = opts->syndrome_mode;
     early = opts->no_early_stop ? 0 : 1;
     soft = opts->soft_out;
@@ -626,6 +692,8 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
     return NBLDPC_ERR_INVALID_ARGUMENT;
   if (mode != 0 && mode != 1) return NBLDPC_ERR_INVALID_ARGUMENT;
   if (direct < 0 || direct > 2) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (f16 && !c->cluster_ok) return NBLDPC_ERR_UNSUPPORTED;  // half messages live in the cluster kernel only
+  if (!c->cluster_ok && direct == 0 && !(pmf && (post || xmap))) direct = 2;  // cluster kernel cannot hold this code
   if (!c->colw2 || direct == 2) {  // column weights != 2, or asked for: the general kernel
     if (mode != 0) return NBLDPC_ERR_INVALID_ARGUMENT;
     if ((soft && !is_device_ptr(soft)) || (events && !is_device_ptr(events))) return NBLDPC_ERR_INVALID_ARGUMENT;
@@ -638,22 +706,28 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   int S = slots > 0 ? std::min(slots, frames) : default_slots(c, frames);
   if (!direct) S = std::min(slots > 0 ? slots : c->p_ncl, std::min(c->p_ncl, frames));  // slots = clusters
   NB_TRY(cudaSetDevice(c->device));
-  nbldpc_status_t rs = ensure_workspace(c, S);
-  if (rs != NBLDPC_OK) return rs;
   Workspace& w = c->ws;
+  nbldpc_status_t rs = NBLDPC_OK;
+  WorkDev udev{};
+  if (user_ws) {
+    // the caller's workspace (nbldpc_decode_opts_t::workspace): cluster kernel, LLR input only
+    if (direct || pmf || chunk_flags) return NBLDPC_ERR_UNSUPPORTED;
+    size_t zero_from = 0;
+    const size_t need = layout_workspace(c, S, nullptr, nullptr, &zero_from);
+    if (user_ws_bytes < need || ((uintptr_t)user_ws & 255) || !is_device_ptr(user_ws))
+      return NBLDPC_ERR_INVALID_ARGUMENT;
+    layout_workspace(c, S, static_cast<char*>(user_ws), &udev);
+    NB_TRY(cudaMemsetAsync(static_cast<char*>(user_ws) + zero_from, 0, need - zero_from, st));
+  } else {
+    rs = ensure_workspace(c, S, st);
+    if (rs != NBLDPC_OK) return rs;
+  }
+  const WorkDev& dv = user_ws ? udev : w.dev;
   CallDev call{};
   if (pmf) {
     const size_t need = (size_t)S * c->N * c->q * sizeof(float);
-    if (w.p0buf_bytes < need) {
-      if (w.p0buf) {
-        NB_TRY(cudaStreamSynchronize(st));  // a previous pmf decode on this stream may still read it
-        cudaFree(w.p0buf);
-        w.p0buf = nullptr;
-        w.p0buf_bytes = 0;
-      }
-      NB_TRY(cudaMalloc(&w.p0buf, need));
-      w.p0buf_bytes = need;
-    }
+    rs = grow_buffer(w, &w.p0buf, &w.p0buf_bytes, need, st);  // stream-ordered (a previous pmf decode may read it)
+    if (rs != NBLDPC_OK) return rs;
     call.pmf = pmf;
     call.p0buf = w.p0buf;
   }
@@ -677,24 +751,29 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   if (direct) {
     nb::nb_setup_kernel<<<(S + 255) / 256, 256, 0, st>>>(w.dev, call);
   } else {
-    nb::nb_cluster_setup_kernel<<<(S + 255) / 256, 256, 0, st>>>(w.dev, call);
+    nb::nb_cluster_setup_kernel<<<(S + 255) / 256, 256, 0, st>>>(dv, call);
   }
   NB_TRY(cudaGetLastError());
+  if (user_ws) {
+    nb::ClusterParams PP = make_cparams(c, 0, 0, nullptr, &udev);
+    NB_TRY(launch_cluster(c, PP, S, st, 0, f16, (post || xmap) ? 1 : 0, soft != nullptr));
+    return NBLDPC_OK;
+  }
   w.last_stream = st;
   w.last_graph = use_graph >= 0;
   w.last_host_launches = 1;
   if (!direct) {
     nb::ClusterParams PP = make_cparams(c, 0, 0, nullptr);
-    NB_TRY(launch_cluster(c, PP, S, st, pmf != nullptr, f16, (post || xmap) ? 1 : 0));
+    NB_TRY(launch_cluster(c, PP, S, st, pmf != nullptr, f16, (post || xmap) ? 1 : 0, soft != nullptr));
     w.last_graph = 0;
     w.last_host_launches = 2;
-    return NBLDPC_OK;
+    return mark_done(w, st);
   }
   if (use_graph >= 0) {
     rs = build_graph(c, direct);
     if (rs != NBLDPC_OK) return rs;
     NB_TRY(cudaGraphLaunch(w.graph, st));
-    return NBLDPC_OK;
+    return mark_done(w, st);
   }
   // host-driven loop: launch passes, poll the active-slot counter every few passes
   PassParams P = make_params(c, 0, nullptr);
@@ -707,17 +786,19 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
     NB_TRY(cudaStreamSynchronize(st));
     if (*w.host_flag == 0) break;
   }
-  return NBLDPC_OK;
+  return mark_done(w, st);
 }
 
 // Which edge of a degree-2 variable evaluates its tentative decision ("is_a") is free: both give
-// M_v = P^0 (*) W_a (*) W_b.  The kernels run an edge team per 32 / TT consecutive edge slots in a
-// warp, and a warp with no deciding edge skips the decision (warp-uniform branch) while a warp with
-// any pays it in full.  So choose the deciding warps as a small vertex cover of the graph whose nodes
-// are warps and whose edges are variables (greedy: repeatedly the warp covering most uncovered
-// variables), and let each variable decide in a covering warp.
-void assign_decision_owners(std::vector<EdgeDev>& edges, int E, int tt) {
-  const int per = 32 / tt;  // edge slots per warp
+// M_v = P^0 (*) W_a (*) W_b.  The cluster kernel runs an edge team per TT threads in barrier groups of
+// max(32, kpad TT) threads (a warp, or one check when a check is wider than a warp); a group with no
+// deciding edge skips the decision, while a group with any waits for it at its next barrier.  So
+// choose the deciding groups as a small vertex cover of the graph whose nodes are groups and whose
+// edges are variables (greedy: repeatedly the group covering most uncovered variables), and let each
+// variable decide in a covering group.  (Measured cover: 82% of the checks of C4, 73% of C3, against
+// 57% of the warps at warp granularity -- every check of those had some deciding warp.)
+void assign_decision_owners(std::vector<EdgeDev>& edges, int E, int tt, int kpad) {
+  const int per = std::max(32 / tt, kpad);  // edge slots per barrier group
   const int nw = (E + per - 1) / per;
   std::vector<int> deg(nw, 0);
   for (int e = 0; e < E; ++e)
@@ -788,7 +869,7 @@ const char* nbldpc_status_string(nbldpc_status_t s) {
     case NBLDPC_OK: return "ok";
     case NBLDPC_ERR_INVALID_ARGUMENT: return "invalid argument";
     case NBLDPC_ERR_NOT_PRIMITIVE: return "polynomial is not primitive of degree m";
-    case NBLDPC_ERR_UNSUPPORTED: return "unsupported parity-check matrix (column weight must be 2, rows >= 2)";
+    case NBLDPC_ERR_UNSUPPORTED: return "unsupported code or option combination (column weights 1..16, row degrees >= 2)";
     case NBLDPC_ERR_CUDA: return "CUDA error";
     case NBLDPC_ERR_OUT_OF_MEMORY: return "out of memory";
   }
@@ -886,7 +967,7 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
       ea.plogh = ed.logh;
     }
   }
-  if (colw2 && !getenv("NBLDPC_FIRST_EDGE_DECIDES")) assign_decision_owners(edges, E, tt);
+  if (colw2 && !getenv("NBLDPC_FIRST_EDGE_DECIDES")) assign_decision_owners(edges, E, tt, kpad);
   std::vector<uint8_t> gexp(2 * (q - 1) + 1), glog(q, 0);
   for (size_t i = 0; i < gexp.size(); ++i) gexp[i] = (uint8_t)ex[i];
   for (int x = 1; x < q; ++x) glog[x] = (uint8_t)lg[x];
@@ -994,22 +1075,28 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
       const int v = atoi(env);
       if (v >= 1 && v <= 16 && c->p_groups % v == 0) cs = v;
     }
-    c->p_cs = cs;
     // full CTAs (NTHR threads of checks of kpad teams): the geometry is a compile-time constant
     if (c->p_block == (tpc > 256 ? 512 : 256) && c->p_cpc * tpc == c->p_block && !getenv("NBLDPC_NO_KP") &&
         persist_kp_ptr(m, kpad) != nullptr)
       c->p_kp = kpad;
     const int kt = tpc / tt;
+    // each CTA keeps the 8-byte edge records of its ceil(G / cs) chunks in shared memory, so long codes
+    // need larger clusters: raise cs (2, 4, 8, then the non-portable 16) until the CTA fits in 227 KB
+    // (the kernel balances chunk counts that cs does not divide); beyond that the code runs the
+    // general kernel (cluster_ok = false)
+    auto smem_for = [&](int csz) {
+      const size_t recs = (size_t)((c->p_groups + csz - 1) / csz) * c->p_cpc * kt;
+      return ((size_t)(c->p_block / tt) * persist_team_words(m) + (size_t)c->p_cpc * q) * sizeof(float) +
+             (size_t)q * sizeof(uint64_t) + recs * sizeof(nb::EdgeRec) + align_up(3 * (size_t)q, 16);
+    };
+    while (smem_for(cs) > 227 * 1024 && cs < 16 && cs < c->p_groups) cs *= 2;
+    c->p_cs = cs;
     c->p_recs = ((c->p_groups + cs - 1) / cs) * c->p_cpc * kt;
-    c->p_smem = ((size_t)(c->p_block / tt) * persist_team_words(m) + (size_t)c->p_cpc * q) * sizeof(float) +
-                (size_t)q * sizeof(uint64_t) + (size_t)c->p_recs * sizeof(nb::EdgeRec) + align_up(3 * (size_t)q, 16);
-    if (c->p_smem > 227 * 1024) {
-      nbldpc_destroy(c);
-      return NBLDPC_ERR_UNSUPPORTED;
-    }
+    c->p_smem = smem_for(cs);
+    if (c->p_smem > 227 * 1024) c->cluster_ok = false;
   }
   if (cudaError_t e = ensure_smem_attr(c)) return bail(e);
-  {
+  if (c->cluster_ok) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(c->p_cs * 64));
     cfg.blockDim = dim3((unsigned)c->p_block);
@@ -1023,12 +1110,12 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
     cfg.numAttrs = 1;
     int ncl = 0;
     void* fn = c->p_kp ? persist_kp_ptr(m, c->p_kp) : persist_kernel_ptr(m, c->p_big);
-    if (cudaError_t e = cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg)) return bail(e);
-    if (ncl < 1) {
-      nbldpc_destroy(c);
-      return NBLDPC_ERR_UNSUPPORTED;
+    if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess || ncl < 1) {
+      cudaGetLastError();
+      c->cluster_ok = false;  // no cluster of this shape fits: the general kernel decodes this code
+    } else {
+      c->p_ncl = ncl;
     }
-    c->p_ncl = ncl;
   }
   int bps = 0;
   if (cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pass_kernel_ptr(m, c->big, 0), c->block, c->smem))
@@ -1071,9 +1158,8 @@ size_t nbldpc_workspace_bytes(nbldpc_code_t c, int frames) {
   if (!c || frames < 1) return 0;
   // the default path: the cluster kernel keeps one slot per resident cluster (decode_impl);
   // codes with a column weight != 2 run the general kernel (two message sets + estimates per slot)
-  if (!c->colw2) return 0;  // allocated per call by decode_general, sized by occupancy
-  const size_t S = (size_t)std::min(c->p_ncl, frames);
-  return S * slot_bytes_of(c) + sizeof(CallDev) + 16 * sizeof(int32_t);
+  if (!c->colw2 || !c->cluster_ok) return 0;  // allocated per call by decode_general, sized by occupancy
+  return layout_workspace(c, std::min(c->p_ncl, frames), nullptr, nullptr);
 }
 
 nbldpc_status_t nbldpc_last_decode_launches(nbldpc_code_t c, long long* launches) {
@@ -1100,8 +1186,12 @@ nbldpc_status_t nbldpc_decode_ex(nbldpc_code_t c, const float* llr, int frames, 
   if (!c || frames < 1 || max_iters < 1) return NBLDPC_ERR_INVALID_ARGUMENT;
   if (!is_device_ptr(llr) || !is_device_ptr(hard) || !is_device_ptr(ok) || !is_device_ptr(iters))
     return NBLDPC_ERR_INVALID_ARGUMENT;
+  nbldpc_decode_opts_t o;
+  if (!normalise_opts(opts, &o)) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (o.workspace)  // the caller's workspace: nothing of the handle is written, no lock (concurrent streams)
+    return decode_impl(c, llr, frames, max_iters, hard, ok, iters, static_cast<cudaStream_t>(stream), &o);
   std::lock_guard<std::mutex> lk(c->mu);
-  return decode_impl(c, llr, frames, max_iters, hard, ok, iters, static_cast<cudaStream_t>(stream), opts);
+  return decode_impl(c, llr, frames, max_iters, hard, ok, iters, static_cast<cudaStream_t>(stream), &o);
 }
 
 nbldpc_status_t nbldpc_decode_pmf(nbldpc_code_t c, const float* pmf, int frames, int max_iters, uint8_t* hard,
@@ -1130,7 +1220,10 @@ nbldpc_status_t decode_host_impl(nbldpc_code_t c, const float* llr_host, int is_
   if (!c || frames < 1 || max_iters < 1 || !llr_host || !hard_host || !ok_host || !iters_host)
     return NBLDPC_ERR_INVALID_ARGUMENT;
   if (is_device_ptr(llr_host) || is_device_ptr(hard_host)) return NBLDPC_ERR_INVALID_ARGUMENT;
-  if (opts && opts->struct_size < sizeof(nbldpc_decode_opts_t)) return NBLDPC_ERR_INVALID_ARGUMENT;
+  nbldpc_decode_opts_t onorm;
+  if (!normalise_opts(opts, &onorm)) return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (onorm.workspace) return NBLDPC_ERR_UNSUPPORTED;  // the host entry points stage through the handle
+  opts = &onorm;
   std::lock_guard<std::mutex> lk(c->mu);
   NB_TRY(cudaSetDevice(c->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1138,21 +1231,10 @@ nbldpc_status_t decode_host_impl(nbldpc_code_t c, const float* llr_host, int is_
   const size_t row = (size_t)c->N * (is_pmf ? c->q : c->m);  // floats per frame
   const size_t llr_bytes = (size_t)frames * row * sizeof(float);
   const size_t out_bytes = align_up((size_t)frames * c->N, 256) + align_up(frames, 256) + (size_t)frames * 4;
-  if (w.llr_stage_bytes < llr_bytes) {
-    cudaStreamSynchronize(st);
-    cudaFree(w.llr_stage);
-    w.llr_stage = nullptr;
-    w.llr_stage_bytes = 0;
-    NB_TRY(cudaMalloc(&w.llr_stage, llr_bytes));
-    w.llr_stage_bytes = llr_bytes;
-  }
-  if (w.out_stage_bytes < out_bytes) {
-    cudaStreamSynchronize(st);
-    cudaFree(w.out_stage);
-    w.out_stage = nullptr;
-    w.out_stage_bytes = 0;
-    NB_TRY(cudaMalloc(&w.out_stage, out_bytes));
-    w.out_stage_bytes = out_bytes;
+  {  // stream-ordered growth of the device staging buffers
+    nbldpc_status_t rs = grow_buffer(w, &w.llr_stage, &w.llr_stage_bytes, llr_bytes, st);
+    if (rs == NBLDPC_OK) rs = grow_buffer(w, &w.out_stage, &w.out_stage_bytes, out_bytes, st);
+    if (rs != NBLDPC_OK) return rs;
   }
   uint8_t* hard_d = w.out_stage;
   uint8_t* ok_d = hard_d + align_up((size_t)frames * c->N, 256);
@@ -1171,16 +1253,15 @@ nbldpc_status_t decode_host_impl(nbldpc_code_t c, const float* llr_host, int is_
   // takes a frame of a later chunk waits for that chunk's flag (ld.acquire.gpu).
   using write_value_fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
   static write_value_fn write_value = nullptr;
-  static bool write_value_probed = false;
-  if (!write_value_probed) {
-    write_value_probed = true;
+  static std::once_flag write_value_once;  // handles on other threads probe concurrently
+  std::call_once(write_value_once, [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult qr;
     if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &qr) == cudaSuccess &&
         qr == cudaDriverEntryPointSuccess)
       write_value = reinterpret_cast<write_value_fn>(fn);
     cudaGetLastError();
-  }
+  });
   const bool cluster_path = c->colw2 && o.algorithm == NBLDPC_ALG_LOG_FOURIER && o.vn_algorithm == NBLDPC_VN_SEPARABLE &&
                             !o.symbol_post_out && !o.symbol_map_out;
   const int chunk = std::max(c->p_ncl, (frames + kMaxChunks - 1) / kMaxChunks);
@@ -1237,22 +1318,36 @@ nbldpc_status_t nbldpc_decode_pmf_host(nbldpc_code_t c, const float* pmf_host, i
   return decode_host_impl(c, pmf_host, 1, frames, max_iters, hard_host, ok_host, iters_host, stream, opts);
 }
 
-nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int iter, const float* w_in, float* w_out,
-                            float* u_out, uint8_t* hard, float* soft, int vn_algorithm, void* stream) {
-  if (!c || frames < 1 || iter < 0 || !is_device_ptr(llr) || !is_device_ptr(w_out)) return NBLDPC_ERR_INVALID_ARGUMENT;
+}  // extern "C"
+
+namespace {
+// pmf != NULL: nbldpc_step_pmf (the cluster kernel's symbol-pmf variant; llr unused)
+nbldpc_status_t step_impl(nbldpc_code_t c, const float* llr, const float* pmf, int frames, int iter, const float* w_in,
+                          float* w_out, float* u_out, uint8_t* hard, float* soft, int vn_algorithm, void* stream) {
+  if (!c || frames < 1 || iter < 0 || !is_device_ptr(pmf ? pmf : llr) || !is_device_ptr(w_out))
+    return NBLDPC_ERR_INVALID_ARGUMENT;
+  if (pmf && vn_algorithm != 0) return NBLDPC_ERR_UNSUPPORTED;  // the pass kernel keeps p only from l = 0 on
+  if (pmf && ((uintptr_t)pmf & 15)) return NBLDPC_ERR_INVALID_ARGUMENT;
   if (iter >= 1 && (!is_device_ptr(w_in) || !is_device_ptr(hard))) return NBLDPC_ERR_INVALID_ARGUMENT;
   if ((u_out && !is_device_ptr(u_out)) || (soft && !is_device_ptr(soft))) return NBLDPC_ERR_INVALID_ARGUMENT;
   if (vn_algorithm != 0 && vn_algorithm != 1) return NBLDPC_ERR_INVALID_ARGUMENT;
   if (!c->row_regular || !c->colw2) return NBLDPC_ERR_UNSUPPORTED;  // internal slots == canonical order only then
+  if (vn_algorithm == 0 && !c->cluster_ok) return NBLDPC_ERR_UNSUPPORTED;
   std::lock_guard<std::mutex> lk(c->mu);
   NB_TRY(cudaSetDevice(c->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  nbldpc_status_t rs = ensure_workspace(c, frames);
+  nbldpc_status_t rs = ensure_workspace(c, frames, st);
   if (rs != NBLDPC_OK) return rs;
   Workspace& w = c->ws;
   const size_t msg = (size_t)frames * c->E * c->q * sizeof(float);
   CallDev call{};
   call.llr = llr;
+  if (pmf) {
+    rs = grow_buffer(w, &w.p0buf, &w.p0buf_bytes, (size_t)frames * c->N * c->q * sizeof(float), st);
+    if (rs != NBLDPC_OK) return rs;
+    call.pmf = pmf;
+    call.p0buf = w.p0buf;
+  }
   call.frames = frames;
   call.max_iters = 1 << 30;
   call.mode = 0;
@@ -1260,8 +1355,10 @@ nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int i
   call.want_soft = soft != nullptr;
   nb::nb_step_setup_kernel<<<(frames + 255) / 256, 256, 0, st>>>(w.dev, call, iter);
   NB_TRY(cudaGetLastError());
-  nb::nb_tanh_kernel<<<256, 256, 0, st>>>(llr, w.dev.Tt, (size_t)frames * c->N, c->m);
-  NB_TRY(cudaGetLastError());
+  if (!pmf) {
+    nb::nb_tanh_kernel<<<256, 256, 0, st>>>(llr, w.dev.Tt, (size_t)frames * c->N, c->m);
+    NB_TRY(cudaGetLastError());
+  }
   // the direct pass kernel selects buffers by iteration parity, the persistent one by epoch (0)
   const int in_buf = vn_algorithm ? (iter & 1) : 0;
   float* wcur = w.dev.W + (size_t)in_buf * frames * c->E * c->q;
@@ -1269,8 +1366,8 @@ nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int i
   if (iter >= 1) {
     if (vn_algorithm) {
       NB_TRY(cudaMemcpyAsync(wcur, w_in, msg, cudaMemcpyDeviceToDevice, st));
-    } else {  // the cluster kernel keeps messages in its chunk-swizzled order
-      NB_TRY(launch_layout(c, w_in, wcur, frames, 1, st));
+    } else {  // the cluster kernel keeps messages in its chunk-swizzled order (linear unless soft outputs)
+      NB_TRY(launch_layout(c, w_in, wcur, frames, 1, soft == nullptr && c->m >= 7, st));
     }
   }
   if (vn_algorithm) {
@@ -1278,12 +1375,12 @@ nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int i
     NB_TRY(launch_pass(c, P, 1, st));
   } else {
     nb::ClusterParams PP = make_cparams(c, 1, iter, u_out);
-    NB_TRY(launch_cluster(c, PP, std::min(frames, c->p_ncl), st));
+    NB_TRY(launch_cluster(c, PP, std::min(frames, c->p_ncl), st, pmf != nullptr, 0, 0, soft != nullptr));
   }
   if (vn_algorithm) {
     NB_TRY(cudaMemcpyAsync(w_out, wnxt, msg, cudaMemcpyDeviceToDevice, st));
   } else {
-    NB_TRY(launch_layout(c, wnxt, w_out, frames, 0, st));
+    NB_TRY(launch_layout(c, wnxt, w_out, frames, 0, soft == nullptr && c->m >= 7, st));
   }
   if (iter >= 1) {
     NB_TRY(cudaMemcpyAsync(hard, w.dev.xhat, (size_t)frames * c->N, cudaMemcpyDeviceToDevice, st));
@@ -1291,7 +1388,20 @@ nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int i
       NB_TRY(cudaMemcpyAsync(soft, w.dev.soft, (size_t)frames * c->N * c->m * sizeof(float), cudaMemcpyDeviceToDevice,
                              st));
   }
-  return NBLDPC_OK;
+  return mark_done(w, st);
+}
+}  // namespace
+
+extern "C" {
+
+nbldpc_status_t nbldpc_step(nbldpc_code_t c, const float* llr, int frames, int iter, const float* w_in, float* w_out,
+                            float* u_out, uint8_t* hard, float* soft, int vn_algorithm, void* stream) {
+  return step_impl(c, llr, nullptr, frames, iter, w_in, w_out, u_out, hard, soft, vn_algorithm, stream);
+}
+
+nbldpc_status_t nbldpc_step_pmf(nbldpc_code_t c, const float* pmf, int frames, int iter, const float* w_in,
+                                float* w_out, float* u_out, uint8_t* hard, float* soft, void* stream) {
+  return step_impl(c, nullptr, pmf, frames, iter, w_in, w_out, u_out, hard, soft, 0, stream);
 }
 
 }  // extern "C"

@@ -79,6 +79,18 @@ def message_mismatch(gs, gl, os_, ol, ln_tol=1e-3, lin_tol=1e-4):
     return ~(ok_val & sign_ok)
 
 
+def soft_mismatch(g, ref, ln_tol=1e-3, lin_tol=1e-4, ln_floor=-5.0):
+    """The north-star bar on posterior bit log-magnitudes soft = ln|M_v(alpha^i)/M_v(0)| (BASELINE.json
+    north_star): within ``ln_tol`` in ln wherever the oracle's value is >= ln_floor,
+    elsewhere within ``lin_tol`` in linear value.  Returns the boolean mask of failing entries."""
+    g = np.asarray(g, np.float64)
+    ref = np.asarray(ref, np.float64)
+    with np.errstate(over="ignore", invalid="ignore"):
+        dln = np.abs(g - ref)
+        dlin = np.abs(np.exp(g) - np.exp(ref))
+    return np.where(ref >= ln_floor, ~(dln <= ln_tol), ~(dlin <= lin_tol))
+
+
 def stable_frames(ocode, llr, max_iters, mode=0):
     """Oracle f64 results plus the stable-frame mask (f64 and f32 twins agree; reading R20)."""
     a = ocode.lf_decode_batch(llr, max_iters, mode=mode)
@@ -93,6 +105,7 @@ def fail_trajectory_stable(decode, x_row, max_iters, **kw):
     as stable -- a chaotic non-converged frame can coincide at the last iteration by chance (C5 at
     4.5 dB: frame 1999 agrees at 50 and 49 iterations, differs by 2 symbols at 30, 40 and 45).
     ``decode`` is the oracle's batch decode (lf_decode_batch, lf_decode_batch_pmf or ls_decode_batch)."""
+    kw = {k: v for k, v in kw.items() if k != "early_stop"}
     for it in (max_iters - 5, max_iters - 10):
         if it < 1:
             continue
@@ -102,3 +115,28 @@ def fail_trajectory_stable(decode, x_row, max_iters, **kw):
             return False
     return True
 
+
+
+def assert_stable_parity(decode, x, out, ref, max_iters, max_unstable_frac=0.1, what="", also=None, **kw):
+    """The stable-frame protocol (reading R20): every frame whose fp64 and fp32 oracle
+    trajectories agree must be bit-identical (hard symbols, syndrome flag, iterations) on the GPU;
+    differing frames must be unstable ones and at most ``max_unstable_frac`` of the sample.
+    ``decode`` is the oracle's batch decode (lf_decode_batch / lf_decode_batch_pmf / ls_decode_batch),
+    ``x`` its input rows, ``out`` numpy GPU outputs {hard, ok, iters}, ``ref`` the oracle's (fp64) result.
+    ``also``: further decodes (callables of the rows) that must agree with ``ref`` too for a frame to count
+    as stable -- e.g. O-LF without the half-precision store for the F16 path (reading R26).
+    Returns the number of (unstable) differing frames."""
+    hard, ok, it = out["hard"], out["ok"], out["iters"]
+    same = (hard == ref["hard"]).all(1) & (ok == ref["ok"]) & (it == ref["iters"])
+    bad = np.where(~same)[0]
+    if bad.size:
+        twins = [decode(x[bad], max_iters, f32=True, **kw)] + [fn(x[bad]) for fn in (also or [])]
+        for n, b in enumerate(bad):
+            stable = all(np.array_equal(tw["hard"][n], ref["hard"][b]) and tw["ok"][n] == ref["ok"][b]
+                         and tw["iters"][n] == ref["iters"][b] for tw in twins)
+            if stable and ref["ok"][b] == 0:
+                stable = fail_trajectory_stable(decode, x[b], max_iters, **kw)
+            assert not stable, (f"{what}: stable frame {b} differs: gpu iters {it[b]} ok {ok[b]} vs oracle "
+                                f"{ref['iters'][b]} {ref['ok'][b]}, {int((hard[b] != ref['hard'][b]).sum())} symbols")
+    assert bad.size <= max(1, int(max_unstable_frac * len(hard))), (what, bad.size, len(hard))
+    return int(bad.size)

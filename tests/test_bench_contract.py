@@ -29,7 +29,8 @@ def test_roofline_model_c2():
 
     cfg = synth.CONFIGS["C2"]
     mufu, fma, byts = bench.per_frame_iter(cfg, 0)
-    assert mufu == 2 * 2048 * 64 + 1024 * 64  # 2 E q + N q
+    assert mufu == 2 * 2048 * 64 + 1024 * 64  # packed log messages at q = 64: 2 E q + N q
+    assert bench.per_frame_iter(synth.CONFIGS["C4"], 0)[0] == 4096  # linear messages at q = 256: 1 rcp per edge
     assert fma == 2048 * 6 * 64 + 1024 * 7 * 64  # separable VN + the decision points
     assert byts == 2 * 2048 * 64 * 4 + 4 * 1024 * 6 + 1024  # one message set read + written, channel, symbols
     r = bench.roofline(cfg, 0, frame_iters=1000, seconds=1000 * 427e-9, traffic=None)

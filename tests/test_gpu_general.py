@@ -11,7 +11,7 @@ torch = pytest.importorskip("torch")
 import oracle
 import synth
 from helpers import DEFAULT_POLY
-from parity import config_inputs, fail_trajectory_stable, oracle_code
+from parity import soft_mismatch, config_inputs, fail_trajectory_stable, oracle_code
 
 pytestmark = pytest.mark.gpu
 VN_GENERAL = 2
@@ -112,10 +112,8 @@ def test_general_mixed_weights_soft_posterior_pmf(dev):
         ref = ocode.lf_decode_batch(llr, iters, early_stop=False, want_soft=True, want_post=True)
         twin = ocode.lf_decode_batch(llr, iters, early_stop=False, want_soft=True, want_post=True, f32=True)
         soft = o["soft"].cpu().numpy()
-        big = ref["soft"] > -5.0
-        eg = np.abs(soft[big] - ref["soft"][big]).max()
-        et = np.abs(twin["soft"][big] - ref["soft"][big]).max()
-        assert eg <= max(1e-3, 2.0 * et), (iters, eg, et)
+        bad = soft_mismatch(soft, ref["soft"])  # the north-star bar (fp64 decision for soft outputs)
+        assert not bad.any(), (iters, int(bad.sum()))
         post = o["post"].cpu().numpy()
         ep = np.abs(post - ref["post"]).max()
         etp = np.abs(twin["post"] - ref["post"]).max()

@@ -12,7 +12,7 @@ torch = pytest.importorskip("torch")
 import oracle
 import synth
 from helpers import DEFAULT_POLY
-from parity import config_inputs, fail_trajectory_stable, oracle_code
+from parity import assert_stable_parity, config_inputs, fail_trajectory_stable, oracle_code
 
 pytestmark = pytest.mark.gpu
 
@@ -120,8 +120,10 @@ def test_logsp_options_and_errors(dev):
     assert (o["iters"] == 1).all()
     o = code.decode(x, 5, algorithm=ALG_LOG_SP, early_stop=False)
     assert (o["iters"] == 5).all()
-    ref = oracle_code(name).ls_decode_batch(llr, 5, early_stop=False)
-    assert (o["hard"].cpu().numpy() == ref["hard"]).all(1).mean() >= 0.9
+    ocode = oracle_code(name)
+    ref = ocode.ls_decode_batch(llr, 5, early_stop=False)
+    assert_stable_parity(ocode.ls_decode_batch, llr, {k: v.cpu().numpy() for k, v in o.items()}, ref, 5,
+                         max_unstable_frac=0.25, what="Log-SP, 5 iterations, no early stop", early_stop=False)
     # end to end with host buffers
     h = code.decode_host(torch.from_numpy(llr).pin_memory(), c["max_iters"], algorithm=ALG_LOG_SP)
     d = code.decode(x, c["max_iters"], algorithm=ALG_LOG_SP)

@@ -14,7 +14,7 @@ torch = pytest.importorskip("torch")
 import oracle
 import synth
 from parity import (config_inputs, fail_trajectory_stable, message_mismatch, oracle_code, oracle_to_packed,
-                    packed_to_oracle)
+                    packed_to_oracle, soft_mismatch, assert_stable_parity)
 
 pytestmark = pytest.mark.gpu
 
@@ -67,8 +67,8 @@ DECODE_CASES = [
     # name, point, gpu frames, oracle sample size
     ("C1", 0, 64, 64),
     ("C2", 0, 4096, 24),
-    ("C3", 0, 512, 8),
-    ("C4", 0, 64, 3),
+    ("C3", 0, 512, 16),
+    ("C4", 0, 1024, 16),
     ("C5", 0, 256, 8),   # 3.0 dB: every frame runs all 50 iterations
     ("C5", 3, 256, 16),  # 4.5 dB
     ("C5", 4, 256, 16),  # 5.0 dB
@@ -105,14 +105,14 @@ def _decode_parity(dev, name, point, F, nsample, vn):
         assert bool(okg[f]) == ocode.syndrome(hard[f])[0]
 
 
-@pytest.mark.parametrize("name", ["C1", "C5"])
-def test_paper_syndrome_mode_parity(dev, name):
+@pytest.mark.parametrize("name,nsample", [("C1", 64), ("C5", 16), ("C2", 16), ("C3", 8)])
+def test_paper_syndrome_mode_parity(dev, name, nsample):
     c = synth.CONFIGS[name]
     point = 4 if name == "C5" else 0
     _, llr, _ = config_inputs(name, 0, 64, point=point)
     out = gpu_code(name).decode(torch.from_numpy(llr).to(dev), c["max_iters"], syndrome_mode=1)
     torch.cuda.synchronize()
-    idx = np.arange(64) if name == "C1" else np.arange(0, 64, 4)
+    idx = np.arange(0, 64, 64 // nsample)
     n, unstable = compare_decode(name, out, llr, idx, c["max_iters"], mode=1)
     assert unstable <= max(1, n // 10)
 
@@ -128,18 +128,47 @@ def _oracle_state(ocode, llr_row, iters):
     return S0, L0, Ws, Wl
 
 
-@pytest.mark.parametrize("vn", [0, 1])
-@pytest.mark.parametrize("name,point", [("C1", 0), ("C5", 3), ("C2", 0), ("C3", 0)])
-@pytest.mark.parametrize("ell", [1, 2, 3])
-def test_step_parity(dev, name, point, ell, vn):
+# a GF(8) code (q = 8: one thread per edge holding all 8 entries) for the step parity
+G8 = dict(name="G8", m=3, poly=0xB, k=4, N=96, q=8, ebn0=[1.5], rate=0.5, seed=4242)
+
+
+def _step_inputs(name, F, point):
+    """(config, llr [F, N*m], oracle code, GPU code) for a step-parity case."""
+    import paper_1008_4370_b200 as nb
+
+    if name == "G8":
+        c = G8
+        M, rows, cols, coeffs = synth.make_regular_code(c["N"], c["k"], c["m"], c["seed"])
+        llr = synth.awgn_llr(c["N"] * c["m"], 0, F, synth.sigma2_for(c["ebn0"][0], c["rate"]), c["seed"] + 1)
+        return (c, llr, oracle.Code(oracle.Field(c["m"], c["poly"]), M, c["N"], rows, cols, coeffs),
+                nb.Code(c["m"], c["poly"], M, c["N"], rows, cols, coeffs))
     c = synth.CONFIGS[name]
-    F = 2
     _, llr, _ = config_inputs(name, 0, F, point=point)
-    ocode = oracle_code(name)
-    code = gpu_code(name)
-    w_in = []
-    refs = []
-    twins = []
+    return c, llr, oracle_code(name), gpu_code(name)
+
+
+STEP_CASES = [("C1", 0, 1, 2), ("G8", 0, 1, 2), ("C5", 3, 1, 2), ("C2", 0, 1, 2), ("C3", 0, 1, 2),
+              ("C1", 0, 2, 2), ("G8", 0, 2, 2), ("C5", 3, 2, 2), ("C2", 0, 2, 2), ("C3", 0, 2, 2), ("C4", 0, 2, 1),
+              ("C1", 0, 3, 2), ("G8", 0, 3, 2), ("C5", 3, 3, 2), ("C2", 0, 3, 2), ("C3", 0, 3, 2)]
+# the cluster kernel also at the fourth iteration of GF(256) (the most ill-conditioned decision sums);
+# the direct-convolution pass kernel (vn = 1, the paper's q^2-term CONV, a comparison kernel) sums q
+# fp32 products per entry and misses 1e-3 on a few U entries there (DESIGN.md 8), so only up to l = 3
+STEP_PARAMS = ([(n, p, e, F, 0) for n, p, e, F in STEP_CASES + [("C3", 0, 4, 2)]] +
+               [(n, p, e, F, 1) for n, p, e, F in STEP_CASES])
+
+
+@pytest.mark.parametrize("name,point,ell,F,vn", STEP_PARAMS)
+def test_step_parity(dev, name, point, ell, F, vn):
+    """One iteration from the oracle's state W^(ell), rounded to the packed f32 format (nbldpc_step):
+    * U within 1e-3 ln or 1e-4 linear of the oracle's U computed from the same rounded state;
+    * the check node in isolation: W^(ell+1) within (k-1) 1e-3 ln / 1e-4 linear of the oracle's check
+      node applied to the GPU's own U (k-1 log-magnitudes are summed);
+    * W^(ell+1) from the GPU's U within (k-1) 1e-3 of the oracle's (U errors add up over k-1 terms);
+    * posterior bit log-magnitudes (soft) under the north-star bar: 1e-3 ln where ln >= -5, else
+      1e-4 linear (the fp64 decision of soft outputs, decision_f64, reading R22);
+    * hard decisions equal wherever every bit is away from a tie."""
+    c, llr, ocode, code = _step_inputs(name, F, point)
+    w_in, refs = [], []
     for f in range(F):
         S0, L0, Ws, Wl = _oracle_state(ocode, llr[f], ell)
         packed = oracle_to_packed(Ws, Wl)
@@ -148,45 +177,37 @@ def test_step_parity(dev, name, point, ell, vn):
         Ws32, Wl32 = packed_to_oracle(packed)
         Us, Ul, _ = ocode.lf_variable_to_check(S0, L0, Ws32, Wl32)
         x, soft, _ = ocode.lf_decision(S0, L0, Ws32, Wl32)
-        S032, L032 = ocode.lf_init(llr[f].astype(np.float64), f32=True)
-        _, soft32, _ = ocode.lf_decision(S032, L032, Ws32, Wl32.astype(np.float32), f32=True)
-        twins.append(soft32.astype(np.float64))
         Wn_s, Wn_l = ocode.lf_check_to_variable(Us, Ul)
         refs.append((Us, Ul, x, soft, Wn_s, Wn_l))
     w_in = torch.from_numpy(np.stack(w_in)).to(dev)
-    res = code.step(torch.from_numpy(llr).to(dev), ell, w_in, want_u=True, want_soft=True, vn_algorithm=vn)
+    x = torch.from_numpy(llr).to(dev)
+    # with soft outputs the step runs the soft-output instantiation (packed log messages, fp64 decision);
+    # without, the hot-path instantiation (linear messages): both are checked
+    runs = [(True, code.step(x, ell, w_in, want_u=True, want_soft=True, vn_algorithm=vn)),
+            (False, code.step(x, ell, w_in, want_u=True, want_soft=False, vn_algorithm=vn))]
     torch.cuda.synchronize()
-    for f in range(F):
-        Us, Ul, x, soft, Wn_s, Wn_l = refs[f]
-        gs, gl = packed_to_oracle(res["u"][f].cpu().numpy())
-        bad_u = message_mismatch(gs, gl, Us, Ul)
-        assert bad_u.sum() == 0, f"U: {bad_u.sum()} of {bad_u.size} entries off"
-        gs, gl = packed_to_oracle(res["w"][f].cpu().numpy())
-        bad_w = message_mismatch(gs, gl, Wn_s, Wn_l, ln_tol=2e-3 * (c["k"] - 1), lin_tol=1e-4)
-        assert bad_w.sum() == 0, f"W: {bad_w.sum()} of {bad_w.size} entries off"
-        gsoft = res["soft"][f].cpu().numpy().reshape(c["N"], c["m"])
-        # posterior bit log-magnitudes soft = ln|M_v(alpha^i)/M_v(0)| (reading R22):
-        #  * every entry within 1e-3 in ln or 1e-4 in linear value, or no further from the fp64 oracle
-        #    than the paper's own algorithm evaluated in fp32 (the oracle's f32 twin) on the same inputs;
-        #  * at q = 256 from the third iteration on, where fp32 cancellation in the decision sums is
-        #    largest (the f32 twin itself misses 1e-3 on ~10 entries per frame), the bar is aggregate:
-        #    no more failing entries and no larger worst error than the f32 twin.
-        dln = np.abs(gsoft - soft)
-        dlin = np.abs(np.exp(gsoft.astype(np.float64)) - np.exp(soft))
-        twin_err = np.abs(twins[f] - soft)
-        twin_dlin = np.abs(np.exp(twins[f]) - np.exp(soft))
-        bad = (dln > np.maximum(1e-3, twin_err)) & (dlin > 1e-4)
-        if vn == 1 and c["q"] == 256:  # direct q^2-term fp32 convolution: more cancellation
-            bad &= dln > np.maximum(5e-3, twin_err)
-        if c["q"] == 256 and ell >= 3:
-            twin_bad = (twin_err > 1e-3) & (twin_dlin > 1e-4)
-            assert bad.sum() <= max(1, twin_bad.sum()), (int(bad.sum()), int(twin_bad.sum()))
-            assert dln[soft > -5].max(initial=0) <= max(1e-3, twin_err[soft > -5].max(initial=0))
-        else:
-            assert not bad.any(), f"soft: {int(bad.sum())} entries off, worst dln {dln[bad].max()}"
-        hard = res["hard"][f].cpu().numpy()
-        sure = (soft > -12.0).all(1)
-        assert np.array_equal(hard[sure], x[sure])
+    k1 = c["k"] - 1
+    for soft_run, res in runs:
+        for f in range(F):
+            Us, Ul, x_ref, soft, Wn_s, Wn_l = refs[f]
+            what = f"{'soft' if soft_run else 'plain'} kernel, frame {f}"
+            gus, gul = packed_to_oracle(res["u"][f].cpu().numpy())
+            bad_u = message_mismatch(gus, gul, Us, Ul)
+            assert bad_u.sum() == 0, f"{what}: U: {bad_u.sum()} of {bad_u.size} entries off"
+            gs, gl = packed_to_oracle(res["w"][f].cpu().numpy())
+            cn_s, cn_l = ocode.lf_check_to_variable(gus, gul)  # the oracle's check node on the GPU's U
+            bad_cn = message_mismatch(gs, gl, cn_s, cn_l, ln_tol=1e-3 * k1, lin_tol=1e-4)
+            assert bad_cn.sum() == 0, f"{what}: check node: {bad_cn.sum()} of {bad_cn.size} entries off"
+            bad_w = message_mismatch(gs, gl, Wn_s, Wn_l, ln_tol=1e-3 * k1, lin_tol=1e-4)
+            assert bad_w.sum() == 0, f"{what}: W: {bad_w.sum()} of {bad_w.size} entries off"
+            hard = res["hard"][f].cpu().numpy()
+            sure = (soft > -12.0).all(1)
+            assert np.array_equal(hard[sure], x_ref[sure]), what
+            if soft_run:
+                gsoft = res["soft"][f].cpu().numpy().reshape(c["N"], c["m"])
+                bad = soft_mismatch(gsoft, soft)
+                assert not bad.any(), (f"{what}: soft: {int(bad.sum())} entries off, worst dln "
+                                       f"{np.abs(gsoft - soft)[bad].max(initial=0):.2e}")
 
 
 def test_invariance_slots_graph_batch(dev):
@@ -217,8 +238,39 @@ def test_workspace_accounting(dev):
     c = synth.CONFIGS["C2"]
     assert sb >= 2 * code.E * c["q"] * 4  # the two message sets of a resident frame
     w1, wbig = code.workspace_bytes(1), code.workspace_bytes(1 << 20)
-    assert sb <= w1 < 2 * sb and wbig > w1 and (wbig - w1) % sb == 0
-    assert code.workspace_bytes(0) == 0
+    assert sb <= w1 < 2 * sb and wbig > w1
+    S = round((wbig - w1) / sb) + 1  # resident clusters
+    assert S >= 100 and S * sb <= wbig <= S * sb + 64 * 1024
+
+
+def test_caller_workspace_concurrent_streams(dev):
+    """nbldpc_decode_opts_t::workspace: decodes with their own workspaces on two streams at once give
+    the same results as the handle-workspace decode; a too-small workspace is rejected."""
+    import paper_1008_4370_b200 as nb
+
+    name = "C2"
+    c = synth.CONFIGS[name]
+    _, llr, _ = config_inputs(name, 0, 600)
+    x = torch.from_numpy(llr).to(dev)
+    code = gpu_code(name)
+    base = code.decode(x, c["max_iters"])
+    torch.cuda.synchronize()
+    halves = (x[:300].contiguous(), x[300:].contiguous())
+    nbytes = code.workspace_bytes(300)
+    wss = [torch.empty(nbytes + 256, dtype=torch.uint8, device=dev) for _ in range(2)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    for h, ws, s in zip(halves, wss, streams):
+        with torch.cuda.stream(s):
+            outs.append(code.decode(h, c["max_iters"], workspace=ws, stream=s))
+    torch.cuda.synchronize()
+    for k in ("hard", "ok", "iters"):
+        assert torch.equal(torch.cat([outs[0][k], outs[1][k]]), base[k]), k
+    with pytest.raises(nb.NbldpcError):
+        code.decode(halves[0], c["max_iters"], workspace=wss[0][: nbytes // 2])
+    with pytest.raises(nb.NbldpcError):  # not on the cluster kernel
+        code.decode(halves[0], c["max_iters"], workspace=wss[0], vn_algorithm=1)
+
 
 
 def test_decode_host_matches_device(dev):
@@ -256,9 +308,8 @@ def test_binary_code_and_small_fields(dev):
         llr = synth.awgn_llr(N * m, 0, 48, synth.sigma2_for(2.0, 1 - 2 / k), 77 + m)
         out = code.decode(torch.from_numpy(llr).to(dev), 20)
         ref = ocode.lf_decode_batch(llr, 20)
-        same = ((out["hard"].cpu().numpy() == ref["hard"]).all(1) & (out["ok"].cpu().numpy() == ref["ok"])
-                & (out["iters"].cpu().numpy() == ref["iters"]))
-        assert same.mean() >= 0.95, (m, same.mean())
+        assert_stable_parity(ocode.lf_decode_batch, llr, {k: v.cpu().numpy() for k, v in out.items()}, ref, 20,
+                             what=f"m={m}")
 
 
 def test_edge_cases_and_errors(dev):
@@ -328,9 +379,8 @@ def test_irregular_check_degrees_and_cycle_codes(dev, vn):
         out = code.decode(torch.from_numpy(llr).to(dev), 15, vn_algorithm=vn)
         torch.cuda.synchronize()
         ref = ocode.lf_decode_batch(llr, 15)
-        same = ((out["hard"].cpu().numpy() == ref["hard"]).all(1) & (out["ok"].cpu().numpy() == ref["ok"])
-                & (out["iters"].cpu().numpy() == ref["iters"]))
-        assert same.mean() >= 0.95, (m, degs[:4], same.mean())
+        assert_stable_parity(ocode.lf_decode_batch, llr, {k: v.cpu().numpy() for k, v in out.items()}, ref, 15,
+                             what=f"m={m} degs {degs[:4]}")
 
 
 def test_largest_check_team_and_empty_batches(dev):

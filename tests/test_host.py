@@ -106,13 +106,38 @@ def test_null_handles_are_rejected(L):
 def test_frame_range_partitions_frames():
     from paper_1008_4370_b200 import shard
 
+    # weak: F per rank
     seen = []
     for r in range(8):
-        a, b = shard.frame_range(r, 8, 2048)
+        a, b = shard.frame_range(r, 8, 2048, "weak")
         seen.extend(range(a, b))
     assert seen == list(range(8 * 2048))
+    # strong: a fixed global batch in contiguous 256-frame-chunk-aligned shards
+    for F, G in ((16384, 1), (16384, 2), (16384, 4), (16384, 8), (65536, 8), (1000, 3), (300, 2), (4096, 3)):
+        rs = [shard.frame_range(r, G, F, "strong") for r in range(G)]
+        assert rs[0][0] == 0 and rs[-1][1] == F
+        assert all(rs[i][1] == rs[i + 1][0] for i in range(G - 1))
+        assert all(a % 256 == 0 for a, _ in rs)
+        if F % (256 * G) == 0:
+            assert all(b - a == F // G for a, b in rs)
     with pytest.raises(ValueError):
         shard.frame_range(2, 2, 16)
+    with pytest.raises(ValueError):
+        shard.frame_range(0, 2, 16, "diagonal")
+
+
+def test_error_counts_against_sent_codeword():
+    from paper_1008_4370_b200 import shard
+
+    hard = torch.zeros((4, 5), dtype=torch.uint8)
+    hard[1, 2] = 0b101  # one symbol, two bits wrong, frame flagged converged -> undetected
+    hard[2, 0], hard[2, 4] = 1, 0xFF  # two symbols, 9 bits
+    ok = torch.tensor([1, 1, 0, 0], dtype=torch.uint8)
+    c = shard.error_counts(hard, ok, events=torch.tensor([0, 2, 0, 1], dtype=torch.int32))
+    assert c == {"frames": 4, "ok": 2, "frame_err": 2, "sym_err": 3, "bit_err": 11, "undetected": 1, "events": 3}
+    sent = hard.clone()
+    c = shard.error_counts(hard, ok, sent)
+    assert c["frame_err"] == c["sym_err"] == c["bit_err"] == c["undetected"] == 0
 
 
 def test_llr_shards_do_not_depend_on_sharding():
@@ -123,6 +148,12 @@ def test_llr_shards_do_not_depend_on_sharding():
         per = 600 // world
         parts = [synth.config_llr("C5", r * per, per, point=3) for r in range(world)]
         assert np.array_equal(np.concatenate(parts), whole[: per * world])
+    for world in (2, 3):  # strong-scaling shards (chunk-aligned)
+        from paper_1008_4370_b200 import shard
+
+        parts = [synth.config_llr("C5", *(lambda a, b: (a, b - a))(*shard.frame_range(r, world, 600, "strong")),
+                                  point=3) for r in range(world)]
+        assert np.array_equal(np.concatenate(parts), whole)
 
 
 def _free_port():
@@ -133,27 +164,52 @@ def _free_port():
     return p
 
 
+C1_FRAMES, C1_CHUNK = 60, 16
+
+
+def _c1_sent(f0, f1):
+    from parity import config_inputs
+
+    _, llr, xs = config_inputs("C1", f0, f1 - f0)
+    return llr, xs
+
+
 def _gloo_worker(rank, world, port, q):
+    """One rank of the N>1 path on CPU: decode ITS strong-scaling shard of C1 (the fp64 oracle
+    stands in for the GPU kernel here; the GPU version is tests/test_gpu_shard.py), count errors
+    against the sent codewords, reduce the counter vector and the max time, all-gather the outputs."""
     import torch.distributed as dist
 
     from paper_1008_4370_b200 import shard
+    from parity import oracle_code
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        a, b = shard.frame_range(rank, world, 40)
-        llr = synth.config_llr("C2", a, b - a)
-        # stand-in for a rank's decode: per-frame "iterations" derived from its own inputs only
-        iters = (np.abs(llr).sum(1) % 7).astype(np.int64) + 1
-        c, t = shard.reduce_stats({"frame_iters": int(iters.sum()), "frames": b - a, "ok": rank},
-                                  {"ms": 10.0 + rank}, dist)
-        q.put((rank, c, t, iters.tolist()))
+        a, b = shard.frame_range(rank, world, C1_FRAMES, "strong", chunk=C1_CHUNK)
+        llr, xs = _c1_sent(a, b)
+        r = oracle_code("C1").lf_decode_batch(llr, synth.CONFIGS["C1"]["max_iters"], nthreads=1)
+        hard, ok, it = (torch.from_numpy(np.ascontiguousarray(r[k])) for k in ("hard", "ok", "iters"))
+        cnt = shard.error_counts(hard.to(torch.uint8), ok, torch.from_numpy(xs))
+        cnt["frame_iters"] = int(it.sum())
+        c, t = shard.reduce_stats(cnt, {"ms": 10.0 + rank}, dist)
+        sizes = [shard.frame_range(g, world, C1_FRAMES, "strong", chunk=C1_CHUNK) for g in range(world)]
+        sizes = [y - x for x, y in sizes]
+        g_hard = shard.gather_rows(hard.to(torch.int32), dist, sizes)
+        g_ok = shard.gather_rows(ok.to(torch.int32), dist, sizes)
+        g_it = shard.gather_rows(it.to(torch.int32), dist, sizes)
+        q.put((rank, c, t, g_hard.numpy(), g_ok.numpy(), g_it.numpy()))
     finally:
         dist.destroy_process_group()
 
 
-def test_gloo_world2_sharding_and_reduction():
+def test_gloo_world2_sharded_decode_and_reduction():
+    """Two gloo ranks decode their shards; the all-gathered outputs and the reduced counters are
+    identical to a single-process decode of the whole batch."""
     import torch.multiprocessing as mp
+
+    from paper_1008_4370_b200 import shard
+    from parity import oracle_code
 
     world, port = 2, _free_port()
     ctx = mp.get_context("spawn")
@@ -161,15 +217,18 @@ def test_gloo_world2_sharding_and_reduction():
     procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=120) for _ in range(world)]
+    res = [q.get(timeout=300) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    res.sort()
-    # the single-process computation over all 80 frames
-    llr = synth.config_llr("C2", 0, 80)
-    iters = (np.abs(llr).sum(1) % 7).astype(np.int64) + 1
-    assert res[0][3] + res[1][3] == iters.tolist()
-    for _, c, t, _ in res:
-        assert c == {"frame_iters": float(iters.sum()), "frames": 80.0, "ok": 1.0}
+    res.sort(key=lambda x: x[0])
+    llr, xs = _c1_sent(0, C1_FRAMES)
+    r = oracle_code("C1").lf_decode_batch(llr, synth.CONFIGS["C1"]["max_iters"], nthreads=1)
+    want = shard.error_counts(torch.from_numpy(r["hard"].astype(np.uint8)), torch.from_numpy(r["ok"]),
+                              torch.from_numpy(xs))
+    want["frame_iters"] = int(r["iters"].sum())
+    for _, c, t, gh, gok, git in res:
+        assert c == want
         assert t == {"ms": 11.0}
+        assert np.array_equal(gh, r["hard"]) and np.array_equal(gok, r["ok"]) and np.array_equal(git, r["iters"])
+    assert want["frame_err"] > 0  # the sample exercises the error counters (C1 at 2 dB has failures)
