@@ -884,6 +884,9 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           load_wo();
 #endif
           float* DB = st;
+          // two teams per warp (q = 256): their rows are 1 KB apart (the same banks), so the odd team's D words
+          // are XOR-ed by 16 (the other half of the banks) -- the scalar D stores no longer collide
+          const int dbx = (TT == 16 && (trow & 1)) ? 16 : 0;
           if constexpr (TT > 1) __syncwarp();  // transposition reads done
           if constexpr (F16) {
             if (is_a) {
@@ -905,14 +908,14 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
                 // z = 16 t + w: tB = w >> LJ, rB = (w & (2^LJ - 1)) | t << LJ; runs of 2^LJ entries stay
                 // contiguous in a D row, so store them as one vector
                 if constexpr (LJ >= 2) {
-                  *reinterpret_cast<float4*>(DB + db_word(ch >> (LJ - 2), ((4 * ch) & ((1 << LJ) - 1)) | (t << LJ))) =
+                  *reinterpret_cast<float4*>(DB + (dbx ^ db_word(ch >> (LJ - 2), ((4 * ch) & ((1 << LJ) - 1)) | (t << LJ)))) =
                       make_float4(d4[0], d4[1], d4[2], d4[3]);
                 } else if constexpr (LJ == 1) {
-                  *reinterpret_cast<float2*>(DB + db_word(2 * ch, t << 1)) = make_float2(d4[0], d4[1]);
-                  *reinterpret_cast<float2*>(DB + db_word(2 * ch + 1, t << 1)) = make_float2(d4[2], d4[3]);
+                  *reinterpret_cast<float2*>(DB + (dbx ^ db_word(2 * ch, t << 1))) = make_float2(d4[0], d4[1]);
+                  *reinterpret_cast<float2*>(DB + (dbx ^ db_word(2 * ch + 1, t << 1))) = make_float2(d4[2], d4[3]);
                 } else {
 #pragma unroll
-                  for (int k4 = 0; k4 < 4; ++k4) DB[db_word(4 * ch + k4, t)] = d4[k4];
+                  for (int k4 = 0; k4 < 4; ++k4) DB[dbx ^ db_word(4 * ch + k4, t)] = d4[k4];
                 }
               }
             } else if constexpr (R >= 4) {
@@ -941,7 +944,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             if constexpr (TT > 1) {
 #pragma unroll
               for (int ch = 0; ch < 4; ++ch) {
-                const float4 v4 = *reinterpret_cast<const float4*>(DB + db_word(t, 4 * ch));
+                const float4 v4 = *reinterpret_cast<const float4*>(DB + (dbx ^ db_word(t, 4 * ch)));
                 d[4 * ch] = v4.x; d[4 * ch + 1] = v4.y; d[4 * ch + 2] = v4.z; d[4 * ch + 3] = v4.w;
               }
             } else {
@@ -970,7 +973,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
                   const int tp = t ^ (1 << b);
 #pragma unroll
                   for (int ch = 0; ch < 4; ++ch) {
-                    const float4 v4 = *reinterpret_cast<const float4*>(DB + db_word(tp, 4 * ch));
+                    const float4 v4 = *reinterpret_cast<const float4*>(DB + (dbx ^ db_word(tp, 4 * ch)));
                     acc[LJ + b + 1] = __ffma2_rn(make_float2(x[4 * ch], x[4 * ch + 1]), make_float2(v4.x, v4.y),
                                                  acc[LJ + b + 1]);
                     acc[LJ + b + 1] = __ffma2_rn(make_float2(x[4 * ch + 2], x[4 * ch + 3]), make_float2(v4.z, v4.w),
@@ -992,7 +995,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             if constexpr (TT > 1) {
 #pragma unroll
               for (int ch = 0; ch < 4; ++ch) {
-                const float4 v4 = is_a ? *reinterpret_cast<const float4*>(DB + db_word(t, 4 * ch)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float4 v4 = is_a ? *reinterpret_cast<const float4*>(DB + (dbx ^ db_word(t, 4 * ch))) : make_float4(0.f, 0.f, 0.f, 0.f);
                 bq[4 * ch] = v4.x; bq[4 * ch + 1] = v4.y; bq[4 * ch + 2] = v4.z; bq[4 * ch + 3] = v4.w;
               }
             } else {
@@ -1112,7 +1115,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
                   const int yy = zr[r] ^ z;
                   int w;
                   if constexpr (TT > 1) {
-                    w = db_word((yy >> LJ) & (TT - 1), (yy & ((1 << LJ) - 1)) | ((yy >> 4) << LJ));
+                    w = dbx ^ db_word((yy >> LJ) & (TT - 1), (yy & ((1 << LJ) - 1)) | ((yy >> 4) << LJ));
                   } else {
                     w = yy;
                   }

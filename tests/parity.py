@@ -118,24 +118,39 @@ def fail_trajectory_stable(decode, x_row, max_iters, **kw):
 
 
 def assert_stable_parity(decode, x, out, ref, max_iters, max_unstable_frac=0.1, what="", also=None, **kw):
-    """The stable-frame protocol (reading R20): every frame whose fp64 and fp32 oracle
-    trajectories agree must be bit-identical (hard symbols, syndrome flag, iterations) on the GPU;
-    differing frames must be unstable ones and at most ``max_unstable_frac`` of the sample.
+    """The stable-frame protocol (readings R20, R26): every frame whose oracle outcome is
+    robust must be bit-identical (hard symbols, syndrome flag, iterations) on the GPU; differing frames
+    must be unstable ones and at most ``max_unstable_frac`` of the sample.
+    A frame is stable when the oracle's fp64 run (``ref``) agrees with its fp32 twin and with every
+    variant in ``also`` (extra keyword sets for ``decode``, e.g. O-LF without the half store for the F16
+    path) -- at the stopping iteration, and for a converged frame also one iteration before it (a frame
+    whose last symbol settles at the last moment converges one iteration earlier or later under any
+    rounding difference); a frame the oracle does not converge on must also agree 5 and 10 iterations
+    before the end (fail_trajectory_stable).
     ``decode`` is the oracle's batch decode (lf_decode_batch / lf_decode_batch_pmf / ls_decode_batch),
     ``x`` its input rows, ``out`` numpy GPU outputs {hard, ok, iters}, ``ref`` the oracle's (fp64) result.
-    ``also``: further decodes (callables of the rows) that must agree with ``ref`` too for a frame to count
-    as stable -- e.g. O-LF without the half-precision store for the F16 path (reading R26).
     Returns the number of (unstable) differing frames."""
     hard, ok, it = out["hard"], out["ok"], out["iters"]
     same = (hard == ref["hard"]).all(1) & (ok == ref["ok"]) & (it == ref["iters"])
     bad = np.where(~same)[0]
+    variants = [dict(f32=True)] + [dict(v) for v in (also or [])]
+    base_kw = {k: v for k, v in kw.items() if k != "early_stop"}
+
+    def agree(a, b, n, m):
+        return np.array_equal(a["hard"][n], b["hard"][m]) and a["ok"][n] == b["ok"][m] and a["iters"][n] == b["iters"][m]
+
     if bad.size:
-        twins = [decode(x[bad], max_iters, f32=True, **kw)] + [fn(x[bad]) for fn in (also or [])]
+        runs = [decode(x[bad], max_iters, **{**kw, **v}) for v in variants]
         for n, b in enumerate(bad):
-            stable = all(np.array_equal(tw["hard"][n], ref["hard"][b]) and tw["ok"][n] == ref["ok"][b]
-                         and tw["iters"][n] == ref["iters"][b] for tw in twins)
+            stable = all(agree(r, ref, n, b) for r in runs)
+            if stable and ref["ok"][b] == 1 and ref["iters"][b] > 1:
+                before = ref["iters"][b] - 1
+                r0 = decode(x[b][None], before, early_stop=False, **base_kw)
+                stable = all(np.array_equal(decode(x[b][None], before, early_stop=False, **{**base_kw, **v})["hard"][0],
+                                            r0["hard"][0]) for v in variants)
             if stable and ref["ok"][b] == 0:
-                stable = fail_trajectory_stable(decode, x[b], max_iters, **kw)
+                stable = fail_trajectory_stable(decode, x[b], max_iters, **kw) and all(
+                    fail_trajectory_stable(decode, x[b], max_iters, **{**kw, **v}) for v in variants[1:])
             assert not stable, (f"{what}: stable frame {b} differs: gpu iters {it[b]} ok {ok[b]} vs oracle "
                                 f"{ref['iters'][b]} {ref['ok'][b]}, {int((hard[b] != ref['hard'][b]).sum())} symbols")
     assert bad.size <= max(1, int(max_unstable_frac * len(hard))), (what, bad.size, len(hard))

@@ -11,7 +11,7 @@ torch = pytest.importorskip("torch")
 import oracle
 import synth
 from helpers import DEFAULT_POLY
-from parity import soft_mismatch, config_inputs, fail_trajectory_stable, oracle_code
+from parity import assert_stable_parity, config_inputs, oracle_code, soft_mismatch
 
 pytestmark = pytest.mark.gpu
 VN_GENERAL = 2
@@ -31,25 +31,11 @@ def _codes(m, M, N, rows, cols, coeffs):
 
 
 def _compare(ocode, out, x, idx, max_iters, pmf=False):
+    """Bit-exact on stable frames (assert_stable_parity); returns the number of unstable differing frames."""
     dec = ocode.lf_decode_batch_pmf if pmf else ocode.lf_decode_batch
     ref = dec(x[idx], max_iters)
-    hard = out["hard"].cpu().numpy()[idx]
-    ok = out["ok"].cpu().numpy()[idx]
-    it = out["iters"].cpu().numpy()[idx]
-    same = (hard == ref["hard"]).all(1) & (ok == ref["ok"]) & (it == ref["iters"])
-    unstable = 0
-    if not same.all():
-        bad = np.where(~same)[0]
-        twin = dec(x[idx][bad], max_iters, f32=True)
-        for n, b in enumerate(bad):
-            stable = (np.array_equal(twin["hard"][n], ref["hard"][b]) and twin["ok"][n] == ref["ok"][b]
-                      and twin["iters"][n] == ref["iters"][b])
-            if stable and ref["ok"][b] == 0:
-                stable = fail_trajectory_stable(dec, x[idx][b], max_iters)
-            assert not stable, (f"stable frame {idx[b]} differs: gpu iters {it[b]} ok {ok[b]} vs oracle "
-                                f"{ref['iters'][b]} {ref['ok'][b]}")
-            unstable += 1
-    return unstable
+    got = {k: out[k].cpu().numpy()[idx] for k in ("hard", "ok", "iters")}
+    return assert_stable_parity(dec, x[idx], got, ref, max_iters, max_unstable_frac=1.0, what="general")
 
 
 @pytest.mark.parametrize("m,N,k,j,ebn0", [(3, 96, 6, 3, 2.5), (4, 120, 6, 3, 2.0), (6, 64, 8, 4, 3.0),

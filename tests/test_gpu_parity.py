@@ -39,27 +39,12 @@ def gpu_code(name):
 
 
 def compare_decode(name, gpu_out, llr_np, idx, max_iters, mode=0):
-    """Oracle on frames idx; bit-exact on stable frames.  Returns (n_checked, n_unstable)."""
+    """Oracle on frames idx; bit-exact on stable frames (assert_stable_parity).  Returns (n_checked, n_unstable)."""
     ocode = oracle_code(name)
     sub = llr_np[idx]
     ref = ocode.lf_decode_batch(sub, max_iters, mode=mode)
-    hard = gpu_out["hard"].cpu().numpy()[idx]
-    ok = gpu_out["ok"].cpu().numpy()[idx]
-    it = gpu_out["iters"].cpu().numpy()[idx]
-    same = (hard == ref["hard"]).all(1) & (ok == ref["ok"]) & (it == ref["iters"])
-    unstable = 0
-    if not same.all():
-        bad = np.where(~same)[0]
-        twin = ocode.lf_decode_batch(sub[bad], max_iters, mode=mode, f32=True)
-        for n, b in enumerate(bad):
-            oracle_stable = (np.array_equal(twin["hard"][n], ref["hard"][b]) and twin["ok"][n] == ref["ok"][b]
-                             and twin["iters"][n] == ref["iters"][b])
-            if oracle_stable and ref["ok"][b] == 0:
-                oracle_stable = fail_trajectory_stable(ocode.lf_decode_batch, sub[b], max_iters, mode=mode)
-            assert not oracle_stable, (
-                f"{name}: stable frame {idx[b]} differs: gpu iters {it[b]} ok {ok[b]} vs oracle "
-                f"{ref['iters'][b]} {ref['ok'][b]}, {int((hard[b] != ref['hard'][b]).sum())} symbols")
-            unstable += 1
+    got = {k: gpu_out[k].cpu().numpy()[idx] for k in ("hard", "ok", "iters")}
+    unstable = assert_stable_parity(ocode.lf_decode_batch, sub, got, ref, max_iters, what=name, mode=mode)
     return len(idx), unstable
 
 

@@ -12,7 +12,7 @@ torch = pytest.importorskip("torch")
 
 import synth
 from helpers import bit_prior
-from parity import soft_mismatch, config_inputs, fail_trajectory_stable, oracle_code
+from parity import assert_stable_parity, config_inputs, oracle_code, soft_mismatch
 
 pytestmark = pytest.mark.gpu
 
@@ -41,26 +41,11 @@ def _pmf_inputs(name, F, ebn0):
 
 
 def _compare(name, out, pmf, idx, max_iters):
-    """Bit-exact on stable frames; returns the number of unstable frames among idx."""
+    """Bit-exact on stable frames (assert_stable_parity); returns the number of unstable frames among idx."""
     ocode = oracle_code(name)
     ref = ocode.lf_decode_batch_pmf(pmf[idx], max_iters)
-    hard = out["hard"].cpu().numpy()[idx]
-    ok = out["ok"].cpu().numpy()[idx]
-    it = out["iters"].cpu().numpy()[idx]
-    same = (hard == ref["hard"]).all(1) & (ok == ref["ok"]) & (it == ref["iters"])
-    unstable = 0
-    if not same.all():
-        bad = np.where(~same)[0]
-        twin = ocode.lf_decode_batch_pmf(pmf[idx][bad], max_iters, f32=True)
-        for n, b in enumerate(bad):
-            stable = (np.array_equal(twin["hard"][n], ref["hard"][b]) and twin["ok"][n] == ref["ok"][b]
-                      and twin["iters"][n] == ref["iters"][b])
-            if stable and ref["ok"][b] == 0:
-                stable = fail_trajectory_stable(ocode.lf_decode_batch_pmf, pmf[idx][b], max_iters)
-            assert not stable, (f"{name}: stable frame {idx[b]} differs: gpu iters {it[b]} ok {ok[b]} vs "
-                                f"oracle {ref['iters'][b]} {ref['ok'][b]}")
-            unstable += 1
-    return unstable
+    got = {k: out[k].cpu().numpy()[idx] for k in ("hard", "ok", "iters")}
+    return assert_stable_parity(ocode.lf_decode_batch_pmf, pmf[idx], got, ref, max_iters, what=name)
 
 
 PMF_CASES = [
