@@ -256,13 +256,17 @@ __device__ __forceinline__ void tot_sum(const float* smem, int gbase, float* TOT
                                         bool cvalid) {
   constexpr int WPT = R / JPT;
   const float* g = smem + gbase;
+  // one w split over lanes (WPT == 1): the lanes of a w read rows JPT apart, which for TEAM * JPT = 0 mod 32
+  // words are the same banks -- so odd split lanes take the rows in the order jj ^ 1 (a different bank half
+  // when TEAM = 16; the sum does not depend on the order up to rounding)
+  const int jx = (WPT == 1 && TEAM % 32 != 0) ? (pck & 1) : 0;
 #pragma unroll
   for (int i = 0; i < WPT; ++i) {
     float mag = 0.0f;
     uint32_t sg = 0;
 #pragma unroll
     for (int jj = 0; jj < JPT; ++jj) {
-      const float v = g[jj * TEAM + i * TT * JPT];
+      const float v = g[((JPT > 1 ? jj ^ jx : jj)) * TEAM + i * TT * JPT];
       mag += fabsf(v);
       sg ^= __float_as_uint(v);
     }
@@ -274,6 +278,37 @@ __device__ __forceinline__ void tot_sum(const float* smem, int gbase, float* TOT
     }
     if (cvalid && (WPT > 1 || (pck & (split - 1)) == 0))
       TOT[wgrp + TT * JPT * i] = __uint_as_float(__float_as_uint(mag) | (sg & kSign));
+  }
+}
+
+// TOT for one-thread teams (q <= 16) from the lane-major scatter buffer xs[w][32] (X_j(w) of the team in
+// lane j of the warp at xs[32 w + j]): the scatter of every lane hits its own bank, and here the threads of
+// a w read the check's lanes in an order rotated by w, so that every load instruction covers 32 banks.
+// c0: the check's first lane in the warp; the rest as tot_sum.
+template <int R, int JPT>
+__device__ __forceinline__ void tot_sum_lm(const float* xs, int c0, float* TOT, int wgrp, int split, int pck,
+                                           bool cvalid) {
+  constexpr int WPT = R / JPT;
+  const int jb = c0 + (pck % split) * JPT;
+#pragma unroll
+  for (int i = 0; i < WPT; ++i) {
+    const int w = wgrp + JPT * i;
+    const float* g = xs + 32 * w + jb;
+    float mag = 0.0f;
+    uint32_t sg = 0;
+#pragma unroll
+    for (int jj = 0; jj < JPT; ++jj) {
+      const float v = g[(jj + wgrp) & (JPT - 1)];
+      mag += fabsf(v);
+      sg ^= __float_as_uint(v);
+    }
+    if constexpr (WPT == 1) {
+      for (int off = 1; off < split; off <<= 1) {
+        mag += __shfl_xor_sync(0xffffffffu, mag, off);
+        sg ^= __shfl_xor_sync(0xffffffffu, sg, off);
+      }
+    }
+    if (cvalid && (WPT > 1 || (pck & (split - 1)) == 0)) TOT[w] = __uint_as_float(__float_as_uint(mag) | (sg & kSign));
   }
 }
 
@@ -315,6 +350,54 @@ __device__ __forceinline__ void tot_prod(float* smem, int gbase, int split, bool
     if (cvalid) {
 #pragma unroll
       for (int jj = 0; jj < JPT; ++jj) g[jj * TEAM + i * TT * JPT] = ex[jj];
+    }
+  }
+}
+
+// LIN at q = 256 (two teams per warp): the pair of a warp's two team rows holds X_{2p}(w) and X_{2p+1}(w)
+// interleaved at 2w and 2w + 1, so the two teams' scatters use the even and the odd banks (measured
+// row-major: 2.9 wavefronts per scatter instruction); the column threads then read j in the order jj ^ flip
+// (flip: the upper half-warp, or the odd split lane) so that their loads still cover 32 banks.
+template <int R, int JPT, int TT, int QS>
+__device__ __forceinline__ void tot_prod_il(float* rows, int wgrp, int jbase, int flip, int split, bool cvalid) {
+  constexpr int WPT = R / JPT;
+#pragma unroll
+  for (int i = 0; i < WPT; ++i) {
+    const int w = wgrp + TT * JPT * i;
+    float v[JPT], ex[JPT];
+#pragma unroll
+    for (int jj = 0; jj < JPT; ++jj) {
+      const int j = jbase + (jj ^ flip);
+      v[jj] = rows[(j & ~1) * QS + 2 * w + (j & 1)];
+    }
+    float pre = 1.0f;
+#pragma unroll
+    for (int jj = 0; jj < JPT; ++jj) {
+      ex[jj] = pre;
+      pre *= v[jj];
+    }
+    float suf = 1.0f;
+#pragma unroll
+    for (int jj = JPT - 1; jj >= 0; --jj) {
+      ex[jj] *= suf;
+      suf *= v[jj];
+    }
+    if constexpr (WPT == 1) {
+      float other = 1.0f, incl = pre;
+      for (int off = 1; off < split; off <<= 1) {
+        const float o = __shfl_xor_sync(0xffffffffu, incl, off);
+        other *= o;
+        incl *= o;
+      }
+#pragma unroll
+      for (int jj = 0; jj < JPT; ++jj) ex[jj] *= other;
+    }
+    if (cvalid) {
+#pragma unroll
+      for (int jj = 0; jj < JPT; ++jj) {
+        const int j = jbase + (jj ^ flip);
+        rows[(j & ~1) * QS + 2 * w + (j & 1)] = ex[jj];
+      }
     }
   }
 }
@@ -446,6 +529,11 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   EdgeRec* const recs = reinterpret_cast<EdgeRec*>(PT + Q);
   uint8_t* const GL = reinterpret_cast<uint8_t*>(recs + P.rec_per_cta);  // [q] log_alpha
   uint8_t* const GE = GL + Q;                                            // [2q] alpha^i
+  // pmf input, one-thread teams (q <= 16): the teams' pmf rows staged one chunk ahead beside the message
+  // rows ([NS][nteams][q], LDGSTS on the stage mbarrier), instead of an L2 load at the chunk's start
+  // (ncu, C5 pmf: 33% of the stall samples waited on that load)
+  constexpr bool PSTAGE = PMF && TT == 1 && Q >= 4;
+  float* const PB = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(GL) + 3 * Q + 15) & ~(uintptr_t)15);
 
   // TOT(w) gather offsets: thread pck owns WPT w's x JPT teams of its check (R terms, natural X)
   const int SPLIT = KT > R ? KT / R : 1;
@@ -500,6 +588,10 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   // -2.5%, C4 -2% time; C2 +5%, C5 +12%, so q <= 64 keeps the log format); the F16 format and the
   // soft-output kernels (whose fp64 decision needs the exact log-magnitudes) always keep the packed log format
   constexpr bool LIN = !F16 && !SOFT && MB >= 7;
+  // one-thread teams (q <= 16): the check node's scatter goes to the group's consumed stage buffer in a
+  // lane-major layout xs[w][lane] (conflict-free; ncu, C5: the row-major scatter replayed 3.6x)
+  constexpr bool LANEMAJOR = TT == 1 && !F16 && Q >= 2;
+  constexpr bool PAIRIL = LIN && TT == 16;  // the interleaved team pairs of tot_prod_il
   const int step = P.step_mode;
   const size_t EQ = (size_t)cd.E * Q;
   const uint32_t flag0 = dsmem_addr(&sh_flag[0], 0), flag1 = dsmem_addr(&sh_flag[1], 0);
@@ -545,27 +637,45 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
     uint8_t* const con = ws.con + (size_t)slot * ws.con_stride;
     float* const Pp = PMF ? call->p0buf + (size_t)slot * cd.N * Q : nullptr;
     if (PMF) {  // (also in step mode: nbldpc_step_pmf, slot = frame)
-      // the frame's pmf rows scaled to probabilities p_v, one warp per row, stored at
+      // the frame's pmf rows scaled to probabilities p_v, several rows per warp, stored at
       // ppos(z) for the teams' phase-B reads; a row with a non-positive sum becomes all zero (its
       // variable-node outputs are then neutral and counted as numerical events, reading R23)
       const float* pf = call->pmf + (size_t)f * cd.N * Q;
       const int nwarp = nthr >> 5;
-      constexpr int PER = Q >= 32 ? Q / 32 : 1;
-      for (int v = (int)rank * nwarp + (tid >> 5); v < cd.N; v += (int)csz * nwarp) {
-        float pv[PER], sum = 0.0f;
+      if constexpr (Q >= 4) {
+        // each lane takes EL consecutive entries of a row (16-byte loads), LN = Q / EL lanes per row, 32 / LN
+        // rows per warp and pass (q = 16: 8 rows per warp-pass instead of 1 with half the lanes idle)
+        constexpr int EL = Q / 32 > 4 ? Q / 32 : 4, LN = Q / EL, RW = 32 / LN;
+        const int sub = lane / LN, zl = (lane % LN) * EL;
+        for (int v0 = ((int)rank * nwarp + (tid >> 5)) * RW; v0 < cd.N; v0 += (int)csz * nwarp * RW) {
+          const int v = v0 + sub;
+          float pv[EL], sum = 0.0f;
 #pragma unroll
-        for (int k = 0; k < PER; ++k) {
-          const int z = lane + 32 * k;
-          pv[k] = z < Q ? __ldcs(pf + (size_t)v * Q + z) : 0.0f;  // streamed: read once
-          sum += pv[k];
+          for (int k = 0; k < EL / 4; ++k) {
+            const float4 x4 = v < cd.N ? __ldcs(reinterpret_cast<const float4*>(pf + (size_t)v * Q + zl) + k)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);  // streamed: read once
+            pv[4 * k] = x4.x; pv[4 * k + 1] = x4.y; pv[4 * k + 2] = x4.z; pv[4 * k + 3] = x4.w;
+            sum += (x4.x + x4.y) + (x4.z + x4.w);
+          }
+#pragma unroll
+          for (int off = LN / 2; off >= 1; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+          const float inv = sum > 0.0f ? 1.0f / sum : 0.0f;
+          if (v < cd.N) {
+#pragma unroll
+            for (int k = 0; k < EL; ++k) Pp[(size_t)v * Q + ppos<MB>(zl + k)] = pv[k] * inv;
+          }
         }
+      } else {
+        constexpr int PER = 1;
+        for (int v = (int)rank * nwarp + (tid >> 5); v < cd.N; v += (int)csz * nwarp) {
+          float pv[PER], sum = 0.0f;
+          const int z = lane;
+          pv[0] = z < Q ? __ldcs(pf + (size_t)v * Q + z) : 0.0f;
+          sum = pv[0];
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-        const float inv = sum > 0.0f ? 1.0f / sum : 0.0f;
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-          const int z = lane + 32 * k;
-          if (z < Q) Pp[(size_t)v * Q + ppos<MB>(z)] = pv[k] * inv;
+          for (int off = 16; off >= 1; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+          const float inv = sum > 0.0f ? 1.0f / sum : 0.0f;
+          if (z < Q) Pp[(size_t)v * Q + ppos<MB>(z)] = pv[0] * inv;
         }
       }
       cluster_sync_all();
@@ -617,6 +727,17 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         // the team's channel-term row by two LDGSTS tracked by the same mbarrier (the pending count
         // is raised before this thread's own arrival, so the phase waits for them): a bulk copy from a
         // divergent thread would cost a uniform-register waterfall loop over the warp's team leaders
+        if constexpr (PSTAGE) {
+          if (act) {
+            const float* srcp = call->p0buf + ((size_t)slot * cd.N + (rr.var_h >> 8)) * Q;
+            float* dstp = PB + ((size_t)b * nteams + team) * Q;
+#pragma unroll
+            for (int c4 = 0; c4 < Q / 4; ++c4)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dstp + 4 * c4)), "l"(srcp + 4 * c4)
+                           : "memory");
+            asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(&gmbar[b])) : "memory");
+          }
+        }
         if (act && !C::THREG && !PMF) {
           const float* srcT = Tt + (size_t)(rr.var_h >> 8) * 8;
           float* dstT = THB + b * nteams * 8;
@@ -692,7 +813,14 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         }
         // pmf input: my R entries of p_v at the phase-B coordinates zr, straight from L2
         float pv[PMF ? R : 1];
-        if constexpr (PMF) {
+        if constexpr (PSTAGE) {
+          const float* src = PB + ((size_t)buf * nteams + team) * Q;
+#pragma unroll
+          for (int ch = 0; ch < CH; ++ch) {
+            const float4 v = active ? *reinterpret_cast<const float4*>(src + 4 * ch) : make_float4(0.f, 0.f, 0.f, 0.f);
+            pv[4 * ch] = v.x; pv[4 * ch + 1] = v.y; pv[4 * ch + 2] = v.z; pv[4 * ch + 3] = v.w;
+          }
+        } else if constexpr (PMF) {
           const float* src = Pp + (size_t)var * Q + t * R;
           if constexpr (R >= 4) {
 #pragma unroll
@@ -918,19 +1046,24 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
                   for (int k4 = 0; k4 < 4; ++k4) DB[dbx ^ db_word(4 * ch + k4, t)] = d4[k4];
                 }
               }
-            } else if constexpr (R >= 4) {
+            } else if (mode == 1 || SYM) {
+              // one-thread teams hold all of D themselves (the dot products below read registers); the
+              // row is written only for the paper syndrome's points and the symbol outputs (ncu, C5: these
+              // stores were 16-way bank-conflicted, 2.0e9 wavefronts per 4,096-frame launch)
+              if constexpr (R >= 4) {
 #pragma unroll
-              for (int ch = 0; ch < CH; ++ch) {
-                const float4 v = wo4[ch];
-                if constexpr (LIN) {
-                  *reinterpret_cast<float4*>(DB + 4 * ch) = v;
-                } else {
-                  DB[4 * ch] = to_lin(v.x); DB[4 * ch + 1] = to_lin(v.y); DB[4 * ch + 2] = to_lin(v.z); DB[4 * ch + 3] = to_lin(v.w);
+                for (int ch = 0; ch < CH; ++ch) {
+                  const float4 v = wo4[ch];
+                  if constexpr (LIN) {
+                    *reinterpret_cast<float4*>(DB + 4 * ch) = v;
+                  } else {
+                    DB[4 * ch] = to_lin(v.x); DB[4 * ch + 1] = to_lin(v.y); DB[4 * ch + 2] = to_lin(v.z); DB[4 * ch + 3] = to_lin(v.w);
+                  }
                 }
+              } else {
+                DB[0] = LIN ? wo4[0].x : to_lin(wo4[0].x);
+                if constexpr (R > 1) DB[1] = LIN ? wo4[0].y : to_lin(wo4[0].y);
               }
-            } else {
-              DB[0] = LIN ? wo4[0].x : to_lin(wo4[0].x);
-              if constexpr (R > 1) DB[1] = LIN ? wo4[0].y : to_lin(wo4[0].y);
             }
           }
           if constexpr (TT > 1) __syncwarp();
@@ -949,7 +1082,10 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               }
             } else {
 #pragma unroll
-              for (int r = 0; r < R; ++r) d[r] = DB[r];
+              for (int r = 0; r < R; ++r) {
+                const float v = R >= 4 ? (&wo4[r >> 2].x)[r & 3] : (r == 0 ? wo4[0].x : wo4[0].y);
+                d[r] = LIN ? v : to_lin(v);
+              }
             }
             if constexpr (R >= 2) {
               float2 acc[MB + 1];
@@ -1161,33 +1297,61 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               for (int r = 0; r < R; ++r) oidx[r] = zr[r];
             }
           }
-          if constexpr (TT > 1) __syncwarp();  // transposition / DB reads of X done
+          // transposition / DB reads of X done (LANEMAJOR: the scatter writes into the whole warp's buffer)
+          if constexpr (TT > 1 || LANEMAJOR) __syncwarp();
           if (cvalid) {
             // scatter: X_e(pi_e^-1 z) = U_e(z) = T_e(.); padding teams hold the neutral message
-#ifdef NB_SMEM_GENERIC
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-              NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
-              st[oidx[r]] = __uint_as_float(up[r]);
-            }
-#else
             // 32-bit shared-window addresses: one LEA per entry instead of an IMAD + IADD3 pair
-            const uint32_t st_s = smem_u32(st);
+            if constexpr (PAIRIL) {
+              const uint32_t il_s = smem_u32(GST + buf * GBLK + (trow & ~1) * C::QS) + ((uint32_t)(trow & 1) << 2);
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-              NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
-              asm volatile("st.shared.b32 [%0], %1;" ::"r"(st_s + ((uint32_t)oidx[r] << 2)), "r"(up[r]) : "memory");
+              for (int r = 0; r < R; ++r) {
+                NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(il_s + ((uint32_t)oidx[r] << 3)), "r"(up[r]) : "memory");
+              }
+            } else if constexpr (LANEMAJOR) {
+              const uint32_t xs_s = smem_u32(GST + buf * GBLK) + ((uint32_t)(tid - grp * GT) << 2);
+#pragma unroll
+              for (int r = 0; r < R; ++r) {
+                NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(xs_s + ((uint32_t)oidx[r] << 7)), "r"(up[r]) : "memory");
+              }
+            } else {
+              const uint32_t st_s = smem_u32(st);
+#pragma unroll
+              for (int r = 0; r < R; ++r) {
+                NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(st_s + ((uint32_t)oidx[r] << 2)), "r"(up[r]) : "memory");
+              }
             }
-#endif
           }
           check_sync(lc, TPC);
-          if constexpr (LIN) {
+          if constexpr (PAIRIL) {
+            float* rows = GST + buf * GBLK + (lc - grp * CPG) * KT * C::QS;
+            const int flip = SPLIT == 1 ? ((lane >> 4) & 1) : (pck & 1);
+            switch (JPT) {
+              case 2: tot_prod_il<R, 2, TT, C::QS>(rows, wgrp, jbase, flip, SPLIT, cvalid); break;
+              case 4: tot_prod_il<R, 4, TT, C::QS>(rows, wgrp, jbase, flip, SPLIT, cvalid); break;
+              case 8: tot_prod_il<R, 8, TT, C::QS>(rows, wgrp, jbase, flip, SPLIT, cvalid); break;
+              default: tot_prod_il<R, R, TT, C::QS>(rows, wgrp, jbase, flip, SPLIT, cvalid); break;
+            }
+          } else if constexpr (LIN) {
             switch (JPT) {
               case 1: tot_prod<R, 1, TT, C::QS>(smem, gbase + buf * GBLK, SPLIT, cvalid); break;
               case 2: tot_prod<R, (R >= 2 ? 2 : 1), TT, C::QS>(smem, gbase + buf * GBLK, SPLIT, cvalid); break;
               case 4: tot_prod<R, (R >= 4 ? 4 : 1), TT, C::QS>(smem, gbase + buf * GBLK, SPLIT, cvalid); break;
               case 8: tot_prod<R, (R >= 8 ? 8 : 1), TT, C::QS>(smem, gbase + buf * GBLK, SPLIT, cvalid); break;
               default: tot_prod<R, R, TT, C::QS>(smem, gbase + buf * GBLK, SPLIT, cvalid); break;
+            }
+          } else if constexpr (LANEMAJOR) {
+            const float* xs = GST + buf * GBLK;
+            const int c0 = (lc - grp * CPG) * KT;
+            switch (JPT) {
+              case 1: tot_sum_lm<R, 1>(xs, c0, TOT, wgrp, SPLIT, pck, cvalid); break;
+              case 2: tot_sum_lm<R, (R >= 2 ? 2 : 1)>(xs, c0, TOT, wgrp, SPLIT, pck, cvalid); break;
+              case 4: tot_sum_lm<R, (R >= 4 ? 4 : 1)>(xs, c0, TOT, wgrp, SPLIT, pck, cvalid); break;
+              case 8: tot_sum_lm<R, (R >= 8 ? 8 : 1)>(xs, c0, TOT, wgrp, SPLIT, pck, cvalid); break;
+              default: tot_sum_lm<R, R>(xs, c0, TOT, wgrp, SPLIT, pck, cvalid); break;
             }
           } else switch (JPT) {
             case 1: tot_sum<R, 1, TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid); break;
@@ -1199,18 +1363,14 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           check_sync(lc, TPC);
           if (active) {
             float out[R];
-#ifndef NB_SMEM_GENERIC
-            const uint32_t tot_s = smem_u32(LIN ? st : TOT);
-#endif
+            const uint32_t tot_s = PAIRIL ? smem_u32(GST + buf * GBLK + (trow & ~1) * C::QS) + ((uint32_t)(trow & 1) << 2)
+                                          : smem_u32(LIN ? st : TOT);
+            constexpr int osh = PAIRIL ? 3 : 2;  // PAIRIL: my entries sit at 2 w + (trow & 1) of the pair
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
-#ifdef NB_SMEM_GENERIC
-              const float xt = LIN ? st[oidx[r]] : TOT[oidx[r]];
-#else
               float xt;
-              asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xt) : "r"(tot_s + ((uint32_t)oidx[r] << 2)) : "memory");
-#endif
+              asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xt) : "r"(tot_s + ((uint32_t)oidx[r] << osh)) : "memory");
               if constexpr (LIN) {
                 out[r] = xt;  // W_e(z) = prod_{j != e} X_j(pi_e^-1 z), written back into my own scatter row
               } else {

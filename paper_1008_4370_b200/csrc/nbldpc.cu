@@ -91,6 +91,7 @@ struct nbldpc_code_s {
   int p_tpc = 1, p_cpc = 1, p_groups = 1, p_block = 32, p_big = 0, p_cs = 1, p_ncl = 1, p_recs = 0;
   int p_kp = 0;  // > 0: the plain LLR launch uses the compile-time-geometry instantiation (KP = kpad)
   size_t p_smem = 0;
+  size_t p_smem_pmf = 0;  // the pmf variant: + its staged pmf rows for one-thread teams (PSTAGE)
   // false: the cluster kernel cannot run this code (its per-CTA edge records do not fit in shared memory
   // even with 16-CTA clusters, or no cluster fits on the GPU): NBLDPC_VN_SEPARABLE decodes run the
   // general-column-weight kernel instead (same results up to rounding)
@@ -196,7 +197,7 @@ cudaError_t launch_cluster(const nbldpc_code_s* c, const nb::ClusterParams& P, i
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(ncl * c->p_cs));
   cfg.blockDim = dim3((unsigned)c->p_block);
-  cfg.dynamicSmemBytes = c->p_smem;
+  cfg.dynamicSmemBytes = pmf ? c->p_smem_pmf : c->p_smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -242,10 +243,11 @@ cudaError_t ensure_smem_attr(const nbldpc_code_s* c) {
     int k = (c->m * 2 + c->p_big) * 9 + var;
     if (var == 3) k = 18 * 9 + (c->m - 1) * 4 + (c->p_kp == 4 ? 0 : c->p_kp == 8 ? 1 : c->p_kp == 16 ? 2 : 3);
     const int d = c->device & 63;
-    if (p_attr[d][k] < c->p_smem) {
-      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->p_smem);
+    const size_t need = pmf ? c->p_smem_pmf : c->p_smem;
+    if (p_attr[d][k] < need) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
       if (e != cudaSuccess) return e;
-      p_attr[d][k] = c->p_smem;
+      p_attr[d][k] = need;
     }
   }
   return cudaSuccess;
@@ -700,6 +702,7 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
     return decode_general(c, llr, pmf, frames, max_iters, hard, ok, iters, early, soft, events, post, xmap, st);
   }
   if ((post || xmap) && direct == 0 && pmf) direct = 1;  // pmf + symbol outputs: the pass kernel
+  if (pmf && direct == 0 && c->p_smem_pmf > 227 * 1024) direct = 1;  // staged pmf rows do not fit: the pass kernel
   if (pmf && direct) direct = 2;                   // the pass kernel's pmf variant
   if (slots < 0) return NBLDPC_ERR_INVALID_ARGUMENT;
   if ((soft && !is_device_ptr(soft)) || (events && !is_device_ptr(events))) return NBLDPC_ERR_INVALID_ARGUMENT;
@@ -1093,6 +1096,9 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
     c->p_cs = cs;
     c->p_recs = ((c->p_groups + cs - 1) / cs) * c->p_cpc * kt;
     c->p_smem = smem_for(cs);
+    c->p_smem_pmf = c->p_smem;
+    if (tt == 1 && q >= 4)  // PSTAGE in lf_cluster.cuh: [NS][teams][q] floats, 16-byte aligned after the GF tables
+      c->p_smem_pmf += 16 + (size_t)nb::CCfg<1>::NS * (size_t)(c->p_block / tt) * q * sizeof(float);
     if (c->p_smem > 227 * 1024) c->cluster_ok = false;
   }
   if (cudaError_t e = ensure_smem_attr(c)) return bail(e);
