@@ -591,7 +591,13 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   // one-thread teams (q <= 16): the check node's scatter goes to the group's consumed stage buffer in a
   // lane-major layout xs[w][lane] (conflict-free; ncu, C5: the row-major scatter replayed 3.6x)
   constexpr bool LANEMAJOR = TT == 1 && !F16 && Q >= 2;
-  constexpr bool PAIRIL = LIN && TT == 16;  // the interleaved team pairs of tot_prod_il
+  // the interleaved team pairs of tot_prod_il: measured neutral on C4 (conflict replays -14%, instructions
+  // +7%), kept off; NB_PAIRIL=1 builds it
+#ifdef NB_PAIRIL
+  constexpr bool PAIRIL = LIN && TT == 16;
+#else
+  constexpr bool PAIRIL = false;
+#endif
   const int step = P.step_mode;
   const size_t EQ = (size_t)cd.E * Q;
   const uint32_t flag0 = dsmem_addr(&sh_flag[0], 0), flag1 = dsmem_addr(&sh_flag[1], 0);
