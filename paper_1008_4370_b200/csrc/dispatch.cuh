@@ -9,28 +9,28 @@ namespace nbk {
 
 constexpr int kBigBlock = 512;  // block-size variant for k_max * TT > 256 (as in nbldpc.cu)
 
-template <int MB, int MAXB, bool DIRECT, bool PMF>
-void* pass_fn() { return reinterpret_cast<void*>(&nb::nb_pass_kernel<MB, MAXB, DIRECT, PMF>); }
+template <int MB, int MAXB, bool DIRECT, bool PMF, bool SOFT>
+void* pass_fn() { return reinterpret_cast<void*>(&nb::nb_pass_kernel<MB, MAXB, DIRECT, PMF, SOFT>); }
 
-template <bool DIRECT, bool PMF>
+template <bool DIRECT, bool PMF, bool SOFT = false>
 void* pass_kernel_ptr_t(int m, int big) {
   switch (m * 2 + (big ? 1 : 0)) {
-    case 2: return pass_fn<1, 256, DIRECT, PMF>();
-    case 3: return pass_fn<1, kBigBlock, DIRECT, PMF>();
-    case 4: return pass_fn<2, 256, DIRECT, PMF>();
-    case 5: return pass_fn<2, kBigBlock, DIRECT, PMF>();
-    case 6: return pass_fn<3, 256, DIRECT, PMF>();
-    case 7: return pass_fn<3, kBigBlock, DIRECT, PMF>();
-    case 8: return pass_fn<4, 256, DIRECT, PMF>();
-    case 9: return pass_fn<4, kBigBlock, DIRECT, PMF>();
-    case 10: return pass_fn<5, 256, DIRECT, PMF>();
-    case 11: return pass_fn<5, kBigBlock, DIRECT, PMF>();
-    case 12: return pass_fn<6, 256, DIRECT, PMF>();
-    case 13: return pass_fn<6, kBigBlock, DIRECT, PMF>();
-    case 14: return pass_fn<7, 256, DIRECT, PMF>();
-    case 15: return pass_fn<7, kBigBlock, DIRECT, PMF>();
-    case 16: return pass_fn<8, 256, DIRECT, PMF>();
-    case 17: return pass_fn<8, kBigBlock, DIRECT, PMF>();
+    case 2: return pass_fn<1, 256, DIRECT, PMF, SOFT>();
+    case 3: return pass_fn<1, kBigBlock, DIRECT, PMF, SOFT>();
+    case 4: return pass_fn<2, 256, DIRECT, PMF, SOFT>();
+    case 5: return pass_fn<2, kBigBlock, DIRECT, PMF, SOFT>();
+    case 6: return pass_fn<3, 256, DIRECT, PMF, SOFT>();
+    case 7: return pass_fn<3, kBigBlock, DIRECT, PMF, SOFT>();
+    case 8: return pass_fn<4, 256, DIRECT, PMF, SOFT>();
+    case 9: return pass_fn<4, kBigBlock, DIRECT, PMF, SOFT>();
+    case 10: return pass_fn<5, 256, DIRECT, PMF, SOFT>();
+    case 11: return pass_fn<5, kBigBlock, DIRECT, PMF, SOFT>();
+    case 12: return pass_fn<6, 256, DIRECT, PMF, SOFT>();
+    case 13: return pass_fn<6, kBigBlock, DIRECT, PMF, SOFT>();
+    case 14: return pass_fn<7, 256, DIRECT, PMF, SOFT>();
+    case 15: return pass_fn<7, kBigBlock, DIRECT, PMF, SOFT>();
+    case 16: return pass_fn<8, 256, DIRECT, PMF, SOFT>();
+    case 17: return pass_fn<8, kBigBlock, DIRECT, PMF, SOFT>();
   }
   return nullptr;
 }

@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   constexpr bool LIN = !F16 && !SOFT && MB >= 7;
   // one-thread teams (q <= 16): the check node's scatter goes to the group's consumed stage buffer in a
   // lane-major layout xs[w][lane] (conflict-free; ncu, C5: the row-major scatter replayed 3.6x)
-  constexpr bool LANEMAJOR = TT == 1 && !F16 && Q >= 2;
+  constexpr bool LANEMAJOR = TT == 1 && Q >= 2;
   // the interleaved team pairs of tot_prod_il: measured neutral on C4 (conflict replays -14%, instructions
   // +7%), kept off; NB_PAIRIL=1 builds it
 #ifdef NB_PAIRIL
@@ -1316,7 +1316,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
                 asm volatile("st.shared.b32 [%0], %1;" ::"r"(il_s + ((uint32_t)oidx[r] << 3)), "r"(up[r]) : "memory");
               }
             } else if constexpr (LANEMAJOR) {
-              const uint32_t xs_s = smem_u32(GST + buf * GBLK) + ((uint32_t)(tid - grp * GT) << 2);
+              // the group's consumed stage buffer (F16: its float work rows), 32 q floats
+              const uint32_t xs_s = smem_u32(F16 ? GST + NS * GBLKH : GST + buf * GBLK) + ((uint32_t)(tid - grp * GT) << 2);
 #pragma unroll
               for (int r = 0; r < R; ++r) {
                 NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
@@ -1350,7 +1351,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               default: tot_prod<R, R, TT, C::QS>(smem, gbase + buf * GBLK, SPLIT, cvalid); break;
             }
           } else if constexpr (LANEMAJOR) {
-            const float* xs = GST + buf * GBLK;
+            const float* xs = F16 ? GST + NS * GBLKH : GST + buf * GBLK;
             const int c0 = (lc - grp * CPG) * KT;
             switch (JPT) {
               case 1: tot_sum_lm<R, 1>(xs, c0, TOT, wgrp, SPLIT, pck, cvalid); break;

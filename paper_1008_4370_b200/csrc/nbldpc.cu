@@ -166,7 +166,10 @@ void free_workspace(Workspace& w) {
   w = Workspace{};
 }
 
-using nbk::pass_kernel_ptr;
+// the slot-pass kernel for a VN variant (0 separable, 1 direct, 2 pmf), soft = 1: its soft-output instantiation
+void* pass_kernel_ptr(int m, int big, int direct, int soft = 0) {
+  return soft ? nbk::pass_kernel_soft_ptr(m, big, direct) : nbk::pass_kernel_ptr(m, big, direct);
+}
 using nbk::persist_kp_ptr;
 
 // pmf = 1: the nbldpc_decode_pmf variant; f16 = 1: half-precision messages (NBLDPC_MSG_F16);
@@ -215,14 +218,14 @@ cudaError_t launch_cluster(const nbldpc_code_s* c, const nb::ClusterParams& P, i
 // cudaFuncAttributeMaxDynamicSharedMemorySize is a property of the kernel (one instantiation per
 // (m, block variant)) shared by every code on the device: only ever raise it.
 std::mutex g_attr_mu;
-size_t g_attr_smem[64][54] = {};
+size_t g_attr_smem[64][108] = {};
 
 cudaError_t ensure_smem_attr(const nbldpc_code_s* c) {
   std::lock_guard<std::mutex> lk(g_attr_mu);
-  for (int direct = 0; direct < 3; ++direct) {
-    const int d = c->device & 63, k = (c->m * 2 + c->big) * 3 + direct;
+  for (int direct = 0; direct < 6; ++direct) {  // 3 VN variants x {plain, soft}
+    const int d = c->device & 63, k = (c->m * 2 + c->big) * 6 + direct;
     if (g_attr_smem[d][k] >= c->smem) continue;
-    cudaError_t e = cudaFuncSetAttribute(pass_kernel_ptr(c->m, c->big, direct),
+    cudaError_t e = cudaFuncSetAttribute(pass_kernel_ptr(c->m, c->big, direct % 3, direct / 3),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem);
     if (e != cudaSuccess) return e;
     g_attr_smem[d][k] = c->smem;
@@ -444,14 +447,14 @@ nb::ClusterParams make_cparams(const nbldpc_code_s* c, int step_mode, int step_i
 
 dim3 pass_grid(const nbldpc_code_s* c) { return dim3((unsigned)(c->groups * c->ws.Y)); }
 
-cudaError_t launch_pass(const nbldpc_code_s* c, const PassParams& P, int direct, cudaStream_t st) {
+cudaError_t launch_pass(const nbldpc_code_s* c, const PassParams& P, int direct, cudaStream_t st, int soft = 0) {
   void* args[] = {const_cast<PassParams*>(&P)};
-  return cudaLaunchKernel(pass_kernel_ptr(c->m, c->big, direct), pass_grid(c), dim3(c->block), args, c->smem, st);
+  return cudaLaunchKernel(pass_kernel_ptr(c->m, c->big, direct, soft), pass_grid(c), dim3(c->block), args, c->smem, st);
 }
 
-nbldpc_status_t build_graph(nbldpc_code_s* c, int direct) {
+nbldpc_status_t build_graph(nbldpc_code_s* c, int direct, int soft = 0) {
   Workspace& w = c->ws;
-  if (w.graph && w.graph_direct == direct) return NBLDPC_OK;
+  if (w.graph && w.graph_direct == direct + 3 * soft) return NBLDPC_OK;
   if (w.graph) {
     cudaGraphExecDestroy(w.graph);
     w.graph = nullptr;
@@ -477,7 +480,7 @@ nbldpc_status_t build_graph(nbldpc_code_s* c, int direct) {
   for (int i = 0; i < kPassesPerGraphIter; ++i) {
     cudaGraphNodeParams kp = {};
     kp.type = cudaGraphNodeTypeKernel;
-    kp.kernel.func = pass_kernel_ptr(c->m, c->big, direct);
+    kp.kernel.func = pass_kernel_ptr(c->m, c->big, direct, soft);
     kp.kernel.gridDim = pass_grid(c);
     kp.kernel.blockDim = dim3(c->block);
     kp.kernel.sharedMemBytes = (unsigned)c->smem;
@@ -505,7 +508,7 @@ nbldpc_status_t build_graph(nbldpc_code_s* c, int direct) {
     w.graph = nullptr;
     return cuda_status(e);
   }
-  w.graph_direct = direct;
+  w.graph_direct = direct + 3 * soft;
   return NBLDPC_OK;
 }
 
@@ -589,7 +592,7 @@ nbldpc_status_t decode_general(nbldpc_code_s* c, const float* llr, const float* 
   if (teams < 1) return NBLDPC_ERR_UNSUPPORTED;
   const int threads = ((teams * tt + 31) / 32) * 32;
   const size_t smem = teams * per_team + tables;
-  void* fn = gen_kernel_ptr(c->m);
+  void* fn = gen_kernel_ptr(c->m, soft != nullptr);
   NB_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   NB_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
@@ -773,7 +776,7 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
     return mark_done(w, st);
   }
   if (use_graph >= 0) {
-    rs = build_graph(c, direct);
+    rs = build_graph(c, direct, soft != nullptr);
     if (rs != NBLDPC_OK) return rs;
     NB_TRY(cudaGraphLaunch(w.graph, st));
     return mark_done(w, st);
@@ -782,7 +785,7 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
   PassParams P = make_params(c, 0, nullptr);
   for (;;) {
     for (int i = 0; i < kPassesPerGraphIter; ++i) {
-      NB_TRY(launch_pass(c, P, direct, st));
+      NB_TRY(launch_pass(c, P, direct, st, soft != nullptr));
       w.last_host_launches++;
     }
     NB_TRY(cudaMemcpyAsync(w.host_flag, w.dev.glob + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -1378,7 +1381,7 @@ nbldpc_status_t step_impl(nbldpc_code_t c, const float* llr, const float* pmf, i
   }
   if (vn_algorithm) {
     PassParams P = make_params(c, 1, u_out);
-    NB_TRY(launch_pass(c, P, 1, st));
+    NB_TRY(launch_pass(c, P, 1, st, soft != nullptr));
   } else {
     nb::ClusterParams PP = make_cparams(c, 1, iter, u_out);
     NB_TRY(launch_cluster(c, PP, std::min(frames, c->p_ncl), st, pmf != nullptr, 0, 0, soft != nullptr));
