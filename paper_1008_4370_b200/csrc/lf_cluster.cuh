@@ -590,7 +590,11 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   constexpr bool LIN = !F16 && !SOFT && MB >= 7;
   // one-thread teams (q <= 16): the check node's scatter goes to the group's consumed stage buffer in a
   // lane-major layout xs[w][lane] (conflict-free; ncu, C5: the row-major scatter replayed 3.6x)
+#ifdef NB_LANEMAJOR_F16
   constexpr bool LANEMAJOR = TT == 1 && Q >= 2;
+#else
+  constexpr bool LANEMAJOR = TT == 1 && !F16 && Q >= 2;
+#endif
   // the interleaved team pairs of tot_prod_il: measured neutral on C4 (conflict replays -14%, instructions
   // +7%), kept off; NB_PAIRIL=1 builds it
 #ifdef NB_PAIRIL
