@@ -1077,10 +1077,79 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             }
           }
           if constexpr (TT > 1) __syncwarp();
+          // q = 256 (two teams per warp, WARPDEC): the decision of a deciding team is computed by the whole
+          // warp -- the other team's lanes take the upper half of its entries (x by one shuffle each, D
+          // from the deciding team's row) -- so a warp pays half a decision per deciding team; the host
+          // orients the warp graph so that every warp has exactly one deciding team
+          // measured slower (C4 3,592 -> 3,882, C3 853 -> 935 ns/frame-iter: every warp then runs a decision
+          // round, and the other CTA on the SM hid most of the imbalance it removes); NB_WARPDEC=1 builds it
+#ifdef NB_WARPDEC
+          constexpr bool WARPDEC = TT == 16 && !SYM && !SOFT;
+#else
+          constexpr bool WARPDEC = false;
+#endif
+          uint32_t wd_bits = 0;
+          if constexpr (WARPDEC) {
+            if (mode == 0) {
+              const bool dec0 = __shfl_sync(0xffffffffu, (int)is_a, 0) != 0;
+              const bool dec1 = __shfl_sync(0xffffffffu, (int)is_a, 16) != 0;
+#pragma unroll 1
+              for (int T = 0; T < 2; ++T) {
+                if (!(T == 0 ? dec0 : dec1)) continue;  // warp-uniform
+                const bool inT = (lane >> 4) == T;
+                const int hh = inT ? 0 : 1;  // the half of team T's 16 phase-B entries this lane takes
+                float xs[8];
+#pragma unroll
+                for (int hp = 0; hp < 8; ++hp) {
+                  const float o = __shfl_xor_sync(0xffffffffu, x[8 + hp], 16);
+                  xs[hp] = inT ? x[hp] : o;
+                }
+                const int trT = (trow & ~1) | T;
+                const float* DT = F16 ? GST + NS * GBLKH + trT * C::QS : GST + buf * GBLK + trT * C::QS;
+                const int dxT = T ? 16 : 0;
+                float dh[8], dq[8];
+#pragma unroll
+                for (int c4 = 0; c4 < 2; ++c4) {
+                  const float4 a4 = *reinterpret_cast<const float4*>(DT + (dxT ^ db_word(t, 8 * hh + 4 * c4)));
+                  const float4 b4 = *reinterpret_cast<const float4*>(DT + (dxT ^ db_word(t, 8 * (1 - hh) + 4 * c4)));
+                  dh[4 * c4] = a4.x; dh[4 * c4 + 1] = a4.y; dh[4 * c4 + 2] = a4.z; dh[4 * c4 + 3] = a4.w;
+                  dq[4 * c4] = b4.x; dq[4 * c4 + 1] = b4.y; dq[4 * c4 + 2] = b4.z; dq[4 * c4 + 3] = b4.w;
+                }
+                float2 acc[MB + 1];
+#pragma unroll
+                for (int b = 0; b <= MB; ++b) acc[b] = make_float2(0.0f, 0.0f);
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                  const float2 xp = make_float2(xs[2 * p], xs[2 * p + 1]);
+                  acc[0] = __ffma2_rn(xp, make_float2(dh[2 * p], dh[2 * p + 1]), acc[0]);
+                  acc[5] = __ffma2_rn(xp, make_float2(dh[2 * p + 1], dh[2 * p]), acc[5]);                    // z bit 4
+                  acc[6] = __ffma2_rn(xp, make_float2(dh[(2 * p) ^ 2], dh[((2 * p) ^ 2) + 1]), acc[6]);      // z bit 5
+                  acc[7] = __ffma2_rn(xp, make_float2(dh[(2 * p) ^ 4], dh[((2 * p) ^ 4) + 1]), acc[7]);      // z bit 6
+                  acc[8] = __ffma2_rn(xp, make_float2(dq[2 * p], dq[2 * p + 1]), acc[8]);                    // z bit 7
+                }
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {  // z bits 0..3: the partner rows t ^ 2^b
+                  const int tp = t ^ (1 << b);
+#pragma unroll
+                  for (int c4 = 0; c4 < 2; ++c4) {
+                    const float4 v4 = *reinterpret_cast<const float4*>(DT + (dxT ^ db_word(tp, 8 * hh + 4 * c4)));
+                    acc[b + 1] = __ffma2_rn(make_float2(xs[4 * c4], xs[4 * c4 + 1]), make_float2(v4.x, v4.y), acc[b + 1]);
+                    acc[b + 1] = __ffma2_rn(make_float2(xs[4 * c4 + 2], xs[4 * c4 + 3]), make_float2(v4.z, v4.w), acc[b + 1]);
+                  }
+                }
+                float mw[MB + 1];
+#pragma unroll
+                for (int b = 0; b <= MB; ++b) mw[b] = acc[b].x + acc[b].y;
+                int so = 0, sn = MB + 1;
+                const uint32_t bits = team_sign_bits<MB + 1, 32>(mw, lane, so, sn);
+                if (inT) wd_bits = bits;
+              }
+            }
+          }
           float mf[MB + 1];
 #pragma unroll
           for (int b = 0; b <= MB; ++b) mf[b] = 0.0f;
-          if (is_a) {
+          if (is_a && !(WARPDEC && mode == 0)) {
             // pairwise FFMA2 dot products: M(0) and the register-bit points in-thread, the
             // thread-bit points against the partner thread's row
             float d[R];
@@ -1207,6 +1276,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             sbits = 0;
 #pragma unroll
             for (int b = 0; b <= MB; ++b) sbits |= (md[b] < 0.0 ? 1u : 0u) << b;
+          } else if (WARPDEC && mode == 0) {
+            sbits = wd_bits;
           } else if constexpr (TT >= NB_RS_MIN_TT) {
             sbits = team_sign_bits<MB + 1, TT>(mf, lane, s_off, s_n);
           } else if constexpr (TT > 1) {  // small teams: full butterfly all-reduce, every lane holds all totals

@@ -803,7 +803,42 @@ nbldpc_status_t decode_impl(nbldpc_code_s* c, const float* llr, int frames, int 
 // edges are variables (greedy: repeatedly the group covering most uncovered variables), and let each
 // variable decide in a covering group.  (Measured cover: 82% of the checks of C4, 73% of C3, against
 // 57% of the warps at warp granularity -- every check of those had some deciding warp.)
+// q = 256 (tt = 16, two edge slots per warp): the cluster kernel computes a deciding team's decision with
+// the whole warp (WARPDEC), so the best assignment gives every warp exactly one deciding slot.  The graph
+// whose nodes are warps and whose edges are variables has degree <= 2 (a path or a cycle per component);
+// walking each component and handing every variable to the warp the walk arrives at gives every warp at
+// most one (on a cycle exactly one) deciding slot.
+void orient_decision_owners(std::vector<EdgeDev>& edges, int E) {
+  const int nw = (E + 1) / 2;
+  std::vector<int> deg(nw, 0);
+  for (int e = 0; e < E; ++e)
+    if (edges[e].var >= 0) deg[e / 2]++;
+  std::vector<char> done(E, 0);  // indexed by either slot of a variable (both set when assigned)
+  auto walk = [&](int w) {
+    for (;;) {
+      int e = -1;
+      for (int k = 2 * w; k < std::min(E, 2 * w + 2); ++k)
+        if (edges[k].var >= 0 && !done[k]) { e = k; break; }
+      if (e < 0) return;
+      const int o = edges[e].partner;  // the variable's other slot; its warp decides
+      done[e] = done[o] = 1;
+      edges[e].is_a = 0;
+      edges[o].is_a = 1;
+      w = o / 2;
+    }
+  };
+  for (int w = 0; w < nw; ++w)
+    if (deg[w] == 1) walk(w);  // paths from one end first
+  for (int w = 0; w < nw; ++w) walk(w);  // then the cycles
+}
+
 void assign_decision_owners(std::vector<EdgeDev>& edges, int E, int tt, int kpad) {
+#ifdef NB_WARPDEC
+  if (tt == 16) {  // goes with the kernel's WARPDEC (off by default, see lf_cluster.cuh)
+    orient_decision_owners(edges, E);
+    return;
+  }
+#endif
   const int per = std::max(32 / tt, kpad);  // edge slots per barrier group
   const int nw = (E + per - 1) / per;
   std::vector<int> deg(nw, 0);
