@@ -253,7 +253,9 @@ __device__ __forceinline__ void dsmem_or(uint32_t addr, int v) {
 // TOT(w) = sum_j X_j(w) over the thread's WPT w's (stride TT*JPT) and JPT teams (stride TEAM words)
 template <int R, int JPT, int TT, int TEAM>
 __device__ __forceinline__ void tot_sum(const float* smem, int gbase, float* TOT, int wgrp, int split, int pck,
-                                        bool cvalid) {
+                                        bool cvalid, int ix = 0) {
+  // ix: XOR on the w-group index i (the odd check of a warp holding two checks takes its w's in the order
+  // i ^ 1, so the two checks' loads and TOT stores fall in different bank halves)
   constexpr int WPT = R / JPT;
   const float* g = smem + gbase;
   // one w split over lanes (WPT == 1): the lanes of a w read rows JPT apart, which for TEAM * JPT = 0 mod 32
@@ -264,9 +266,10 @@ __device__ __forceinline__ void tot_sum(const float* smem, int gbase, float* TOT
   for (int i = 0; i < WPT; ++i) {
     float mag = 0.0f;
     uint32_t sg = 0;
+    const int iw = WPT > 1 ? (i ^ ix) : i;
 #pragma unroll
     for (int jj = 0; jj < JPT; ++jj) {
-      const float v = g[((JPT > 1 ? jj ^ jx : jj)) * TEAM + i * TT * JPT];
+      const float v = g[((JPT > 1 ? jj ^ jx : jj)) * TEAM + iw * TT * JPT];
       mag += fabsf(v);
       sg ^= __float_as_uint(v);
     }
@@ -277,7 +280,7 @@ __device__ __forceinline__ void tot_sum(const float* smem, int gbase, float* TOT
       }
     }
     if (cvalid && (WPT > 1 || (pck & (split - 1)) == 0))
-      TOT[wgrp + TT * JPT * i] = __uint_as_float(__float_as_uint(mag) | (sg & kSign));
+      TOT[wgrp + TT * JPT * iw] = __uint_as_float(__float_as_uint(mag) | (sg & kSign));
   }
 }
 
@@ -294,6 +297,7 @@ __device__ __forceinline__ void tot_sum_lm(const float* xs, int c0, float* TOT, 
   for (int i = 0; i < WPT; ++i) {
     const int w = wgrp + JPT * i;
     const float* g = xs + 32 * w + jb;
+    NB_CHECK(w < R * (32 / (JPT * split) > 0 ? 32 : 32) && jb + JPT <= 32);
     float mag = 0.0f;
     uint32_t sg = 0;
 #pragma unroll
@@ -540,6 +544,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   const int JPT = KT / SPLIT;
   const int wgrp = pck / SPLIT;
   const int jbase = (pck % SPLIT) * JPT;
+  const int tix = (TPC == 16) ? (lc & 1) : 0;  // tot_sum's i rotation for the odd check of a warp
   const int gbase = in_check ? (int)(GST - smem) + (F16 ? NS * GBLKH : 0) + ((lc - grp * CPG) * KT + jbase) * C::QS + wgrp
                              : 0;  // + buf * GBLK (F32: the consumed stage rows; F16: the work rows)
   // my phase-B z's
@@ -741,6 +746,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           if (act) {
             const float* srcp = call->p0buf + ((size_t)slot * cd.N + (rr.var_h >> 8)) * Q;
             float* dstp = PB + ((size_t)b * nteams + team) * Q;
+            NB_CHECK((rr.var_h >> 8) < (uint32_t)cd.N && b < NS && team < nteams);
 #pragma unroll
             for (int c4 = 0; c4 < Q / 4; ++c4)
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dstp + 4 * c4)), "l"(srcp + 4 * c4)
@@ -929,15 +935,18 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             bfly_regs<R, 0, LR>(x, th);  // z bits 0..LR-1
           }
           if constexpr (TT > 1) {
-            // transposition through the consumed stage buffer, chunk-swizzled layout tpos(z)
+            // transposition through the consumed stage buffer, chunk-swizzled layout tpos(z); at q = 64 two
+            // teams share each quarter warp and their rows are 64 words apart (the same banks), so the odd
+            // team XORs its words by 16 (the other half of the bank quads): conflict-free both ways
+            const int tpx = (TT == 4 && (trow & 1)) ? 16 : 0;
             __syncwarp();  // every thread of the team has read its phase-A chunks
 #pragma unroll
             for (int ch = 0; ch < 4; ++ch)
-              *reinterpret_cast<float4*>(st + tpos(16 * t + 4 * ch)) = make_float4(x[4 * ch], x[4 * ch + 1], x[4 * ch + 2], x[4 * ch + 3]);
+              *reinterpret_cast<float4*>(st + (tpx ^ tpos(16 * t + 4 * ch))) = make_float4(x[4 * ch], x[4 * ch + 1], x[4 * ch + 2], x[4 * ch + 3]);
             __syncwarp();
 #pragma unroll
             for (int h = 0; h < TT; ++h) {
-              const float* src = st + tpos((t << LJ) | (h << 4));
+              const float* src = st + (tpx ^ tpos((t << LJ) | (h << 4)));
               if constexpr (LJ == 0) {
                 x[h] = src[0];
               } else if constexpr (LJ == 1) {
@@ -946,7 +955,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               } else {
 #pragma unroll
                 for (int q4 = 0; q4 < (1 << LJ) / 4; ++q4) {
-                  const float4 v = *reinterpret_cast<const float4*>(st + tpos(((t << LJ) | (h << 4)) + 4 * q4));
+                  const float4 v = *reinterpret_cast<const float4*>(st + (tpx ^ tpos(((t << LJ) | (h << 4)) + 4 * q4)));
                   x[(h << LJ) + 4 * q4] = v.x; x[(h << LJ) + 4 * q4 + 1] = v.y;
                   x[(h << LJ) + 4 * q4 + 2] = v.z; x[(h << LJ) + 4 * q4 + 3] = v.w;
                 }
@@ -1024,7 +1033,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           float* DB = st;
           // two teams per warp (q = 256): their rows are 1 KB apart (the same banks), so the odd team's D words
           // are XOR-ed by 16 (the other half of the banks) -- the scalar D stores no longer collide
-          const int dbx = (TT == 16 && (trow & 1)) ? 16 : 0;
+          const int dbx = ((TT == 16 || TT == 4) && (trow & 1)) ? 16 : 0;
           if constexpr (TT > 1) __syncwarp();  // transposition reads done
           if constexpr (F16) {
             if (is_a) {
@@ -1395,7 +1404,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               const uint32_t xs_s = smem_u32(F16 ? GST + NS * GBLKH : GST + buf * GBLK) + ((uint32_t)(tid - grp * GT) << 2);
 #pragma unroll
               for (int r = 0; r < R; ++r) {
-                NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
+                NB_CHECK(oidx[r] >= 0 && oidx[r] < Q && 32 * Q <= GBLK && tid - grp * GT < 32);
                 asm volatile("st.shared.b32 [%0], %1;" ::"r"(xs_s + ((uint32_t)oidx[r] << 7)), "r"(up[r]) : "memory");
               }
             } else {
@@ -1435,12 +1444,12 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               case 8: tot_sum_lm<R, (R >= 8 ? 8 : 1)>(xs, c0, TOT, wgrp, SPLIT, pck, cvalid); break;
               default: tot_sum_lm<R, R>(xs, c0, TOT, wgrp, SPLIT, pck, cvalid); break;
             }
-          } else switch (JPT) {
-            case 1: tot_sum<R, 1, TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid); break;
-            case 2: tot_sum<R, (R >= 2 ? 2 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid); break;
-            case 4: tot_sum<R, (R >= 4 ? 4 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid); break;
-            case 8: tot_sum<R, (R >= 8 ? 8 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid); break;
-            default: tot_sum<R, R, TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid); break;
+          } else switch (JPT) {  // tix: two checks per warp -> the odd one rotates its w groups
+            case 1: tot_sum<R, 1, TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid, tix); break;
+            case 2: tot_sum<R, (R >= 2 ? 2 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid, tix); break;
+            case 4: tot_sum<R, (R >= 4 ? 4 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid, tix); break;
+            case 8: tot_sum<R, (R >= 8 ? 8 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid, tix); break;
+            default: tot_sum<R, R, TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid, tix); break;
           }
           check_sync(lc, TPC);
           if (active) {
