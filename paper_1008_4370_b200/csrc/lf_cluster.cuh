@@ -825,7 +825,14 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         {
           const float tv[8] = {thc[0].x, thc[0].y, thc[0].z, thc[0].w, thc[1].x, thc[1].y, thc[1].z, thc[1].w};
 #pragma unroll
-          for (int b = 0; b < MB; ++b) th[b] = (active && !PMF) ? (C::THREG ? tv[b] : THB[buf * nteams * 8 + b]) : 0.0f;
+          float tb8[8];
+          if constexpr (!C::THREG) {  // the team's staged row of 8 channel terms: two 16-byte loads (broadcast)
+            const float4 a4 = *reinterpret_cast<const float4*>(THB + buf * nteams * 8);
+            const float4 b4 = *reinterpret_cast<const float4*>(THB + buf * nteams * 8 + 4);
+            tb8[0] = a4.x; tb8[1] = a4.y; tb8[2] = a4.z; tb8[3] = a4.w; tb8[4] = b4.x; tb8[5] = b4.y; tb8[6] = b4.z; tb8[7] = b4.w;
+          }
+#pragma unroll
+          for (int b = 0; b < MB; ++b) th[b] = (active && !PMF) ? (C::THREG ? tv[b] : tb8[b]) : 0.0f;
         }
         // pmf input: my R entries of p_v at the phase-B coordinates zr, straight from L2
         float pv[PMF ? R : 1];
@@ -1033,7 +1040,9 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           float* DB = st;
           // two teams per warp (q = 256): their rows are 1 KB apart (the same banks), so the odd team's D words
           // are XOR-ed by 16 (the other half of the banks) -- the scalar D stores no longer collide
-          const int dbx = ((TT == 16 || TT == 4) && (trow & 1)) ? 16 : 0;
+          // (q = 64: XOR 24 -- the writes need the other half of the bank quads (^16), the row reads the
+          // complementary quads within a half (^8))
+          const int dbx = (trow & 1) ? (TT == 16 ? 16 : TT == 4 ? 24 : 0) : 0;
           if constexpr (TT > 1) __syncwarp();  // transposition reads done
           if constexpr (F16) {
             if (is_a) {
