@@ -951,13 +951,19 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             for (int ch = 0; ch < 4; ++ch)
               *reinterpret_cast<float4*>(st + (tpx ^ tpos(16 * t + 4 * ch))) = make_float4(x[4 * ch], x[4 * ch + 1], x[4 * ch + 2], x[4 * ch + 3]);
             __syncwarp();
+            // LJ <= 1 (q >= 128): tpos((t << LJ) | (h << 4)) = 16 h + (((a ^ h ^ (h >> 2)) & 3) << 2) + ((t << LJ) & 3)
+            // with a = ((t << LJ) >> 2) & 3 -- four row pointers, then every read is [pointer + 64 h bytes]
+            const float* pc[4];
+            if constexpr (LJ <= 1) {
+#pragma unroll
+              for (int c = 0; c < 4; ++c) pc[c] = st + (((((t << LJ) >> 2) ^ c) & 3) << 2) + ((t << LJ) & 3);
+            }
 #pragma unroll
             for (int h = 0; h < TT; ++h) {
-              const float* src = st + (tpx ^ tpos((t << LJ) | (h << 4)));
               if constexpr (LJ == 0) {
-                x[h] = src[0];
+                x[h] = pc[(h ^ (h >> 2)) & 3][16 * h];
               } else if constexpr (LJ == 1) {
-                const float2 v = *reinterpret_cast<const float2*>(src);
+                const float2 v = *reinterpret_cast<const float2*>(pc[(h ^ (h >> 2)) & 3] + 16 * h);
                 x[2 * h] = v.x; x[2 * h + 1] = v.y;
               } else {
 #pragma unroll
@@ -1056,6 +1062,9 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           }
           if (is_a) {
             if constexpr (TT > 1) {
+              // LJ == 0: the even / odd D rows of my team (dbx = 16 for the odd team of the warp swaps them)
+              float* const dbe = DB + (dbx & 16) + (t & 3);
+              float* const dbo = DB + (16 ^ (dbx & 16)) + (t & 3);
 #pragma unroll
               for (int ch = 0; ch < 4; ++ch) {
                 const float4 v = wo4[ch];
@@ -1070,8 +1079,14 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
                   *reinterpret_cast<float2*>(DB + (dbx ^ db_word(2 * ch, t << 1))) = make_float2(d4[0], d4[1]);
                   *reinterpret_cast<float2*>(DB + (dbx ^ db_word(2 * ch + 1, t << 1))) = make_float2(d4[2], d4[3]);
                 } else {
+                  // DB[dbx ^ db_word(tb, t)], tb = 4 ch + k4: the XOR 16 flips tb's bit 0, so the word is
+                  // 32 (tb >> 1) + 16 ((tb & 1) ^ odd) + (((a ^ (tb >> 1)) & 3) << 2) + (t & 3), a = (t >> 2) & 3
 #pragma unroll
-                  for (int k4 = 0; k4 < 4; ++k4) DB[dbx ^ db_word(4 * ch + k4, t)] = d4[k4];
+                  for (int k4 = 0; k4 < 4; ++k4) {
+                    const int tb = 4 * ch + k4;
+                    float* const rowp = ((tb & 1) ? dbo : dbe) + 32 * (tb >> 1);
+                    rowp[((((t >> 2) ^ (tb >> 1)) & 3) << 2)] = d4[k4];
+                  }
                 }
               }
             } else if (mode == 1 || SYM) {
@@ -1171,10 +1186,13 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             // pairwise FFMA2 dot products: M(0) and the register-bit points in-thread, the
             // thread-bit points against the partner thread's row
             float d[R];
+            // dbx ^ db_word(t ^ m, 4 ch) = Lt ^ 16 m ^ 4 ((m >> 1) & 3) ^ 4 ch (the fields are disjoint, the map
+            // XOR-linear): one XOR with a constant per 16-byte read
+            const int Lt = dbx ^ (16 * t) ^ (((t >> 1) & 3) << 2);
             if constexpr (TT > 1) {
 #pragma unroll
               for (int ch = 0; ch < 4; ++ch) {
-                const float4 v4 = *reinterpret_cast<const float4*>(DB + (dbx ^ db_word(t, 4 * ch)));
+                const float4 v4 = *reinterpret_cast<const float4*>(DB + (Lt ^ (4 * ch)));
                 d[4 * ch] = v4.x; d[4 * ch + 1] = v4.y; d[4 * ch + 2] = v4.z; d[4 * ch + 3] = v4.w;
               }
             } else {
@@ -1203,10 +1221,10 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               if constexpr (TT > 1) {
 #pragma unroll
                 for (int b = 0; b < MB - 4; ++b) {
-                  const int tp = t ^ (1 << b);
+                  const int cm = (16 << b) ^ ((((1 << b) >> 1) & 3) << 2);  // the row t ^ 2^b
 #pragma unroll
                   for (int ch = 0; ch < 4; ++ch) {
-                    const float4 v4 = *reinterpret_cast<const float4*>(DB + (dbx ^ db_word(tp, 4 * ch)));
+                    const float4 v4 = *reinterpret_cast<const float4*>(DB + (Lt ^ cm ^ (4 * ch)));
                     acc[LJ + b + 1] = __ffma2_rn(make_float2(x[4 * ch], x[4 * ch + 1]), make_float2(v4.x, v4.y),
                                                  acc[LJ + b + 1]);
                     acc[LJ + b + 1] = __ffma2_rn(make_float2(x[4 * ch + 2], x[4 * ch + 3]), make_float2(v4.z, v4.w),
