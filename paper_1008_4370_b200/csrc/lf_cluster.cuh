@@ -59,6 +59,10 @@ struct EdgeRec {
   uint32_t var_h;     // variable << 8 | h_cv
 };
 
+// bytes added to the cluster kernels' dynamic shared memory so that the kernel can align its base to a
+// message row (q floats, q <= 256)
+constexpr uint32_t kSmemAlignPad = 1024;
+
 template <int MB>
 struct CCfg {
   static constexpr int Q = 1 << MB;
@@ -476,7 +480,14 @@ template <int MB, int NTHR, bool PMF = false, bool F16 = false, int KP = 0, bool
 __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_cluster_kernel(ClusterParams P) {
   using C = CCfg<MB>;
   constexpr int Q = C::Q, R = C::R, TT = C::TT, LR = C::LR, LJ = C::LJ, CH = C::CH;
-  extern __shared__ __align__(16) float smem[];
+  extern __shared__ __align__(16) float smem_raw[];
+  // LIN (q >= 128): the dynamic region starts on a q-float boundary of the shared window (the host adds
+  // kSmemAlignPad bytes), so that a team row's shared address ORs with an entry's byte offset -- the check
+  // node's scatter / read-back addresses are then the XOR chain itself (no per-entry address arithmetic)
+  float* const smem = MB >= 7 ? reinterpret_cast<float*>(reinterpret_cast<char*>(smem_raw) +
+                                                         ((kSmemAlignPad - (smem_u32(smem_raw) & (kSmemAlignPad - 1))) &
+                                                          (kSmemAlignPad - 1)))
+                              : smem_raw;
   __shared__ int sh_frame, sh_flag[2], sh_bad;
   __shared__ __align__(8) uint64_t sh_mbar[8 * C::NS];  // [group][buffer]: the group's teams arrive, bulk copies complete_tx
 
@@ -832,7 +843,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             tb8[0] = a4.x; tb8[1] = a4.y; tb8[2] = a4.z; tb8[3] = a4.w; tb8[4] = b4.x; tb8[5] = b4.y; tb8[6] = b4.z; tb8[7] = b4.w;
           }
 #pragma unroll
-          for (int b = 0; b < MB; ++b) th[b] = (active && !PMF) ? (C::THREG ? tv[b] : tb8[b]) : 0.0f;
+          // (an inactive padding team's terms are never used: its outputs become the neutral message below)
+          for (int b = 0; b < MB; ++b) th[b] = !PMF ? (C::THREG ? tv[b] : tb8[b]) : 0.0f;
         }
         // pmf input: my R entries of p_v at the phase-B coordinates zr, straight from L2
         float pv[PMF ? R : 1];
@@ -946,22 +958,29 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             // teams share each quarter warp and their rows are 64 words apart (the same banks), so the odd
             // team XORs its words by 16 (the other half of the bank quads): conflict-free both ways
             const int tpx = (TT == 4 && (trow & 1)) ? 16 : 0;
+            // q = 256 (two teams per warp, rows 1 KB apart): the odd team stores 16-entry block b at block
+            // (b + 1) mod 16 of its row, so that in every phase-B read the two teams' words differ in bank
+            // bit 4 (ncu: the unshifted reads replayed 2x); the phase-A stores stay conflict-free
+            const int tsh = (TT == 16 && (trow & 1)) ? 1 : 0;
             __syncwarp();  // every thread of the team has read its phase-A chunks
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch)
-              *reinterpret_cast<float4*>(st + (tpx ^ tpos(16 * t + 4 * ch))) = make_float4(x[4 * ch], x[4 * ch + 1], x[4 * ch + 2], x[4 * ch + 3]);
+            for (int ch = 0; ch < 4; ++ch) {
+              const int wa = TT == 16 ? (16 * ((t + tsh) & 15) + (tpos(16 * t + 4 * ch) & 15)) : (tpx ^ tpos(16 * t + 4 * ch));
+              *reinterpret_cast<float4*>(st + wa) = make_float4(x[4 * ch], x[4 * ch + 1], x[4 * ch + 2], x[4 * ch + 3]);
+            }
             __syncwarp();
             // LJ <= 1 (q >= 128): tpos((t << LJ) | (h << 4)) = 16 h + (((a ^ h ^ (h >> 2)) & 3) << 2) + ((t << LJ) & 3)
             // with a = ((t << LJ) >> 2) & 3 -- four row pointers, then every read is [pointer + 64 h bytes]
+            // (q = 256, odd team: + 16 words, and block 15 wraps to block 0)
             const float* pc[4];
             if constexpr (LJ <= 1) {
 #pragma unroll
-              for (int c = 0; c < 4; ++c) pc[c] = st + (((((t << LJ) >> 2) ^ c) & 3) << 2) + ((t << LJ) & 3);
+              for (int c = 0; c < 4; ++c) pc[c] = st + 16 * tsh + (((((t << LJ) >> 2) ^ c) & 3) << 2) + ((t << LJ) & 3);
             }
 #pragma unroll
             for (int h = 0; h < TT; ++h) {
               if constexpr (LJ == 0) {
-                x[h] = pc[(h ^ (h >> 2)) & 3][16 * h];
+                x[h] = (TT == 16 && h == 15) ? pc[0][tsh ? -16 : 240] : pc[(h ^ (h >> 2)) & 3][16 * h];
               } else if constexpr (LJ == 1) {
                 const float2 v = *reinterpret_cast<const float2*>(pc[(h ^ (h >> 2)) & 3] + 16 * h);
                 x[2 * h] = v.x; x[2 * h + 1] = v.y;
@@ -1005,13 +1024,15 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv0) : "f"(raw0));
 #pragma unroll
           for (int r = 0; r < R; ++r) up[r] = __float_as_uint(x[r] * inv0);
-          if (!active) {  // padding edge: the neutral factor 1 in every entry
+          if (__builtin_expect(!(active && raw0 > 0.0f), 0)) {  // rare: one branch instead of per-entry selects
+            if (!active) {  // padding edge: the neutral factor 1 in every entry
 #pragma unroll
-            for (int r = 0; r < R; ++r) up[r] = 0x3f800000u;
-          } else if (!(raw0 > 0.0f)) {  // DC term <= 0: neutral message + numerical event (reading R10)
+              for (int r = 0; r < R; ++r) up[r] = 0x3f800000u;
+            } else {  // DC term <= 0: neutral message + numerical event (reading R10)
 #pragma unroll
-            for (int r = 0; r < R; ++r) up[r] = zr[r] == 0 ? 0x3f800000u : 0u;
-            if (t == 0) atomicAdd(&ws.slot_events[step ? 0 : slot], 1);
+              for (int r = 0; r < R; ++r) up[r] = zr[r] == 0 ? 0x3f800000u : 0u;
+              if (t == 0) atomicAdd(&ws.slot_events[step ? 0 : slot], 1);
+            }
           }
         } else {
           const float lg0 = lg2a(raw0);
@@ -1393,7 +1414,28 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         if (do_cn) {
           // pi_e^-1 of my z's (linear: XOR of basis images)
           int oidx[R];
-          {
+          // LIN: the byte addresses in my (row-aligned) scatter row directly, st_s ^ 4 pi_e^-1(z) -- the same XOR
+          // chain on pre-shifted images; the read-back uses the same addresses (padding edges take h = 1, the
+          // identity, so they keep the natural order)
+          uint32_t sa[LIN && !PAIRIL ? R : 1];
+          if constexpr (LIN && !PAIRIL) {
+            const uint64_t pv = PT[active ? (rr.var_h & 0xFFu) : 1u];
+            uint32_t base = smem_u32(st);
+            NB_CHECK((base & (Q * 4 - 1)) == 0);
+            if constexpr (TT > 1) {
+#pragma unroll
+              for (int b = 0; b < MB - 4; ++b)
+                if ((t >> b) & 1) base ^= (uint32_t)((pv >> (8 * (LJ + b))) & 0xFFu) << 2;
+            }
+            sa[0] = base;
+#pragma unroll
+            for (int rb = 0; rb < LR; ++rb) {
+              const int zb = (TT > 1) ? (rb < LJ ? rb : 4 + rb - LJ) : rb;
+              const uint32_t img = (uint32_t)((pv >> (8 * zb)) & 0xFFu) << 2;
+#pragma unroll
+              for (int jj = 0; jj < (1 << rb); ++jj) sa[(1 << rb) + jj] = sa[jj] ^ img;
+            }
+          } else {
             const uint64_t pv = PT[rr.var_h & 0xFFu];
             int base = 0;
             if constexpr (TT > 1) {
@@ -1414,6 +1456,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               for (int r = 0; r < R; ++r) oidx[r] = zr[r];
             }
           }
+          (void)oidx;
+          (void)sa;
           // transposition / DB reads of X done (LANEMAJOR: the scatter writes into the whole warp's buffer)
           if constexpr (TT > 1 || LANEMAJOR) __syncwarp();
           if (cvalid) {
@@ -1433,6 +1477,12 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               for (int r = 0; r < R; ++r) {
                 NB_CHECK(oidx[r] >= 0 && oidx[r] < Q && 32 * Q <= GBLK && tid - grp * GT < 32);
                 asm volatile("st.shared.b32 [%0], %1;" ::"r"(xs_s + ((uint32_t)oidx[r] << 7)), "r"(up[r]) : "memory");
+              }
+            } else if constexpr (LIN) {
+#pragma unroll
+              for (int r = 0; r < R; ++r) {
+                NB_CHECK((sa[r] ^ smem_u32(st)) < (uint32_t)Q * 4);
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(sa[r]), "r"(up[r]) : "memory");
               }
             } else {
               const uint32_t st_s = smem_u32(st);
@@ -1486,9 +1536,13 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             constexpr int osh = PAIRIL ? 3 : 2;  // PAIRIL: my entries sit at 2 w + (trow & 1) of the pair
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-              NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
               float xt;
-              asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xt) : "r"(tot_s + ((uint32_t)oidx[r] << osh)) : "memory");
+              if constexpr (LIN && !PAIRIL) {
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xt) : "r"(sa[r]) : "memory");
+              } else {
+                NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xt) : "r"(tot_s + ((uint32_t)oidx[r] << osh)) : "memory");
+              }
               if constexpr (LIN) {
                 out[r] = xt;  // W_e(z) = prod_{j != e} X_j(pi_e^-1 z), written back into my own scatter row
               } else {
