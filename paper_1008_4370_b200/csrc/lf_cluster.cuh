@@ -87,7 +87,12 @@ struct CCfg {
 #define NB_NSTAGE 2
 #endif
   static constexpr int NS = NB_NSTAGE;               // stage buffers per group (chunks in flight + 1)
-  static constexpr int TEAMW = NS * QS + NS * THW;
+  // q >= 128: one more row per team, the work row of the linear F32 path (transposition, decision buffer,
+  // check-node scatter): the staged rows are then only read by the generic proxy, so no proxy fence and no
+  // end-of-chunk barrier is needed before their next bulk fill
+  static constexpr int NW = MB >= 7 ? 1 : 0;
+  static constexpr int RB = NS + NW;                 // row buffers per team
+  static constexpr int TEAMW = RB * QS + NS * THW;
 };
 
 // Message storage ("reader-ordered rows"): row r holds the message CONSUMED by edge slot r, i.e. the
@@ -532,13 +537,13 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   const int TG = GT / TT;                        // teams per group
   const int CPG = GT / TPC;                      // checks per group
   const int GBLK = TG * C::QS;                   // one stage buffer of a group (floats)
-  float* const GST = smem + grp * NS * GBLK;     // the group's stage buffers
+  float* const GST = smem + grp * C::RB * GBLK;  // the group's stage buffers (+ its work rows, q >= 128)
   const int trow = team - grp * TG;              // my team's row within a group stage buffer
   // F16: the group's region holds two stage buffers of half rows (GBLKH floats each) and the float
   // work rows (GBLK floats), the same bytes as two float stage buffers
   const int GBLKH = GBLK / 2;
   float* const WK = F16 ? GST + NS * GBLKH + trow * C::QS : nullptr;  // my work row
-  float* const THB = smem + nteams * NS * C::QS + team * 8;  // + b * nteams * 8 (wide teams only)
+  float* const THB = smem + nteams * C::RB * C::QS + team * 8;  // + b * nteams * 8 (wide teams only)
   float* const TOT = smem + nteams * C::TEAMW + lc * Q;
   uint64_t* const PT = reinterpret_cast<uint64_t*>(smem + nteams * C::TEAMW + CPC * Q);  // [q] pi_h^-1 images
   EdgeRec* const recs = reinterpret_cast<EdgeRec*>(PT + Q);
@@ -618,6 +623,17 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #else
   constexpr bool PAIRIL = false;
 #endif
+  // SPLITDEC (q = 256 hot path, exact syndrome): the tentative decision is split over the variable's two
+  // edge teams instead of being computed whole by one of them.  M_v = raw_a (*) W_a = raw_b (*) W_b
+  // (raw_e = P^0 (*) W_partner(e)), so the is_a team evaluates M_v(0) and M_v(alpha^i),
+  // i = 4..7 (its phase-B register bits: W_e transposed into phase B), the other team M_v(0) and i = 0..3
+  // (its phase-A register bits: raw_e transposed into phase A, W_e straight from its phase-A load) -- every
+  // point is an in-thread FFMA2 dot product, no partner-row reads, and every team does the same ~half
+  // decision (no deciding / idle imbalance at the check barriers).  Each team stores its nibble of the
+  // fast bit rule in con[e]; at the end of the pass x_v = the two nibbles and each CTA forms its checks'
+  // exact syndromes from them.  The paper syndrome (mode 1) keeps the whole decision.
+  constexpr bool SPLITDEC_CT = LIN && TT == 16 && !SYM && !SOFT;
+  const bool split = SPLITDEC_CT && mode == 0;
   const int step = P.step_mode;
   const size_t EQ = (size_t)cd.E * Q;
   const uint32_t flag0 = dsmem_addr(&sh_flag[0], 0), flag1 = dsmem_addr(&sh_flag[1], 0);
@@ -828,7 +844,9 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         const int var = (int)(rr.var_h >> 8);
         // my row: the message consumed by edge e (F32; it doubles as the work row), or (F16) the half
         // stage row sth, read only in phase A, and the float work row
-        float* st = F16 ? WK : GST + buf * GBLK + trow * C::QS;
+        // LIN: the staged row stg is only read (phase A); st is my work row
+        float* const stg = GST + buf * GBLK + trow * C::QS;
+        float* st = F16 ? WK : LIN ? GST + NS * GBLK + trow * C::QS : stg;
         const __half* sth = reinterpret_cast<const __half*>(GST + buf * GBLKH) + trow * C::QS;
 
         // ---- channel terms t_i = tanh(L_i / 2)
@@ -880,7 +898,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #ifdef NB_DIAG_DEC_NOLOAD
           if (false) {
 #else
-          if (is_a && do_dec) {
+          if ((is_a || (split && active)) && do_dec) {
 #endif
             const int prow = rr.partner_a >> 9;  // W_e is stored in the row its reader (the partner edge) consumes
             if constexpr (F16) {
@@ -934,7 +952,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           } else if constexpr (R >= 4) {
 #pragma unroll
             for (int ch = 0; ch < CH; ++ch) {
-              const float4 v = *reinterpret_cast<const float4*>(st + mpos<MB>(t * R + 4 * ch, e));
+              const float4 v = *reinterpret_cast<const float4*>(stg + mpos<MB>(t * R + 4 * ch, e));
               if constexpr (LIN) {
                 x[4 * ch] = v.x; x[4 * ch + 1] = v.y; x[4 * ch + 2] = v.z; x[4 * ch + 3] = v.w;
               } else {
@@ -943,7 +961,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             }
           } else {
 #pragma unroll
-            for (int r = 0; r < R; ++r) x[r] = LIN ? st[r] : to_lin(st[r]);
+            for (int r = 0; r < R; ++r) x[r] = LIN ? stg[r] : to_lin(stg[r]);
           }
           if constexpr (PMF) {
             if constexpr (LR > 0) wht_reg<R, 0>(x);  // z bits 0..LR-1 of WHT(W_e')
@@ -1058,8 +1076,73 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           for (int r = 0; r < R; ++r) dst[zr[r]] = LIN ? lin_to_packed(__uint_as_float(up[r])) : __uint_as_float(up[r]);
         }
 
+        // ---- TENTATIVE DECISION, split over the two edge teams (SPLITDEC above)
+        if constexpr (SPLITDEC_CT) if (do_dec && split) {
+          // my half: Sum_k Pm[k] Tm[k ^ s], s = 0, 1, 2, 4, 8 over my register index k, where (is_a) Pm = raw in
+          // phase B and Tm = W_e moved to phase B, or (!is_a) Pm = W_e in phase A and Tm = raw moved to phase A.
+          // The move: register k of lane t -> row k, position t of my stage row; then lane t reads row t.  Row
+          // layout: 16 rows of 16 words, row r's 16-byte chunks XOR-swizzled by (r >> 1) & 3; the odd team's
+          // rows shifted by one (row 15 wraps to row 0) -- scalar writes and 16-byte row reads conflict-free.
+          __syncwarp();  // transposition reads of my row done
+          const int sh = trow & 1;
+          float dA[16];
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            dA[4 * ch] = wo4[ch].x; dA[4 * ch + 1] = wo4[ch].y; dA[4 * ch + 2] = wo4[ch].z; dA[4 * ch + 3] = wo4[ch].w;
+          }
+          {
+            float* pw[4];
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) pw[c4] = st + 16 * sh + ((((t >> 2) ^ c4) & 3) << 2) + (t & 3);
+            if (active) {
+              if (is_a) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) (k == 15 ? pw[3][sh ? -16 : 240] : pw[(k >> 1) & 3][16 * k]) = dA[k];
+              } else {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) (k == 15 ? pw[3][sh ? -16 : 240] : pw[(k >> 1) & 3][16 * k]) = x[k];
+              }
+            }
+          }
+          __syncwarp();
+          float Tm[16];
+          {
+            const float* rp = st + 16 * ((t + sh) & 15);
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const float4 v4 = *reinterpret_cast<const float4*>(rp + ((((t >> 1) ^ c4) & 3) << 2));
+              Tm[4 * c4] = v4.x; Tm[4 * c4 + 1] = v4.y; Tm[4 * c4 + 2] = v4.z; Tm[4 * c4 + 3] = v4.w;
+            }
+          }
+          float md5[5];
+          auto half_dots = [&](const float (&Pm)[16]) {
+            float2 acc[5];
+#pragma unroll
+            for (int b = 0; b < 5; ++b) acc[b] = make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int p2 = 0; p2 < 8; ++p2) {
+              const int k = 2 * p2;
+              const float2 pp = make_float2(Pm[k], Pm[k + 1]);
+              acc[0] = __ffma2_rn(pp, make_float2(Tm[k], Tm[k + 1]), acc[0]);
+              acc[1] = __ffma2_rn(pp, make_float2(Tm[k + 1], Tm[k]), acc[1]);
+              acc[2] = __ffma2_rn(pp, make_float2(Tm[k ^ 2], Tm[(k ^ 2) + 1]), acc[2]);
+              acc[3] = __ffma2_rn(pp, make_float2(Tm[k ^ 4], Tm[(k ^ 4) + 1]), acc[3]);
+              acc[4] = __ffma2_rn(pp, make_float2(Tm[k ^ 8], Tm[(k ^ 8) + 1]), acc[4]);
+            }
+#pragma unroll
+            for (int b = 0; b < 5; ++b) md5[b] = acc[b].x + acc[b].y;
+          };
+          if (is_a) half_dots(x); else half_dots(dA);
+          int s_off = 0, s_n = 5;
+          const uint32_t sb = team_sign_bits<5, TT>(md5, lane, s_off, s_n);
+          if (active && t == 0) {
+            const uint32_t nib = ((sb >> 1) ^ ((sb & 1u) ? 0xFu : 0u)) & 0xFu;  // bit = sgn M(alpha^i) ^ sgn M(0)
+            con[e] = (uint8_t)(is_a ? nib << 4 : nib);
+          }
+        }
+
         // ---- TENTATIVE DECISION at v's first edge: M_v(z) = sum_y raw(y) W_e(z ^ y)
-        if (do_dec) {
+        if (do_dec && !split) {
           // D = Gamma^-1(W_e) in the row layout word(z) = 16 tB(z) + rB(z), over the consumed Wp
 #ifdef NB_WO_LATE
           load_wo();
@@ -1159,7 +1242,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
                   xs[hp] = inT ? x[hp] : o;
                 }
                 const int trT = (trow & ~1) | T;
-                const float* DT = F16 ? GST + NS * GBLKH + trT * C::QS : GST + buf * GBLK + trT * C::QS;
+                const float* DT = F16 ? GST + NS * GBLKH + trT * C::QS : GST + (LIN ? NS * GBLK : buf * GBLK) + trT * C::QS;
                 const int dxT = T ? 16 : 0;
                 float dh[8], dq[8];
 #pragma unroll
@@ -1464,7 +1547,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             // scatter: X_e(pi_e^-1 z) = U_e(z) = T_e(.); padding teams hold the neutral message
             // 32-bit shared-window addresses: one LEA per entry instead of an IMAD + IADD3 pair
             if constexpr (PAIRIL) {
-              const uint32_t il_s = smem_u32(GST + buf * GBLK + (trow & ~1) * C::QS) + ((uint32_t)(trow & 1) << 2);
+              const uint32_t il_s = smem_u32(GST + NS * GBLK + (trow & ~1) * C::QS) + ((uint32_t)(trow & 1) << 2);
 #pragma unroll
               for (int r = 0; r < R; ++r) {
                 NB_CHECK(oidx[r] >= 0 && oidx[r] < Q);
@@ -1495,7 +1578,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           }
           check_sync(lc, TPC);
           if constexpr (PAIRIL) {
-            float* rows = GST + buf * GBLK + (lc - grp * CPG) * KT * C::QS;
+            float* rows = GST + NS * GBLK + (lc - grp * CPG) * KT * C::QS;
             const int flip = SPLIT == 1 ? ((lane >> 4) & 1) : (pck & 1);
             switch (JPT) {
               case 2: tot_prod_il<R, 2, TT, C::QS>(rows, wgrp, jbase, flip, SPLIT, cvalid); break;
@@ -1505,11 +1588,11 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             }
           } else if constexpr (LIN) {
             switch (JPT) {
-              case 1: tot_prod<R, 1, TT, C::QS>(smem, gbase + buf * GBLK, SPLIT, cvalid); break;
-              case 2: tot_prod<R, (R >= 2 ? 2 : 1), TT, C::QS>(smem, gbase + buf * GBLK, SPLIT, cvalid); break;
-              case 4: tot_prod<R, (R >= 4 ? 4 : 1), TT, C::QS>(smem, gbase + buf * GBLK, SPLIT, cvalid); break;
-              case 8: tot_prod<R, (R >= 8 ? 8 : 1), TT, C::QS>(smem, gbase + buf * GBLK, SPLIT, cvalid); break;
-              default: tot_prod<R, R, TT, C::QS>(smem, gbase + buf * GBLK, SPLIT, cvalid); break;
+              case 1: tot_prod<R, 1, TT, C::QS>(smem, gbase + NS * GBLK, SPLIT, cvalid); break;
+              case 2: tot_prod<R, (R >= 2 ? 2 : 1), TT, C::QS>(smem, gbase + NS * GBLK, SPLIT, cvalid); break;
+              case 4: tot_prod<R, (R >= 4 ? 4 : 1), TT, C::QS>(smem, gbase + NS * GBLK, SPLIT, cvalid); break;
+              case 8: tot_prod<R, (R >= 8 ? 8 : 1), TT, C::QS>(smem, gbase + NS * GBLK, SPLIT, cvalid); break;
+              default: tot_prod<R, R, TT, C::QS>(smem, gbase + NS * GBLK, SPLIT, cvalid); break;
             }
           } else if constexpr (LANEMAJOR) {
             const float* xs = F16 ? GST + NS * GBLKH : GST + buf * GBLK;
@@ -1531,7 +1614,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           check_sync(lc, TPC);
           if (active) {
             float out[R];
-            const uint32_t tot_s = PAIRIL ? smem_u32(GST + buf * GBLK + (trow & ~1) * C::QS) + ((uint32_t)(trow & 1) << 2)
+            const uint32_t tot_s = PAIRIL ? smem_u32(GST + NS * GBLK + (trow & ~1) * C::QS) + ((uint32_t)(trow & 1) << 2)
                                           : smem_u32(LIN ? st : TOT);
             constexpr int osh = PAIRIL ? 3 : 2;  // PAIRIL: my entries sit at 2 w + (trow & 1) of the pair
 #pragma unroll
@@ -1550,6 +1633,10 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
                 out[r] = __uint_as_float((__float_as_uint(mg) & ~kSign) | ((__float_as_uint(xt) ^ up[r]) & kSign));
               }
             }
+            // my last generic access to this chunk's stage buffer: order it before the buffer's next bulk fill
+            // here, so that the fence does not wait for the global stores below (LIN: the generic writes go to the
+            // work rows, the staged rows are only read -- no fence)
+            if constexpr (!LIN) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             const int prow = rr.partner_a >> 9;  // stored where the partner edge will read it
             NB_CHECK(prow >= 0 && prow < cd.E);
             float* dst = Wout + (size_t)prow * Q;
@@ -1606,20 +1693,65 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             }
           }
         }
-        // generic-proxy writes to this stage buffer (DB) are ordered before its next bulk fill
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        group_sync();  // the group's buffers of this chunk are free
+        // generic-proxy writes to this stage buffer (DB) are ordered before its next bulk fill (active teams of a
+        // check-node pass fenced before their global stores)
+        // LIN: no generic writes to the staged rows; the buffer refilled at the next chunk's start was last read
+        // before this chunk's first check barrier, and a work row is rewritten only by its own team after the
+        // other threads' check-node accesses to it (second check barrier) -- no end-of-chunk barrier either
+        if constexpr (!LIN) {
+          if (!(do_cn && active)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          group_sync();  // the group's buffers of this chunk are free
+        }
         buf = buf + 1 == NS ? 0 : buf + 1;
       }
       cp_async_wait<0>();
-      if (step) break;
+      // SPLITDEC: x_v = the nibbles of v's two edges (con); the CTA whose check holds v's is_a edge writes x_v,
+      // and (decode) each CTA XORs h_e x_v(e) over its checks' edges (exact syndrome) -- one
+      // thread per edge slot, the check's KT slots reduced by shuffles (KT divides 32)
+      auto split_pass_end = [&](bool want_syn) -> int {
+        int badc = 0;
+        const int tot_e = nch * CPC * KT;
+        for (int i0 = 0; i0 < tot_e; i0 += nthr) {
+          const int i = i0 + tid;
+          uint32_t contrib = 0;
+          if (i < tot_e) {
+            const int kc = i / (CPC * KT), rem = i - kc * (CPC * KT);
+            const int l = rem / KT, jj = rem - l * KT;
+            const int c = ((int)rank + kc * (int)csz) * CPC + l;
+            const EdgeRec er = recs[i];
+            if (c < cd.M && er.partner_a >= 0) {
+              const int ee = c * KPAD + jj;
+              const uint32_t xv = (uint32_t)__ldcg(con + ee) | (uint32_t)__ldcg(con + (er.partner_a >> 9));
+              if (er.partner_a & 1) xout[er.var_h >> 8] = (uint8_t)xv;
+              if (xv != 0) contrib = GE[GL[er.var_h & 0xFFu] + GL[xv]];
+            }
+          }
+          if (want_syn) {
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1)
+              if (o < KT) contrib ^= __shfl_xor_sync(0xffffffffu, contrib, o);
+            badc |= (int)contrib;
+          }
+        }
+        return badc;
+      };
+      if (step) {
+        if (SPLITDEC_CT && split && do_dec) {
+          cluster_sync_all();  // every nibble of the frame is written
+          (void)split_pass_end(false);
+        }
+        break;
+      }
 
       // ---- end of the pass: stopping rule, cluster-uniform
       asm volatile("fence.proxy.async.global;" ::: "memory");  // W_out is read next by bulk copies
       cluster_sync_all();  // every message, estimate and syndrome byte of the pass is written
       if (tid == 0) sh_bad = 0;
       __syncthreads();
-      if (ell >= 1) {
+      if (SPLITDEC_CT && split && ell >= 1) {
+        const int bad = split_pass_end(true);
+        if (__syncthreads_or(bad != 0) && tid == 0) dsmem_or((ell & 1) ? flag1 : flag0, 1);
+      } else if (ell >= 1) {
         // my checks' syndromes s_c = XOR of the contribution bytes on their kpad edge slots
         int bad = 0;
         const int kp = KPAD;

@@ -832,10 +832,38 @@ void orient_decision_owners(std::vector<EdgeDev>& edges, int E) {
   for (int w = 0; w < nw; ++w) walk(w);  // then the cycles
 }
 
+// q = 256 (tt = 16, two edge slots 2w, 2w + 1 per warp): the cluster kernel splits each variable's decision
+// over its two edges (SPLITDEC in lf_cluster.cuh), with different code for the is_a half and the other half,
+// so a warp whose two slots are of the same kind runs one of them.  Walking the warp graph (degree <= 2)
+// and alternating the kinds along it makes every warp uniform except one per odd cycle.
+void orient_uniform_kinds(std::vector<EdgeDev>& edges, int E) {
+  std::vector<char> done(E, 0);
+  auto walk = [&](int s, int kind) {
+    while (s < E && edges[s].var >= 0 && !done[s]) {
+      const int p = edges[s].partner;
+      edges[s].is_a = (uint8_t)kind;
+      edges[p].is_a = (uint8_t)(1 - kind);
+      done[s] = done[p] = 1;
+      s = p ^ 1;         // the other slot of the partner's warp takes the partner's kind
+      kind = 1 - kind;
+    }
+  };
+  for (int w = 0; 2 * w < E; ++w) {  // path ends first: warps with one used slot
+    const bool u0 = edges[2 * w].var >= 0, u1 = 2 * w + 1 < E && edges[2 * w + 1].var >= 0;
+    if (u0 != u1) walk(u0 ? 2 * w : 2 * w + 1, 1);
+  }
+  for (int s = 0; s < E; ++s) walk(s, 1);  // then the cycles
+}
+
 void assign_decision_owners(std::vector<EdgeDev>& edges, int E, int tt, int kpad) {
 #ifdef NB_WARPDEC
   if (tt == 16) {  // goes with the kernel's WARPDEC (off by default, see lf_cluster.cuh)
     orient_decision_owners(edges, E);
+    return;
+  }
+#else
+  if (tt == 16) {
+    orient_uniform_kinds(edges, E);
     return;
   }
 #endif
