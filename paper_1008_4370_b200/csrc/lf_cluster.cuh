@@ -554,6 +554,10 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   // (ncu, C5 pmf: 33% of the stall samples waited on that load)
   constexpr bool PSTAGE = PMF && TT == 1 && Q >= 4;
   float* const PB = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(GL) + 3 * Q + 15) & ~(uintptr_t)15);
+  // SPLITDEC (q = 256): each team's own message W_e bulk-copied one chunk ahead ([NS][nteams] rows of q + 16
+  // words after the GF tables, on the stage mbarrier) instead of a register load at the chunk's start (ncu: the
+  // decision waited on that load) -- the region of PB, which only one-thread teams use
+  float* const WE = PB;
 
   // TOT(w) gather offsets: thread pck owns WPT w's x JPT teams of its check (R terms, natural X)
   const int SPLIT = KT > R ? KT / R : 1;
@@ -790,7 +794,13 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         }
 #endif
         tx += blk;
+        // SPLITDEC: my edge's own message W_e (row prow, contiguous) into my WE row, on the same mbarrier
+        const bool wecp = SPLITDEC_CT && split && ell >= 1 && act;
+        if (wecp) tx += Q * 4;
         mbar_arrive_tx(&gmbar[b], tx);
+        if constexpr (SPLITDEC_CT) {
+          if (wecp) bulk_g2s(WE + ((size_t)b * nteams + team) * (Q + 16), Win + (size_t)(rr.partner_a >> 9) * Q, Q * 4, &gmbar[b]);
+        }
         // the block in pieces of <= NB_BLK_PIECE bytes (several TMA transfers in flight)
 #ifndef NB_BLK_PIECE
 #define NB_BLK_PIECE 16384
@@ -898,7 +908,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #ifdef NB_DIAG_DEC_NOLOAD
           if (false) {
 #else
-          if ((is_a || (split && active)) && do_dec) {
+          if (is_a && do_dec && !split) {
 #endif
             const int prow = rr.partner_a >> 9;  // W_e is stored in the row its reader (the partner edge) consumes
             if constexpr (F16) {
@@ -1085,32 +1095,40 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           // rows shifted by one (row 15 wraps to row 0) -- scalar writes and 16-byte row reads conflict-free.
           __syncwarp();  // transposition reads of my row done
           const int sh = trow & 1;
-          float dA[16];
+          // my staged W_e row (WE rows are q + 16 words apart, so the two teams of a warp sit in opposite bank
+          // halves): entry z at mpos(z), for q = 256 = tpos(z) (no row key)
+          const float* wrow = WE + ((size_t)buf * nteams + team) * (Q + 16);
+          float Tm[16], dA[16];
+          if (is_a) {
+            // Tm = W_e in phase B: z = t | h << 4 at 16 h + 4 (((t >> 2) ^ h ^ (h >> 2)) & 3) + (t & 3): four row
+            // pointers, then [pointer + 64 h bytes] (block 15 wraps to block 0 for the odd team)
+            const float* pk[4];
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            dA[4 * ch] = wo4[ch].x; dA[4 * ch + 1] = wo4[ch].y; dA[4 * ch + 2] = wo4[ch].z; dA[4 * ch + 3] = wo4[ch].w;
-          }
-          {
+            for (int c4 = 0; c4 < 4; ++c4) pk[c4] = wrow + ((((t >> 2) ^ c4) & 3) << 2) + (t & 3);
+#pragma unroll
+            for (int h = 0; h < 16; ++h) Tm[h] = pk[(h ^ (h >> 2)) & 3][16 * h];
+          } else {
+            // dA = W_e in phase A: z = 16 t + 4 ch + (0..3), one 16-byte chunk each
+            const float* rp = wrow + 16 * t;
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+              const float4 v4 = *reinterpret_cast<const float4*>(rp + (((ch ^ t ^ (t >> 2)) & 3) << 2));
+              dA[4 * ch] = v4.x; dA[4 * ch + 1] = v4.y; dA[4 * ch + 2] = v4.z; dA[4 * ch + 3] = v4.w;
+            }
+            // Tm = raw in phase A: register k of lane t -> row k, position t of my work row (row r's 16-byte chunks
+            // XOR-swizzled by (r >> 1) & 3, the odd team's rows shifted by one); then lane t reads its row t
             float* pw[4];
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4) pw[c4] = st + 16 * sh + ((((t >> 2) ^ c4) & 3) << 2) + (t & 3);
             if (active) {
-              if (is_a) {
 #pragma unroll
-                for (int k = 0; k < 16; ++k) (k == 15 ? pw[3][sh ? -16 : 240] : pw[(k >> 1) & 3][16 * k]) = dA[k];
-              } else {
-#pragma unroll
-                for (int k = 0; k < 16; ++k) (k == 15 ? pw[3][sh ? -16 : 240] : pw[(k >> 1) & 3][16 * k]) = x[k];
-              }
+              for (int k = 0; k < 16; ++k) (k == 15 ? pw[3][sh ? -16 : 240] : pw[(k >> 1) & 3][16 * k]) = x[k];
             }
-          }
-          __syncwarp();
-          float Tm[16];
-          {
-            const float* rp = st + 16 * ((t + sh) & 15);
+            __syncwarp(__activemask());
+            const float* rq = st + 16 * ((t + sh) & 15);
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4) {
-              const float4 v4 = *reinterpret_cast<const float4*>(rp + ((((t >> 1) ^ c4) & 3) << 2));
+              const float4 v4 = *reinterpret_cast<const float4*>(rq + ((((t >> 1) ^ c4) & 3) << 2));
               Tm[4 * c4] = v4.x; Tm[4 * c4 + 1] = v4.y; Tm[4 * c4 + 2] = v4.z; Tm[4 * c4 + 3] = v4.w;
             }
           }
