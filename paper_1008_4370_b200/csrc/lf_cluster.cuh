@@ -59,8 +59,7 @@ struct EdgeRec {
   uint32_t var_h;     // variable << 8 | h_cv
 };
 
-// bytes added to the cluster kernels' dynamic shared memory so that the kernel can align its base to a
-// message row (q floats, q <= 256)
+// alignment of the cluster kernels' dynamic shared memory: one message row (q floats, q <= 256)
 constexpr uint32_t kSmemAlignPad = 1024;
 
 template <int MB>
@@ -168,6 +167,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(mb))
+               : "memory");
+}
+
+// the same on shared-window addresses computed once (no generic-to-shared conversion in the loop)
+__device__ __forceinline__ void mbar_arrive_tx_s(uint32_t mb, uint32_t tx) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(mb), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(uint32_t mb, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(mb),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mb) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mb)
                : "memory");
 }
 
@@ -485,17 +500,15 @@ template <int MB, int NTHR, bool PMF = false, bool F16 = false, int KP = 0, bool
 __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_cluster_kernel(ClusterParams P) {
   using C = CCfg<MB>;
   constexpr int Q = C::Q, R = C::R, TT = C::TT, LR = C::LR, LJ = C::LJ, CH = C::CH;
-  extern __shared__ __align__(16) float smem_raw[];
-  // LIN (q >= 128): the dynamic region starts on a q-float boundary of the shared window (the host adds
-  // kSmemAlignPad bytes), so that a team row's shared address ORs with an entry's byte offset -- the check
-  // node's scatter / read-back addresses are then the XOR chain itself (no per-entry address arithmetic)
-  float* const smem = MB >= 7 ? reinterpret_cast<float*>(reinterpret_cast<char*>(smem_raw) +
-                                                         ((kSmemAlignPad - (smem_u32(smem_raw) & (kSmemAlignPad - 1))) &
-                                                          (kSmemAlignPad - 1)))
-                              : smem_raw;
+  extern __shared__ __align__(1024) float smem_raw[];
+  // LIN (q >= 128): the dynamic region starts on a 1 KB (message-row) boundary of the shared window (the
+  // declared alignment; checked once below), so that a team row's shared address ORs with an entry's byte
+  // offset -- the check node's scatter / read-back addresses are then the XOR chain itself
+  float* const smem = smem_raw;
   __shared__ int sh_frame, sh_flag[2], sh_bad;
   __shared__ __align__(8) uint64_t sh_mbar[8 * C::NS];  // [group][buffer]: the group's teams arrive, bulk copies complete_tx
 
+  if (MB >= 7 && (smem_u32(smem_raw) & (kSmemAlignPad - 1)) != 0) __trap();  // the row alignment LIN relies on
   const CodeDev& cd = P.code;
   const WorkDev& ws = P.ws;
   const int tid = threadIdx.x;
@@ -557,7 +570,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   // SPLITDEC (q = 256): each team's own message W_e bulk-copied one chunk ahead ([NS][nteams] rows of q + 16
   // words after the GF tables, on the stage mbarrier) instead of a register load at the chunk's start (ncu: the
   // decision waited on that load) -- the region of PB, which only one-thread teams use
-  float* const WE = PB;
+  // (offset arithmetic on smem, not an integer round trip, so that the compiler keeps shared-space accesses)
+  float* const WE = smem + ((((reinterpret_cast<const char*>(GL) - reinterpret_cast<const char*>(smem)) + 3 * Q + 15) & ~15) >> 2);
 
   // TOT(w) gather offsets: thread pck owns WPT w's x JPT teams of its check (R terms, natural X)
   const int SPLIT = KT > R ? KT / R : 1;
@@ -926,7 +940,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           }
         };
 #ifndef NB_WO_LATE
-        load_wo();
+        if (!split) load_wo();  // (SPLITDEC: W_e comes staged)
 #endif
 
         // ---- VARIABLE TO CHECK: x (phase B) = P^0 (*) Gamma^-1(W_e'); at l = 0, x = P^0

@@ -1157,7 +1157,6 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
       const size_t recs = (size_t)((c->p_groups + csz - 1) / csz) * c->p_cpc * kt;
       return ((size_t)(c->p_block / tt) * persist_team_words(m) + (size_t)c->p_cpc * q) * sizeof(float) +
              (size_t)q * sizeof(uint64_t) + recs * sizeof(nb::EdgeRec) + align_up(3 * (size_t)q, 16) +
-             (m >= 7 ? nb::kSmemAlignPad : 0) +  // the kernel aligns its base to a message row (LIN)
              // q = 256 (tt = 16): the split decision's staged W_e rows (WE in lf_cluster.cuh), [NS][teams][q]
              (tt == 16 ? 16 + (size_t)nb::CCfg<8>::NS * (size_t)(c->p_block / tt) * (q + 16) * sizeof(float) : 0);
     };
