@@ -102,7 +102,15 @@ struct CCfg {
 template <int MB>
 __host__ __device__ __forceinline__ int mpos(int z, int row) {
   constexpr int Q = 1 << MB;
-  if constexpr (MB >= 5) {
+  if constexpr (MB == 8) {
+    // q = 256: 16-byte chunk c (= (z >> 2) & 3) of block b (= z >> 4) at chunk 16 c + (b ^ c).  A thread holding a
+    // block (phase A) writes or reads it as four 16-byte chunks, and the 16 blocks' chunk c are one contiguous
+    // 256-byte run (coalesced stores, conflict-free 16-byte shared loads); a phase-B lane (z = t | h << 4) reads
+    // word 64 c + 4 (h ^ c) + (t & 3): its team's 16 lanes hit 16 distinct banks
+    const int b = z >> 4, c = (z >> 2) & 3;
+    (void)row;
+    return (c << 6) | ((b ^ c) << 2) | (z & 3);
+  } else if constexpr (MB >= 5) {
     constexpr int TT = Q / 16;
     const int b = z >> 4, c = (z >> 2) & 3;
     const int f = TT <= 4 ? (row & (8 / TT - 1)) : 0;
@@ -1110,23 +1118,22 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           __syncwarp();  // transposition reads of my row done
           const int sh = trow & 1;
           // my staged W_e row (WE rows are q + 16 words apart, so the two teams of a warp sit in opposite bank
-          // halves): entry z at mpos(z), for q = 256 = tpos(z) (no row key)
+          // halves): entry z at mpos(z) = 64 c + 4 (b ^ c) + (z & 3), c = (z >> 2) & 3, b = z >> 4
           const float* wrow = WE + ((size_t)buf * nteams + team) * (Q + 16);
           float Tm[16], dA[16];
           if (is_a) {
-            // Tm = W_e in phase B: z = t | h << 4 at 16 h + 4 (((t >> 2) ^ h ^ (h >> 2)) & 3) + (t & 3): four row
-            // pointers, then [pointer + 64 h bytes] (block 15 wraps to block 0 for the odd team)
+            // Tm = W_e in phase B: z = t | h << 4 at 64 c + 16 (h >> 2) + 4 ((h & 3) ^ c) + (t & 3), c = t >> 2: four
+            // pointers (by h & 3), then [pointer + 64 (h >> 2) bytes]
             const float* pk[4];
 #pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) pk[c4] = wrow + ((((t >> 2) ^ c4) & 3) << 2) + (t & 3);
+            for (int hl = 0; hl < 4; ++hl) pk[hl] = wrow + 64 * (t >> 2) + 4 * (hl ^ (t >> 2)) + (t & 3);
 #pragma unroll
-            for (int h = 0; h < 16; ++h) Tm[h] = pk[(h ^ (h >> 2)) & 3][16 * h];
+            for (int h = 0; h < 16; ++h) Tm[h] = pk[h & 3][16 * (h >> 2)];
           } else {
             // dA = W_e in phase A: z = 16 t + 4 ch + (0..3), one 16-byte chunk each
-            const float* rp = wrow + 16 * t;
 #pragma unroll
             for (int ch = 0; ch < 4; ++ch) {
-              const float4 v4 = *reinterpret_cast<const float4*>(rp + (((ch ^ t ^ (t >> 2)) & 3) << 2));
+              const float4 v4 = *reinterpret_cast<const float4*>(wrow + 64 * ch + 4 * (t ^ ch));
               dA[4 * ch] = v4.x; dA[4 * ch + 1] = v4.y; dA[4 * ch + 2] = v4.z; dA[4 * ch + 3] = v4.w;
             }
             // Tm = raw in phase A: register k of lane t -> row k, position t of my work row (row r's 16-byte chunks
@@ -1644,7 +1651,35 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             default: tot_sum<R, R, TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid, tix); break;
           }
           check_sync(lc, TPC);
-          if (active) {
+          // q = 256 (LIN): read W_e back in the phase-A coordinates z = 16 t + r (my own XOR chain of pi_e^-1 images,
+          // base from the high nibble t), so that each thread holds 16 consecutive entries: four 16-byte global
+          // stores instead of sixteen words, and the scatter addresses are dead after the scatter
+          constexpr bool RBA = LIN && TT == 16 && !PAIRIL;
+          if (RBA && active) {
+            const uint64_t pv = PT[rr.var_h & 0xFFu];
+            uint32_t ra[16];
+            uint32_t base = smem_u32(st);
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              if ((t >> b) & 1) base ^= (uint32_t)((pv >> (8 * (4 + b))) & 0xFFu) << 2;
+            ra[0] = base;
+#pragma unroll
+            for (int rb = 0; rb < 4; ++rb) {
+              const uint32_t img = (uint32_t)((pv >> (8 * rb)) & 0xFFu) << 2;
+#pragma unroll
+              for (int jj = 0; jj < (1 << rb); ++jj) ra[(1 << rb) + jj] = ra[jj] ^ img;
+            }
+            float out[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(out[r]) : "r"(ra[r]) : "memory");
+            const int prow = rr.partner_a >> 9;
+            NB_CHECK(prow >= 0 && prow < cd.E);
+            float* dst = Wout + (size_t)prow * Q;
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4)
+              *reinterpret_cast<float4*>(dst + mpos<MB>(16 * t + 4 * c4, prow)) =
+                  make_float4(out[4 * c4], out[4 * c4 + 1], out[4 * c4 + 2], out[4 * c4 + 3]);
+          } else if (active) {
             float out[R];
             const uint32_t tot_s = PAIRIL ? smem_u32(GST + NS * GBLK + (trow & ~1) * C::QS) + ((uint32_t)(trow & 1) << 2)
                                           : smem_u32(LIN ? st : TOT);
