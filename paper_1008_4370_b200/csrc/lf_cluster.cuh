@@ -361,6 +361,34 @@ __device__ __forceinline__ void tot_prod(float* smem, int gbase, int split, bool
     float v[JPT], ex[JPT];
 #pragma unroll
     for (int jj = 0; jj < JPT; ++jj) v[jj] = g[jj * TEAM + i * TT * JPT];
+    if constexpr (JPT >= 4) {
+      if (split == 1) {
+        // packed (FMUL2) form: the two halves' prefix products side by side, then their suffix products started
+        // from the other half's total, so (ex[k], ex[k + H]) = (prefix_A, prefix_B) * (suffix_A * total_B,
+        // suffix_B * total_A): 3 H FMUL2 instead of 3 JPT FMUL, the same products reassociated
+        constexpr int H = JPT / 2;
+        float2 pp[H];
+        float2 c = make_float2(1.0f, 1.0f);
+#pragma unroll
+        for (int k = 0; k < H; ++k) {
+          pp[k] = c;
+          c = __fmul2_rn(c, make_float2(v[k], v[k + H]));
+        }
+        float2 sc = make_float2(c.y, c.x);  // (total_B, total_A)
+#pragma unroll
+        for (int k = H - 1; k >= 0; --k) {
+          const float2 e2 = __fmul2_rn(pp[k], sc);
+          ex[k] = e2.x;
+          ex[k + H] = e2.y;
+          sc = __fmul2_rn(sc, make_float2(v[k], v[k + H]));
+        }
+        if (cvalid) {
+#pragma unroll
+          for (int jj = 0; jj < JPT; ++jj) g[jj * TEAM + i * TT * JPT] = ex[jj];
+        }
+        continue;
+      }
+    }
     float pre = 1.0f;
 #pragma unroll
     for (int jj = 0; jj < JPT; ++jj) {
@@ -1072,8 +1100,16 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           // U = raw / raw(0): entry 0 is 1; |U| <= 1 up to rounding
           float inv0;
           asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv0) : "f"(raw0));
+          if constexpr (R >= 2) {
 #pragma unroll
-          for (int r = 0; r < R; ++r) up[r] = __float_as_uint(x[r] * inv0);
+            for (int r = 0; r < R; r += 2) {  // FMUL2 with a broadcast factor
+              const float2 u2 = __fmul2_rn(make_float2(x[r], x[r + 1]), make_float2(inv0, inv0));
+              up[r] = __float_as_uint(u2.x);
+              up[r + 1] = __float_as_uint(u2.y);
+            }
+          } else {
+            up[0] = __float_as_uint(x[0] * inv0);
+          }
           if (__builtin_expect(!(active && raw0 > 0.0f), 0)) {  // rare: one branch instead of per-entry selects
             if (!active) {  // padding edge: the neutral factor 1 in every entry
 #pragma unroll
