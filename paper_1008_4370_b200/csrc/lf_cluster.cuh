@@ -543,6 +543,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   float* const smem = smem_raw;
   __shared__ int sh_frame, sh_flag[2], sh_bad;
   __shared__ __align__(8) uint64_t sh_mbar[8 * C::NS];  // [group][buffer]: the group's teams arrive, bulk copies complete_tx
+  __shared__ __align__(8) uint64_t sh_cbar[8];  // SPLITDEC: [group] "every warp of the check has scattered" (one arrival per warp)
 
   if (MB >= 7 && (smem_u32(smem_raw) & (kSmemAlignPad - 1)) != 0) __trap();  // the row alignment LIN relies on
   const CodeDev& cd = P.code;
@@ -647,12 +648,14 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
     sh_flag[1] = 0;
     for (int gg = 0; gg < ngrp; ++gg) {
       for (int b = 0; b < NS; ++b) mbar_init(&sh_mbar[NS * gg + b], (uint32_t)(GT / TT));
+      mbar_init(&sh_cbar[gg], (uint32_t)(GT / 32));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   cluster_sync_all();
-  uint32_t mb_parity = 0;  // bit b: parity of the next completion of stage buffer b  // every CTA of the cluster has started before any DSMEM access
+  uint32_t mb_parity = 0;
+  uint32_t cb_parity = 0;  // SPLITDEC: parity of the next completion of my group's sh_cbar  // bit b: parity of the next completion of stage buffer b  // every CTA of the cluster has started before any DSMEM access
 
   const CallDev* call = ws.call;
   const int max_iters = call->max_iters;
@@ -1145,6 +1148,17 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         }
 
         // ---- TENTATIVE DECISION, split over the two edge teams (SPLITDEC above)
+        float md5[5];
+        // the sign bits over the team (a chain of shuffles) and my nibble: run after the check-node scatter, between
+        // this warp's arrival on the group's scatter barrier and its wait, when the check node follows
+        auto split_finish = [&]() {
+          int s_off = 0, s_n = 5;
+          const uint32_t sb = team_sign_bits<5, TT>(md5, lane, s_off, s_n);
+          if (active && t == 0) {
+            const uint32_t nib = ((sb >> 1) ^ ((sb & 1u) ? 0xFu : 0u)) & 0xFu;  // bit = sgn M(alpha^i) ^ sgn M(0)
+            con[e] = (uint8_t)(is_a ? nib << 4 : nib);
+          }
+        };
         if constexpr (SPLITDEC_CT) if (do_dec && split) {
           // my half: Sum_k Pm[k] Tm[k ^ s], s = 0, 1, 2, 4, 8 over my register index k, where (is_a) Pm = raw in
           // phase B and Tm = W_e moved to phase B, or (!is_a) Pm = W_e in phase A and Tm = raw moved to phase A.
@@ -1189,7 +1203,6 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               Tm[4 * c4] = v4.x; Tm[4 * c4 + 1] = v4.y; Tm[4 * c4 + 2] = v4.z; Tm[4 * c4 + 3] = v4.w;
             }
           }
-          float md5[5];
           auto half_dots = [&](const float (&Pm)[16]) {
             float2 acc[5];
 #pragma unroll
@@ -1208,12 +1221,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             for (int b = 0; b < 5; ++b) md5[b] = acc[b].x + acc[b].y;
           };
           if (is_a) half_dots(x); else half_dots(dA);
-          int s_off = 0, s_n = 5;
-          const uint32_t sb = team_sign_bits<5, TT>(md5, lane, s_off, s_n);
-          if (active && t == 0) {
-            const uint32_t nib = ((sb >> 1) ^ ((sb & 1u) ? 0xFu : 0u)) & 0xFu;  // bit = sgn M(alpha^i) ^ sgn M(0)
-            con[e] = (uint8_t)(is_a ? nib << 4 : nib);
-          }
+          if (!do_cn) split_finish();
         }
 
         // ---- TENTATIVE DECISION at v's first edge: M_v(z) = sum_y raw(y) W_e(z ^ y)
@@ -1651,7 +1659,19 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               }
             }
           }
-          check_sync(lc, TPC);
+          if (SPLITDEC_CT && split && do_dec) {
+            // arrive on the group's scatter barrier (one arrival per warp, after the warp's scatter: __syncwarp orders
+            // the lanes' stores before lane 0's release), finish the decision, then wait for the other warps
+            __syncwarp();
+            if (lane == 0)
+              asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n}" ::"r"(smem_u32(&sh_cbar[grp]))
+                           : "memory");
+            split_finish();
+            mbar_wait(&sh_cbar[grp], cb_parity);
+            cb_parity ^= 1u;
+          } else {
+            check_sync(lc, TPC);
+          }
           if constexpr (PAIRIL) {
             float* rows = GST + NS * GBLK + (lc - grp * CPG) * KT * C::QS;
             const int flip = SPLIT == 1 ? ((lane >> 4) & 1) : (pck & 1);
