@@ -238,6 +238,37 @@ __device__ __forceinline__ uint32_t team_sign_bits(float (&v)[NV], int lane, int
   return __reduce_or_sync(tmask, bits);
 }
 
+// The five totals of the split decision (q = 256: two 16-lane teams per warp) by recursive halving as in
+// team_sign_bits; the totals of values 0..4 end in team lanes 0, 2, 4, 8 and 10, whose sign bits are collected by
+// one warp-wide ballot (no per-team REDUX, which the two teams' masks serialise)
+__device__ __forceinline__ uint32_t split_sign_bits(float (&v)[5], int lane) {
+  int off = 0, nfin = 0;
+  constexpr int NV = 5, TT = 16;
+  int n = NV, nv = NV;
+#pragma unroll
+  for (int o = TT / 2; o >= 1; o >>= 1) {
+    const int h = (n + 1) / 2;
+    const bool upper = (lane & o) != 0;
+    nv = upper ? (nv > h ? nv - h : 0) : (nv < h ? nv : h);
+#pragma unroll
+    for (int k = 0; k < (NV + 1) / 2; ++k) {
+      if (k < h) {
+        const float lo = v[k];
+        const float hi = (h + k < n) ? v[h + k] : 0.0f;
+        const float send = upper ? lo : hi;
+        const float keep = upper ? hi : lo;
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    if (upper) off += h;
+    n = h;
+  }
+  nfin = nv;
+  (void)off;
+  const uint32_t bal = __ballot_sync(0xffffffffu, nfin > 0 && v[0] < 0.0f) >> (lane & 16);
+  return (bal & 1u) | ((bal >> 1) & 2u) | ((bal >> 2) & 4u) | ((bal >> 5) & 8u) | ((bal >> 6) & 16u);
+}
+
 template <int CH>
 __device__ __forceinline__ int cswz(int c, int key) { return c ^ (key & (CH - 1)); }
 
@@ -1032,7 +1063,9 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             if constexpr (LR > 2) wht_reg<R, 2>(x);
             if constexpr (LR > 3) wht_reg<R, 3>(x);
           } else {
+#ifndef NB_ABL_NOVN
             bfly_regs<R, 0, LR>(x, th);  // z bits 0..LR-1
+#endif
           }
           if constexpr (TT > 1) {
             // transposition through the consumed stage buffer, chunk-swizzled layout tpos(z); at q = 64 two
@@ -1081,7 +1114,13 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               if constexpr (LJ <= 2) wht_reg<R, 2>(x);
               if constexpr (LJ <= 3) wht_reg<R, 3>(x);
             } else {
+#ifdef NB_ABL_NOVN
+              if constexpr (false)
+#endif
               if constexpr (LJ <= 0) bfly_reg<R, 0>(x, th[4 - LJ]);
+#ifdef NB_ABL_NOVN
+              if constexpr (false)
+#endif
               if constexpr (LJ <= 1) bfly_reg<R, 1>(x, th[(5 - LJ) < MB ? 5 - LJ : 0]);
               if constexpr (LJ <= 2) bfly_reg<R, 2>(x, th[(6 - LJ) < MB ? 6 - LJ : 0]);
               if constexpr (LJ <= 3) bfly_reg<R, 3>(x, th[(7 - LJ) < MB ? 7 - LJ : 0]);
@@ -1153,13 +1192,25 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         // this warp's arrival on the group's scatter barrier and its wait, when the check node follows
         auto split_finish = [&]() {
           int s_off = 0, s_n = 5;
-          const uint32_t sb = team_sign_bits<5, TT>(md5, lane, s_off, s_n);
+#ifdef NB_ABL_NORED
+          uint32_t sb = 0;
+          for (int b = 0; b < 5; ++b) sb |= (md5[b] < 0.0f ? 1u : 0u) << b;
+          (void)s_off; (void)s_n;
+#else
+          const uint32_t sb = split_sign_bits(md5, lane);
+          (void)s_off; (void)s_n;
+#endif
           if (active && t == 0) {
             const uint32_t nib = ((sb >> 1) ^ ((sb & 1u) ? 0xFu : 0u)) & 0xFu;  // bit = sgn M(alpha^i) ^ sgn M(0)
             con[e] = (uint8_t)(is_a ? nib << 4 : nib);
           }
         };
-        if constexpr (SPLITDEC_CT) if (do_dec && split) {
+#ifdef NB_ABL_NODEC
+        if constexpr (false)
+#else
+        if constexpr (SPLITDEC_CT)
+#endif
+        if (do_dec && split) {
           // my half: Sum_k Pm[k] Tm[k ^ s], s = 0, 1, 2, 4, 8 over my register index k, where (is_a) Pm = raw in
           // phase B and Tm = W_e moved to phase B, or (!is_a) Pm = W_e in phase A and Tm = raw moved to phase A.
           // The move: register k of lane t -> row k, position t of my stage row; then lane t reads row t.  Row
@@ -1220,7 +1271,11 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #pragma unroll
             for (int b = 0; b < 5; ++b) md5[b] = acc[b].x + acc[b].y;
           };
+#ifdef NB_ABL_NODOTS
+          for (int b = 0; b < 5; ++b) md5[b] = Tm[b] + dA[b] + x[b];
+#else
           if (is_a) half_dots(x); else half_dots(dA);
+#endif
           if (!do_cn) split_finish();
         }
 
@@ -1666,7 +1721,9 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             if (lane == 0)
               asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n}" ::"r"(smem_u32(&sh_cbar[grp]))
                            : "memory");
+#ifndef NB_ABL_NODEC
             split_finish();
+#endif
             mbar_wait(&sh_cbar[grp], cb_parity);
             cb_parity ^= 1u;
           } else {
@@ -1687,7 +1744,11 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               case 2: tot_prod<R, (R >= 2 ? 2 : 1), TT, C::QS>(smem, gbase + NS * GBLK, SPLIT, cvalid); break;
               case 4: tot_prod<R, (R >= 4 ? 4 : 1), TT, C::QS>(smem, gbase + NS * GBLK, SPLIT, cvalid); break;
               case 8: tot_prod<R, (R >= 8 ? 8 : 1), TT, C::QS>(smem, gbase + NS * GBLK, SPLIT, cvalid); break;
-              default: tot_prod<R, R, TT, C::QS>(smem, gbase + NS * GBLK, SPLIT, cvalid); break;
+              default:
+#ifndef NB_ABL_NOTOT
+                tot_prod<R, R, TT, C::QS>(smem, gbase + NS * GBLK, SPLIT, cvalid);
+#endif
+                break;
             }
           } else if constexpr (LANEMAJOR) {
             const float* xs = F16 ? GST + NS * GBLKH : GST + buf * GBLK;
