@@ -42,7 +42,9 @@ struct EdgeDev {      // 32 bytes, one per internal edge slot c*kpad + j (var < 
   uint8_t pib[8];     // pi_h(e_i)    = H_cv alpha^i     (i < m), bit j = bit i of h*alpha^j
   uint8_t pinvb[8];   // pi_h^-1(e_i) = H_cv^-1 alpha^i  (= pi_{h^-1}(e_i))
   uint8_t plogh;      // log_alpha of the partner edge's coefficient
-  uint8_t pad[3];
+  uint8_t kind_a;     // q = 256 split decision: 1 if e evaluates the high half (one of v's two edges; the host
+                      // orients them so that both edge slots of a warp are of the same kind)
+  uint8_t pad[2];
 };
 static_assert(sizeof(EdgeDev) == 32, "EdgeDev layout");
 

@@ -56,7 +56,7 @@ struct ClusterParams {
 // permutation images of h come from a per-field table (CodeDev::pinv_tab, copied to shared memory)
 struct EdgeRec {
   int32_t partner_a;  // partner edge << 9 | h of the partner edge << 1 | is_a ; -1: padding slot
-  uint32_t var_h;     // variable << 8 | h_cv
+  uint32_t var_h;     // variable << 8 | h_cv, bit 31: kind_a (q = 256 split decision)
 };
 
 // alignment of the cluster kernels' dynamic shared memory: one message row (q floats, q <= 256)
@@ -86,10 +86,10 @@ struct CCfg {
 #define NB_NSTAGE 2
 #endif
   static constexpr int NS = NB_NSTAGE;               // stage buffers per group (chunks in flight + 1)
-  // q >= 128: one more row per team, the work row of the linear F32 path (transposition, decision buffer,
-  // check-node scatter): the staged rows are then only read by the generic proxy, so no proxy fence and no
-  // end-of-chunk barrier is needed before their next bulk fill
-  static constexpr int NW = MB >= 7 ? 1 : 0;
+  // q >= 64: one more row per team, the work row of the F32 kernels (transposition, decision buffer, check-node
+  // scatter): the staged rows are then only read by the generic proxy, so no proxy fence and no end-of-chunk
+  // barrier is needed before their next bulk fill
+  static constexpr int NW = MB >= 6 ? 1 : 0;
   static constexpr int RB = NS + NW;                 // row buffers per team
   static constexpr int TEAMW = RB * QS + NS * THW;
 };
@@ -664,7 +664,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
       const EdgeDev* ep = cd.edges + (size_t)c * KPAD + jj;
       if (ep->var >= 0) {
         rr.partner_a = (ep->partner << 9) | ((int)cd.edges[ep->partner].h << 1) | (ep->is_a ? 1 : 0);
-        rr.var_h = ((uint32_t)ep->var << 8) | ep->h;
+        rr.var_h = ((uint32_t)ep->var << 8) | ep->h | ((uint32_t)(ep->kind_a ? 1 : 0) << 31);
       }
     }
     recs[i] = rr;
@@ -721,6 +721,8 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   // fast bit rule in con[e]; at the end of the pass x_v = the two nibbles and each CTA forms its checks'
   // exact syndromes from them.  The paper syndrome (mode 1) keeps the whole decision.
   constexpr bool SPLITDEC_CT = LIN && TT == 16 && !SYM && !SOFT;
+  // F32 kernels at q >= 64: the transposition, decision buffer and scatter go to a per-team work row (CCfg::NW)
+  constexpr bool WROW = !F16 && MB >= 6;
   const bool split = SPLITDEC_CT && mode == 0;
   const int step = P.step_mode;
   const size_t EQ = (size_t)cd.E * Q;
@@ -859,9 +861,9 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         // divergent thread would cost a uniform-register waterfall loop over the warp's team leaders
         if constexpr (PSTAGE) {
           if (act) {
-            const float* srcp = call->p0buf + ((size_t)slot * cd.N + (rr.var_h >> 8)) * Q;
+            const float* srcp = call->p0buf + ((size_t)slot * cd.N + (rr.var_h >> 8 & 0x7FFFFFu)) * Q;
             float* dstp = PB + ((size_t)b * nteams + team) * Q;
-            NB_CHECK((rr.var_h >> 8) < (uint32_t)cd.N && b < NS && team < nteams);
+            NB_CHECK((rr.var_h >> 8 & 0x7FFFFFu) < (uint32_t)cd.N && b < NS && team < nteams);
 #pragma unroll
             for (int c4 = 0; c4 < Q / 4; ++c4)
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dstp + 4 * c4)), "l"(srcp + 4 * c4)
@@ -870,7 +872,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           }
         }
         if (act && !C::THREG && !PMF) {
-          const float* srcT = Tt + (size_t)(rr.var_h >> 8) * 8;
+          const float* srcT = Tt + (size_t)(rr.var_h >> 8 & 0x7FFFFFu) * 8;
           float* dstT = THB + b * nteams * 8;
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dstT)), "l"(srcT) : "memory");
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dstT + 4)), "l"(srcT + 4) : "memory");
@@ -901,7 +903,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
                      blk - o < NB_BLK_PIECE ? blk - o : NB_BLK_PIECE, &gmbar[b]);
         }
 #ifdef NB_TT_BULK
-        if (act && !C::THREG && !PMF) bulk_g2s(THB + b * nteams * 8, Tt + (size_t)(rr.var_h >> 8) * 8, 32, &gmbar[b]);
+        if (act && !C::THREG && !PMF) bulk_g2s(THB + b * nteams * 8, Tt + (size_t)(rr.var_h >> 8 & 0x7FFFFFu) * 8, 32, &gmbar[b]);
 #endif
       };
       // channel-term row of chunk kc's variable, prefetched into registers one chunk ahead
@@ -911,7 +913,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         if (PMF || !C::THREG || !in_check || kc >= nch) return;
         const EdgeRec rr = recs[(kc * CPC + lc) * KT + j];
         if (rr.partner_a < 0) return;
-        const float4* src = reinterpret_cast<const float4*>(Tt + (size_t)(rr.var_h >> 8) * 8);
+        const float4* src = reinterpret_cast<const float4*>(Tt + (size_t)(rr.var_h >> 8 & 0x7FFFFFu) * 8);
         dst[0] = __ldcg(src);
         if constexpr (MB > 4) dst[1] = __ldcg(src + 1);
       };
@@ -933,14 +935,15 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         EdgeRec rr{-1, 0};
         if (in_check) rr = recs[(kc * CPC + lc) * KT + j];
         const bool active = cvalid && rr.partner_a >= 0;
-        const bool is_a = active && (rr.partner_a & 1);
+        const bool is_a = active && (rr.partner_a & 1);  // v's deciding edge (whole decision)
+        const bool kind_a = active && (rr.var_h >> 31);  // SPLITDEC: the edge that evaluates the high half
         const int e = c * KPAD + j;
-        const int var = (int)(rr.var_h >> 8);
+        const int var = (int)(rr.var_h >> 8 & 0x7FFFFFu);
         // my row: the message consumed by edge e (F32; it doubles as the work row), or (F16) the half
         // stage row sth, read only in phase A, and the float work row
         // LIN: the staged row stg is only read (phase A); st is my work row
         float* const stg = GST + buf * GBLK + trow * C::QS;
-        float* st = F16 ? WK : LIN ? GST + NS * GBLK + trow * C::QS : stg;
+        float* st = F16 ? WK : WROW ? GST + NS * GBLK + trow * C::QS : stg;
         const __half* sth = reinterpret_cast<const __half*>(GST + buf * GBLKH) + trow * C::QS;
 
         // ---- channel terms t_i = tanh(L_i / 2)
@@ -1202,7 +1205,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #endif
           if (active && t == 0) {
             const uint32_t nib = ((sb >> 1) ^ ((sb & 1u) ? 0xFu : 0u)) & 0xFu;  // bit = sgn M(alpha^i) ^ sgn M(0)
-            con[e] = (uint8_t)(is_a ? nib << 4 : nib);
+            con[e] = (uint8_t)(kind_a ? nib << 4 : nib);
           }
         };
 #ifdef NB_ABL_NODEC
@@ -1222,7 +1225,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           // halves): entry z at mpos(z) = 64 c + 4 (b ^ c) + (z & 3), c = (z >> 2) & 3, b = z >> 4
           const float* wrow = WE + ((size_t)buf * nteams + team) * (Q + 16);
           float Tm[16], dA[16];
-          if (is_a) {
+          if (kind_a) {
             // Tm = W_e in phase B: z = t | h << 4 at 64 c + 16 (h >> 2) + 4 ((h & 3) ^ c) + (t & 3), c = t >> 2: four
             // pointers (by h & 3), then [pointer + 64 (h >> 2) bytes]
             const float* pk[4];
@@ -1274,7 +1277,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #ifdef NB_ABL_NODOTS
           for (int b = 0; b < 5; ++b) md5[b] = Tm[b] + dA[b] + x[b];
 #else
-          if (is_a) half_dots(x); else half_dots(dA);
+          if (kind_a) half_dots(x); else half_dots(dA);
 #endif
           if (!do_cn) split_finish();
         }
@@ -1380,7 +1383,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
                   xs[hp] = inT ? x[hp] : o;
                 }
                 const int trT = (trow & ~1) | T;
-                const float* DT = F16 ? GST + NS * GBLKH + trT * C::QS : GST + (LIN ? NS * GBLK : buf * GBLK) + trT * C::QS;
+                const float* DT = F16 ? GST + NS * GBLKH + trT * C::QS : GST + (WROW ? NS * GBLK : buf * GBLK) + trT * C::QS;
                 const int dxT = T ? 16 : 0;
                 float dh[8], dq[8];
 #pragma unroll
@@ -1761,11 +1764,11 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               default: tot_sum_lm<R, R>(xs, c0, TOT, wgrp, SPLIT, pck, cvalid); break;
             }
           } else switch (JPT) {  // tix: two checks per warp -> the odd one rotates its w groups
-            case 1: tot_sum<R, 1, TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid, tix); break;
-            case 2: tot_sum<R, (R >= 2 ? 2 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid, tix); break;
-            case 4: tot_sum<R, (R >= 4 ? 4 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid, tix); break;
-            case 8: tot_sum<R, (R >= 8 ? 8 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid, tix); break;
-            default: tot_sum<R, R, TT, C::QS>(smem, gbase + (F16 ? 0 : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid, tix); break;
+            case 1: tot_sum<R, 1, TT, C::QS>(smem, gbase + (F16 ? 0 : WROW ? NS * GBLK : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid, tix); break;
+            case 2: tot_sum<R, (R >= 2 ? 2 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : WROW ? NS * GBLK : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid, tix); break;
+            case 4: tot_sum<R, (R >= 4 ? 4 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : WROW ? NS * GBLK : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid, tix); break;
+            case 8: tot_sum<R, (R >= 8 ? 8 : 1), TT, C::QS>(smem, gbase + (F16 ? 0 : WROW ? NS * GBLK : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid, tix); break;
+            default: tot_sum<R, R, TT, C::QS>(smem, gbase + (F16 ? 0 : WROW ? NS * GBLK : buf * GBLK), TOT, wgrp, SPLIT, pck, cvalid, tix); break;
           }
           check_sync(lc, TPC);
           // q = 256 (LIN): read W_e back in the phase-A coordinates z = 16 t + r (my own XOR chain of pi_e^-1 images,
@@ -1820,7 +1823,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             // my last generic access to this chunk's stage buffer: order it before the buffer's next bulk fill
             // here, so that the fence does not wait for the global stores below (LIN: the generic writes go to the
             // work rows, the staged rows are only read -- no fence)
-            if constexpr (!LIN) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if constexpr (!WROW) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             const int prow = rr.partner_a >> 9;  // stored where the partner edge will read it
             NB_CHECK(prow >= 0 && prow < cd.E);
             float* dst = Wout + (size_t)prow * Q;
@@ -1882,7 +1885,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         // LIN: no generic writes to the staged rows; the buffer refilled at the next chunk's start was last read
         // before this chunk's first check barrier, and a work row is rewritten only by its own team after the
         // other threads' check-node accesses to it (second check barrier) -- no end-of-chunk barrier either
-        if constexpr (!LIN) {
+        if constexpr (!WROW) {
           if (!(do_cn && active)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           group_sync();  // the group's buffers of this chunk are free
         }
@@ -1906,7 +1909,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             if (c < cd.M && er.partner_a >= 0) {
               const int ee = c * KPAD + jj;
               const uint32_t xv = (uint32_t)__ldcg(con + ee) | (uint32_t)__ldcg(con + (er.partner_a >> 9));
-              if (er.partner_a & 1) xout[er.var_h >> 8] = (uint8_t)xv;
+              if (er.var_h >> 31) xout[er.var_h >> 8 & 0x7FFFFFu] = (uint8_t)xv;
               if (xv != 0) contrib = GE[GL[er.var_h & 0xFFu] + GL[xv]];
             }
           }

@@ -833,7 +833,7 @@ void orient_decision_owners(std::vector<EdgeDev>& edges, int E) {
 }
 
 // q = 256 (tt = 16, two edge slots 2w, 2w + 1 per warp): the cluster kernel splits each variable's decision
-// over its two edges (SPLITDEC in lf_cluster.cuh), with different code for the is_a half and the other half,
+// over its two edges (SPLITDEC in lf_cluster.cuh), with different code for the kind_a half and the other half,
 // so a warp whose two slots are of the same kind runs one of them.  Walking the warp graph (degree <= 2)
 // and alternating the kinds along it makes every warp uniform except one per odd cycle.
 void orient_uniform_kinds(std::vector<EdgeDev>& edges, int E) {
@@ -841,8 +841,8 @@ void orient_uniform_kinds(std::vector<EdgeDev>& edges, int E) {
   auto walk = [&](int s, int kind) {
     while (s < E && edges[s].var >= 0 && !done[s]) {
       const int p = edges[s].partner;
-      edges[s].is_a = (uint8_t)kind;
-      edges[p].is_a = (uint8_t)(1 - kind);
+      edges[s].kind_a = (uint8_t)kind;
+      edges[p].kind_a = (uint8_t)(1 - kind);
       done[s] = done[p] = 1;
       s = p ^ 1;         // the other slot of the partner's warp takes the partner's kind
       kind = 1 - kind;
@@ -859,11 +859,6 @@ void assign_decision_owners(std::vector<EdgeDev>& edges, int E, int tt, int kpad
 #ifdef NB_WARPDEC
   if (tt == 16) {  // goes with the kernel's WARPDEC (off by default, see lf_cluster.cuh)
     orient_decision_owners(edges, E);
-    return;
-  }
-#else
-  if (tt == 16) {
-    orient_uniform_kinds(edges, E);
     return;
   }
 #endif
@@ -1037,6 +1032,8 @@ nbldpc_status_t nbldpc_code_create(int m, uint32_t prim_poly, int M, int N, int 
     }
   }
   if (colw2 && !getenv("NBLDPC_FIRST_EDGE_DECIDES")) assign_decision_owners(edges, E, tt, kpad);
+  // q = 256: the split decision's kinds (kind_a), beside the deciding edges (is_a) of the whole decision
+  if (colw2 && tt == 16) orient_uniform_kinds(edges, E);
   std::vector<uint8_t> gexp(2 * (q - 1) + 1), glog(q, 0);
   for (size_t i = 0; i < gexp.size(); ++i) gexp[i] = (uint8_t)ex[i];
   for (int x = 1; x < q; ++x) glog[x] = (uint8_t)lg[x];

@@ -17,11 +17,12 @@ llr = torch.from_numpy(synth.config_llr(name, 0, F, point=point)).cuda()
 for vn in vns:
     for g in graphs:
         es = not os.environ.get('NO_EARLY')
-        out = code.decode(llr, c['max_iters'], slots=slots, use_graph=g, vn_algorithm=vn, early_stop=es); torch.cuda.synchronize()
+        mf = int(os.environ.get('MSG', '0'))  # 1: half-precision messages
+        out = code.decode(llr, c['max_iters'], slots=slots, use_graph=g, vn_algorithm=vn, early_stop=es, message_format=mf); torch.cuda.synchronize()
         ts = []
         for _ in range(3):
             e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-            e0.record(); out = code.decode(llr, c['max_iters'], slots=slots, use_graph=g, vn_algorithm=vn, early_stop=es); e1.record()
+            e0.record(); out = code.decode(llr, c['max_iters'], slots=slots, use_graph=g, vn_algorithm=vn, early_stop=es, message_format=mf); e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
         it = out['iters'].cpu().numpy(); ok = out['ok'].cpu().numpy()
