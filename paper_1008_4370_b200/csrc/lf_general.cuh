@@ -114,7 +114,8 @@ __global__ void __launch_bounds__(256) lfg_frame_kernel(GenParams P) {
   const int team = tid / TT, t = tid & (TT - 1);
   const bool in_team = team < P.teams;
   const unsigned tmask = TT >= 32 ? 0xffffffffu : (((1u << TT) - 1u) << (lane & ~(TT - 1)));
-  const int VS = P.jmax > 1 ? P.jmax : 1;  // team vectors: w_1..w_d (variable phase) / TOT (check phase)
+  // team vectors: w_1..w_d (variable phase) / TOT and one staged U row (check phase)
+  const int VS = P.jmax > 2 ? P.jmax : 2;
   // team stride padded to TT (mod 32): the per-thread vector entries at [i][r][t] of the teams of a
   // warp then fall in 32 distinct banks
   const int TS = VS * Q + ((TT - (VS * Q) % 32) & 31);
@@ -367,17 +368,32 @@ __global__ void __launch_bounds__(256) lfg_frame_kernel(GenParams P) {
           uint32_t sg[R];
 #pragma unroll
           for (int r = 0; r < R; ++r) { mag[r] = 0.0f; sg[r] = 0u; }
+          // each U_k row is loaded coalesced (16-byte loads, the next one prefetched into registers) and staged
+          // in the team's second vector in the interleaved layout z = tR + r -> r TT + t (conflict-free stores);
+          // the permuted gather then reads shared memory instead of issuing scattered 4-byte L2 loads
+          // (ncu, J3: 26% of the stall samples waited on those loads)
+          float* const SG = Tb + Q;
+          auto spos = [&](int z) { return ((z & (R - 1)) * TT) | (z >> LR); };  // a bit permutation: XOR-linear
+          float nxt[R];
+          if (kc > 0) ld_block(U + (size_t)eb * Q + t * R, nxt);
           for (int k = 0; k < kc; ++k) {
             const EdgeDev ed = cd.edges[eb + k];
+#pragma unroll
+            for (int r = 0; r < R; ++r) SG[r * TT + t] = nxt[r];
+            if (k + 1 < kc) ld_block(U + (size_t)(eb + k + 1) * Q + t * R, nxt);
+            uint8_t bp[8];
+#pragma unroll
+            for (int i = 0; i < MB; ++i) bp[i] = (uint8_t)spos(ed.pib[i]);
             int idx[R];
-            perm_block(ed.pib, idx);
-            const float* src = U + (size_t)(eb + k) * Q;
+            perm_block(bp, idx);
+            if constexpr (TT > 1) __syncwarp(tmask);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-              const float u = __ldcg(src + idx[r]);
+              const float u = SG[idx[r]];
               mag[r] += fabsf(u);
               sg[r] ^= __float_as_uint(u);
             }
+            if constexpr (TT > 1) __syncwarp(tmask);
           }
           {
             // scalar stores: the padded team stride keeps Tb only 4-byte aligned

@@ -584,7 +584,7 @@ nbldpc_status_t decode_general(nbldpc_code_s* c, const float* llr, const float* 
                                float* post, uint8_t* xmap, cudaStream_t st) {
   NB_TRY(cudaSetDevice(c->device));
   const int q = c->q, tt = q < 16 ? 1 : q / 16;
-  const int vs = std::max(1, c->j_max);
+  const int vs = std::max(2, c->j_max);  // as the kernel's VS: >= 2 vectors (TOT and a staged U row)
   const int ts = vs * q + ((tt - (vs * q) % 32) & 31);  // the kernel's padded team stride (floats)
   const size_t per_team = (size_t)ts * sizeof(float);
   const size_t tables = (size_t)3 * q * sizeof(int);
