@@ -258,8 +258,10 @@ __global__ void __launch_bounds__(256) lfg_frame_kernel(GenParams P) {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             float a = p0[r];
-            if (d == 3) {
-              a *= TW(0, r) * TW(1, r) * TW(2, r);
+            if (d == 3) {  // the loop's order, unrolled
+              a *= TW(0, r);
+              a *= TW(1, r);
+              a *= TW(2, r);
             } else {
               for (int i = 0; i < d; ++i) a *= TW(i, r);
             }
