@@ -5,9 +5,10 @@
 // the GPU at once (persistent); each cluster of CS CTAs decodes one frame at a time, start to finish,
 // then takes the next frame from a global counter.  CTA rank r of the cluster owns the check chunks
 // r, r + CS, ... (checks_per_cta checks each, CPC * TPC threads).  One flooding iteration is one
-// pass of every CTA over its chunks (the next chunk's messages prefetched with cp.async while the
-// current one computes) followed by a hardware cluster barrier; the frame's two message buffers
-// stay L2-resident (clusters x 2 E 2^m x 4 bytes).  After the barrier each CTA folds its checks'
+// pass of every CTA over its chunks (the next chunk's messages bulk-copied into shared memory while the
+// current one computes) followed by a hardware cluster barrier; the frame's two message buffers live in
+// HBM (148 frames x 2 E 2^m x 4 bytes exceed the L2: every pass streams one set in and one out, DESIGN.md
+// 7.6).  After the barrier each CTA folds its checks'
 // syndrome bytes, ORs a "not a codeword" flag into rank 0's shared memory (DSMEM), and a second
 // barrier makes the stopping decision cluster-uniform.
 //
@@ -15,8 +16,9 @@
 //   VARIABLE TO CHECK  raw = P_v^0 (*) Gamma^-1(W_e'), U_e = normalise(Gamma(raw)),
 //       with P^0 = (x)_i (1, tanh(L_i/2)): the XOR-convolution is m butterfly stages
 //       x(z) <- x(z) + t_i x(z ^ alpha^i)
-//   TENTATIVE DECISION at v's first edge: M_v(z) = sum_y raw(y) W_e(z ^ y) at
-//       z = 0, alpha^i (and H_cv alpha^i in paper mode)
+//   TENTATIVE DECISION at v's deciding edge: M_v(z) = sum_y raw(y) W_e(z ^ y) at
+//       z = 0, alpha^i (and H_cv alpha^i in paper mode); q = 256 hot path: split over
+//       v's two edges (SPLITDEC below)
 //   CHECK TO VARIABLE X_e(pi_e^-1 z) = U_e(z) (scatter), TOT(w) = sum_j X_j(w),
 //       W_e(next)(z) = TOT(pi_e^-1 z) - U_e(z) (log-magnitudes add, signs XOR).
 //
