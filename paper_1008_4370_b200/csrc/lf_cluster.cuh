@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   // exact syndromes from them.  The paper syndrome (mode 1) keeps the whole decision.
   constexpr bool SPLITDEC_CT = LIN && TT == 16 && !SYM && !SOFT;
   // F32 kernels at q >= 64: the transposition, decision buffer and scatter go to a per-team work row (CCfg::NW)
-  constexpr bool WROW = !F16 && MB >= 6;
+  constexpr bool WROW = !F16 && MB >= 6 && !SYM;  // (the symbol-output variant keeps its registers: no work rows)
   const bool split = SPLITDEC_CT && mode == 0;
   const int step = P.step_mode;
   const size_t EQ = (size_t)cd.E * Q;
@@ -960,8 +960,9 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             tb8[0] = a4.x; tb8[1] = a4.y; tb8[2] = a4.z; tb8[3] = a4.w; tb8[4] = b4.x; tb8[5] = b4.y; tb8[6] = b4.z; tb8[7] = b4.w;
           }
 #pragma unroll
-          // (an inactive padding team's terms are never used: its outputs become the neutral message below)
-          for (int b = 0; b < MB; ++b) th[b] = !PMF ? (C::THREG ? tv[b] : tb8[b]) : 0.0f;
+          // (an inactive padding team's terms are never used: its outputs become the neutral message below;
+          // the log-format kernels keep the select, which their register allocation prefers)
+          for (int b = 0; b < MB; ++b) th[b] = (!PMF && (LIN || active)) ? (C::THREG ? tv[b] : tb8[b]) : 0.0f;
         }
         // pmf input: my R entries of p_v at the phase-B coordinates zr, straight from L2
         float pv[PMF ? R : 1];
@@ -1825,7 +1826,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             // my last generic access to this chunk's stage buffer: order it before the buffer's next bulk fill
             // here, so that the fence does not wait for the global stores below (LIN: the generic writes go to the
             // work rows, the staged rows are only read -- no fence)
-            if constexpr (!WROW) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+
             const int prow = rr.partner_a >> 9;  // stored where the partner edge will read it
             NB_CHECK(prow >= 0 && prow < cd.E);
             float* dst = Wout + (size_t)prow * Q;
@@ -1888,7 +1889,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         // before this chunk's first check barrier, and a work row is rewritten only by its own team after the
         // other threads' check-node accesses to it (second check barrier) -- no end-of-chunk barrier either
         if constexpr (!WROW) {
-          if (!(do_cn && active)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           group_sync();  // the group's buffers of this chunk are free
         }
         buf = buf + 1 == NS ? 0 : buf + 1;
@@ -1900,26 +1901,39 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
       auto split_pass_end = [&](bool want_syn) -> int {
         int badc = 0;
         const int tot_e = nch * CPC * KT;
-        for (int i0 = 0; i0 < tot_e; i0 += nthr) {
-          const int i = i0 + tid;
-          uint32_t contrib = 0;
-          if (i < tot_e) {
-            const int kc = i / (CPC * KT), rem = i - kc * (CPC * KT);
-            const int l = rem / KT, jj = rem - l * KT;
-            const int c = ((int)rank + kc * (int)csz) * CPC + l;
-            const EdgeRec er = recs[i];
-            if (c < cd.M && er.partner_a >= 0) {
-              const int ee = c * KPAD + jj;
-              const uint32_t xv = (uint32_t)__ldcg(con + ee) | (uint32_t)__ldcg(con + (er.partner_a >> 9));
-              if (er.var_h >> 31) xout[er.var_h >> 8 & 0x7FFFFFu] = (uint8_t)xv;
-              if (xv != 0) contrib = GE[GL[er.var_h & 0xFFu] + GL[xv]];
+        constexpr int UB = 8;  // edge slots per thread whose byte loads are in flight together
+        for (int i0 = 0; i0 < tot_e; i0 += UB * nthr) {
+          uint32_t xa[UB], vh[UB];
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            const int i = i0 + u * nthr + tid;
+            xa[u] = 0;
+            vh[u] = 0;
+            if (i < tot_e) {
+              const int kc = i / (CPC * KT), rem = i - kc * (CPC * KT);
+              const int l = rem / KT, jj = rem - l * KT;
+              const int c = ((int)rank + kc * (int)csz) * CPC + l;
+              const EdgeRec er = recs[i];
+              if (c < cd.M && er.partner_a >= 0) {
+                xa[u] = (uint32_t)__ldcg(con + c * KPAD + jj) | (uint32_t)__ldcg(con + (er.partner_a >> 9)) | 0x100u;
+                vh[u] = er.var_h;
+              }
             }
           }
-          if (want_syn) {
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1)
-              if (o < KT) contrib ^= __shfl_xor_sync(0xffffffffu, contrib, o);
-            badc |= (int)contrib;
+          for (int u = 0; u < UB; ++u) {
+            uint32_t contrib = 0;
+            if (xa[u] & 0x100u) {  // a real edge
+              const uint32_t xv = xa[u] & 0xFFu;
+              if (vh[u] >> 31) xout[vh[u] >> 8 & 0x7FFFFFu] = (uint8_t)xv;
+              if (xv != 0) contrib = GE[GL[vh[u] & 0xFFu] + GL[xv]];
+            }
+            if (want_syn) {
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1)
+                if (o < KT) contrib ^= __shfl_xor_sync(0xffffffffu, contrib, o);
+              badc |= (int)contrib;
+            }
           }
         }
         return badc;
