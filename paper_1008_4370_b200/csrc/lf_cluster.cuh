@@ -724,7 +724,9 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   // exact syndromes from them.  The paper syndrome (mode 1) keeps the whole decision.
   constexpr bool SPLITDEC_CT = LIN && TT == 16 && !SYM && !SOFT;
   // F32 kernels at q >= 64: the transposition, decision buffer and scatter go to a per-team work row (CCfg::NW)
-  constexpr bool WROW = !F16 && MB >= 6 && !SYM;  // (the symbol-output variant keeps its registers: no work rows)
+  // (the q = 64 symbol-output variant keeps its registers: no work rows -- C2 symbol outputs 3.71e9 -> 4.44e9;
+  // the q >= 128 linear-format check node's read-back assumes separate work rows, so SYM keeps them there)
+  constexpr bool WROW = !F16 && MB >= 6 && !(SYM && MB < 7);
   const bool split = SPLITDEC_CT && mode == 0;
   const int step = P.step_mode;
   const size_t EQ = (size_t)cd.E * Q;

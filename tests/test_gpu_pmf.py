@@ -223,6 +223,7 @@ POST_CASES = [
     ("C5", "pmf", 3.5, 128, 8),
     ("C2", "pmf", 0.5, 64, 4),
     ("C3", "llr", 0, 32, 3),
+    ("C2", "llr", 0, 64, 4),  # the q = 64 symbol-output variant of the cluster kernel (no work rows)
 ]
 
 
