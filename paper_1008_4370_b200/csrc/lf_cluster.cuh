@@ -180,6 +180,32 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+// W_e rows are written once and next read a whole pass later (never from L2: the in-flight frames' message sets
+// exceed it): NB_STCS stores them evict-first so that the L2 keeps the rows that are read twice
+// within a pass (as a partner row and as the decision's own row)
+__device__ __forceinline__ void st_w4(float* p, float4 v) {
+#ifdef NB_STCS
+  __stcs(reinterpret_cast<float4*>(p), v);
+#else
+  *reinterpret_cast<float4*>(p) = v;
+#endif
+}
+
+// NB_STCS >= 2: the decision's own-row copy with an L2 evict-first policy (the row's other read is the partner's
+// block copy, which keeps the default policy)
+__device__ __forceinline__ void bulk_g2s_ef(void* dst, const void* src, uint32_t bytes, uint64_t* mb) {
+#if defined(NB_STCS) && NB_STCS >= 2
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(mb)), "l"(pol)
+               : "memory");
+#else
+  bulk_g2s(dst, src, bytes, mb);
+#endif
+}
+
 // the same on shared-window addresses computed once (no generic-to-shared conversion in the loop)
 __device__ __forceinline__ void mbar_arrive_tx_s(uint32_t mb, uint32_t tx) {
   asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(mb), "r"(tx) : "memory");
@@ -889,7 +915,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
         if (wecp) tx += Q * 4;
         mbar_arrive_tx(&gmbar[b], tx);
         if constexpr (SPLITDEC_CT) {
-          if (wecp) bulk_g2s(WE + ((size_t)b * nteams + team) * (Q + 16), Win + (size_t)(rr.partner_a >> 9) * Q, Q * 4, &gmbar[b]);
+          if (wecp) bulk_g2s_ef(WE + ((size_t)b * nteams + team) * (Q + 16), Win + (size_t)(rr.partner_a >> 9) * Q, Q * 4, &gmbar[b]);
         }
         // the block in pieces of <= NB_BLK_PIECE bytes (several TMA transfers in flight)
 #ifndef NB_BLK_PIECE
@@ -1802,8 +1828,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
             float* dst = Wout + (size_t)prow * Q;
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4)
-              *reinterpret_cast<float4*>(dst + mpos<MB>(16 * t + 4 * c4, prow)) =
-                  make_float4(out[4 * c4], out[4 * c4 + 1], out[4 * c4 + 2], out[4 * c4 + 3]);
+              st_w4(dst + mpos<MB>(16 * t + 4 * c4, prow), make_float4(out[4 * c4], out[4 * c4 + 1], out[4 * c4 + 2], out[4 * c4 + 3]));
           } else if (active) {
             float out[R];
             const uint32_t tot_s = PAIRIL ? smem_u32(GST + NS * GBLK + (trow & ~1) * C::QS) + ((uint32_t)(trow & 1) << 2)
@@ -1870,15 +1895,14 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
                 } else {
 #pragma unroll
                   for (int q4 = 0; q4 < V / 4; ++q4)
-                    *reinterpret_cast<float4*>(dst + mpos<MB>(z0 + 4 * q4, prow)) = make_float4(
-                        out[h * V + 4 * q4], out[h * V + 4 * q4 + 1], out[h * V + 4 * q4 + 2], out[h * V + 4 * q4 + 3]);
+                    st_w4(dst + mpos<MB>(z0 + 4 * q4, prow), make_float4(out[h * V + 4 * q4], out[h * V + 4 * q4 + 1],
+                                                                         out[h * V + 4 * q4 + 2], out[h * V + 4 * q4 + 3]));
                 }
               }
             } else if constexpr (R >= 4) {
 #pragma unroll
               for (int ch = 0; ch < CH; ++ch)
-                *reinterpret_cast<float4*>(dst + mpos<MB>(4 * ch, prow)) =
-                    make_float4(out[4 * ch], out[4 * ch + 1], out[4 * ch + 2], out[4 * ch + 3]);
+                st_w4(dst + mpos<MB>(4 * ch, prow), make_float4(out[4 * ch], out[4 * ch + 1], out[4 * ch + 2], out[4 * ch + 3]));
             } else {
 #pragma unroll
               for (int r = 0; r < R; ++r) dst[r] = out[r];
