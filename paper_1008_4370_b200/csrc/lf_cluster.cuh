@@ -601,6 +601,11 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   // offset -- the check node's scatter / read-back addresses are then the XOR chain itself
   float* const smem = smem_raw;
   __shared__ int sh_frame, sh_flag[2], sh_bad;
+  // lazy decision (SPLITDEC): sh_skip = stamp of the pass in which some probe check of the cluster was
+  // proven unsatisfied (the pass cannot stop the frame, so the rest of its tentative decision is skipped);
+  // sh_pc[team] = the probe chunk's tag << 8 | h_e x_v of the team's edge
+  __shared__ int sh_skip;
+  __shared__ uint32_t sh_pc[64];
   __shared__ __align__(8) uint64_t sh_mbar[8 * C::NS];  // [group][buffer]: the group's teams arrive, bulk copies complete_tx
   __shared__ __align__(8) uint64_t sh_cbar[8];  // SPLITDEC: [group] "every warp of the check has scattered" (one arrival per warp)
 
@@ -705,6 +710,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
   if (tid == 0) {
     sh_flag[0] = 0;
     sh_flag[1] = 0;
+    sh_skip = -1;
     for (int gg = 0; gg < ngrp; ++gg) {
       for (int b = 0; b < NS; ++b) mbar_init(&sh_mbar[NS * gg + b], (uint32_t)(GT / TT));
       mbar_init(&sh_cbar[gg], (uint32_t)(GT / 32));
@@ -862,11 +868,36 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
       __half* const WoutH = reinterpret_cast<__half*>(ws.W) + ((size_t)(rb_ ^ 1) * ws.S + slot) * EQ;
       const bool do_dec = ell >= 1;
       const bool do_cn = step || ell < max_iters;
+      // lazy decision: a pass that also runs the check node (ell < max_iters) needs its tentative decision only to
+      // test the stopping rule (the estimate is returned for the last pass alone).  The first
+      // NB_NPROBE chunks of every CTA are probes: their teams evaluate both halves of the split decision, so the
+      // chunk's checks know their syndromes at once; the first unsatisfied probe check proves that the pass does
+      // not stop the frame, and the remaining chunks of the cluster skip the decision and the own-row copy.
+      // A pass whose probes are all satisfied, the last pass and step mode decide in full (outputs unchanged).
+#ifndef NB_NPROBE
+#define NB_NPROBE 128
+#endif
+      // probes per CTA and pass: at most an eighth of its chunks (a probe chunk costs an extra half decision)
+#ifndef NB_PROBE_SHIFT
+#define NB_PROBE_SHIFT 3
+#endif
+      const int nprobe = NB_NPROBE < (nch >> NB_PROBE_SHIFT) ? NB_NPROBE : ((nch >> NB_PROBE_SHIFT) > 1 ? (nch >> NB_PROBE_SHIFT) : 1);
+      const int ps = round * 4099 + ell;  // pass stamp (max_iters < 4000: distinct over the frames of this CTA)
+      const bool lazy = SPLITDEC_CT && NB_NPROBE > 0 && split && do_dec && do_cn && !step && max_iters < 4000;
+      const bool lazy_all = lazy && !call->early_stop;  // no stopping rule: only the last pass decides
+      auto we_needed = [&](int kcs) -> bool {  // does chunk kcs read its teams' own rows (warp-uniform)
+        if (!lazy) return true;
+        if (lazy_all) return false;
+        if (kcs < nprobe) return true;
+        int v = *reinterpret_cast<volatile int*>(&sh_skip);
+        v = __shfl_sync(0xffffffffu, v, 0);
+        return v != ps;
+      };
 
       // stage chunk kc into buffer b of my group (one arrival per team on gmbar[b]): the group leader
       // bulk-copies the group's block of message rows (contiguous: reader-ordered storage), wide teams
       // bulk-copy their channel-term row; plain loads for q = 2
-      auto stage = [&](int kc, int b) {
+      auto stage = [&](int kc, int b, bool need_we) {
         if (t != 0) return;
         uint32_t tx = 0;
         EdgeRec rr{-1, 0};
@@ -911,7 +942,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #endif
         tx += blk;
         // SPLITDEC: my edge's own message W_e (row prow, contiguous) into my WE row, on the same mbarrier
-        const bool wecp = SPLITDEC_CT && split && ell >= 1 && act;
+        const bool wecp = SPLITDEC_CT && split && ell >= 1 && act && need_we;
         if (wecp) tx += Q * 4;
         mbar_arrive_tx(&gmbar[b], tx);
         if constexpr (SPLITDEC_CT) {
@@ -949,12 +980,27 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
       };
 
       int buf = 0;
-      for (int k0 = 0; k0 < NS - 1 && k0 < nch; ++k0) stage(k0, k0);  // prologue: NS - 1 chunks in flight
+      for (int k0 = 0; k0 < NS - 1 && k0 < nch; ++k0) {  // prologue: NS - 1 chunks in flight
+        const bool nw = we_needed(k0);
+        stage(k0, k0, nw);
+      }
       float4 thn[2];
       th_load(0, thn);
 #pragma unroll 1
       for (int kc = 0; kc < nch; ++kc) {
-        if (kc + NS - 1 < nch) stage(kc + NS - 1, buf == 0 ? NS - 1 : buf - 1);
+        if (kc + NS - 1 < nch) {
+          const bool nw = we_needed(kc + NS - 1);
+          stage(kc + NS - 1, buf == 0 ? NS - 1 : buf - 1, nw);
+        }
+        // lazy decision: this chunk skips the decision (skipc) or is a probe
+        bool skipc = lazy_all, probe = false;
+        if (lazy && !lazy_all) {
+          int v = *reinterpret_cast<volatile int*>(&sh_skip);
+          v = __shfl_sync(0xffffffffu, v, 0);
+          skipc = v == ps;
+          probe = !skipc && kc < nprobe;
+        }
+        const uint32_t ptag = ((uint32_t)ps * 256u + (uint32_t)kc) & 0xFFFFFFu;  // kc < nprobe <= 128
         const float4 thc[2] = {thn[0], thn[1]};
         th_load(kc + 1, thn);
         mbar_wait(&gmbar[buf], (mb_parity >> buf) & 1u);
@@ -1244,72 +1290,91 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #else
         if constexpr (SPLITDEC_CT)
 #endif
-        if (do_dec && split) {
-          // my half: Sum_k Pm[k] Tm[k ^ s], s = 0, 1, 2, 4, 8 over my register index k, where (is_a) Pm = raw in
-          // phase B and Tm = W_e moved to phase B, or (!is_a) Pm = W_e in phase A and Tm = raw moved to phase A.
-          // The move: register k of lane t -> row k, position t of my stage row; then lane t reads row t.  Row
-          // layout: 16 rows of 16 words, row r's 16-byte chunks XOR-swizzled by (r >> 1) & 3; the odd team's
-          // rows shifted by one (row 15 wraps to row 0) -- scalar writes and 16-byte row reads conflict-free.
-          __syncwarp();  // transposition reads of my row done
-          const int sh = trow & 1;
-          // my staged W_e row (WE rows are q + 16 words apart, so the two teams of a warp sit in opposite bank
-          // halves): entry z at mpos(z) = 64 c + 4 (b ^ c) + (z & 3), c = (z >> 2) & 3, b = z >> 4
-          const float* wrow = WE + ((size_t)buf * nteams + team) * (Q + 16);
-          float Tm[16], dA[16];
-          if (kind_a) {
-            // Tm = W_e in phase B: z = t | h << 4 at 64 c + 16 (h >> 2) + 4 ((h & 3) ^ c) + (t & 3), c = t >> 2: four
-            // pointers (by h & 3), then [pointer + 64 (h >> 2) bytes]
-            const float* pk[4];
+        if (do_dec && split && !skipc) {
+          // (probe chunks run both halves: hp = 0 the other edge's half, hp = 1 mine, whose totals stay in md5)
+          uint32_t pnib = 0;
+#pragma unroll 1
+          for (int hp = probe ? 0 : 1; hp < 2; ++hp) {
+            const bool ka = (hp == 1) == kind_a;
+            // my half: Sum_k Pm[k] Tm[k ^ s], s = 0, 1, 2, 4, 8 over my register index k, where (is_a) Pm = raw in
+            // phase B and Tm = W_e moved to phase B, or (!is_a) Pm = W_e in phase A and Tm = raw moved to phase A.
+            // The move: register k of lane t -> row k, position t of my stage row; then lane t reads row t.  Row
+            // layout: 16 rows of 16 words, row r's 16-byte chunks XOR-swizzled by (r >> 1) & 3; the odd team's
+            // rows shifted by one (row 15 wraps to row 0) -- scalar writes and 16-byte row reads conflict-free.
+            __syncwarp();  // transposition reads of my row done
+            const int sh = trow & 1;
+            // my staged W_e row (WE rows are q + 16 words apart, so the two teams of a warp sit in opposite bank
+            // halves): entry z at mpos(z) = 64 c + 4 (b ^ c) + (z & 3), c = (z >> 2) & 3, b = z >> 4
+            const float* wrow = WE + ((size_t)buf * nteams + team) * (Q + 16);
+            float Tm[16], dA[16];
+            if (ka) {
+              // Tm = W_e in phase B: z = t | h << 4 at 64 c + 16 (h >> 2) + 4 ((h & 3) ^ c) + (t & 3), c = t >> 2: four
+              // pointers (by h & 3), then [pointer + 64 (h >> 2) bytes]
+              const float* pk[4];
 #pragma unroll
-            for (int hl = 0; hl < 4; ++hl) pk[hl] = wrow + 64 * (t >> 2) + 4 * (hl ^ (t >> 2)) + (t & 3);
+              for (int hl = 0; hl < 4; ++hl) pk[hl] = wrow + 64 * (t >> 2) + 4 * (hl ^ (t >> 2)) + (t & 3);
 #pragma unroll
-            for (int h = 0; h < 16; ++h) Tm[h] = pk[h & 3][16 * (h >> 2)];
-          } else {
-            // dA = W_e in phase A: z = 16 t + 4 ch + (0..3), one 16-byte chunk each
+              for (int h = 0; h < 16; ++h) Tm[h] = pk[h & 3][16 * (h >> 2)];
+            } else {
+              // dA = W_e in phase A: z = 16 t + 4 ch + (0..3), one 16-byte chunk each
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-              const float4 v4 = *reinterpret_cast<const float4*>(wrow + 64 * ch + 4 * (t ^ ch));
-              dA[4 * ch] = v4.x; dA[4 * ch + 1] = v4.y; dA[4 * ch + 2] = v4.z; dA[4 * ch + 3] = v4.w;
+              for (int ch = 0; ch < 4; ++ch) {
+                const float4 v4 = *reinterpret_cast<const float4*>(wrow + 64 * ch + 4 * (t ^ ch));
+                dA[4 * ch] = v4.x; dA[4 * ch + 1] = v4.y; dA[4 * ch + 2] = v4.z; dA[4 * ch + 3] = v4.w;
+              }
+              // Tm = raw in phase A: register k of lane t -> row k, position t of my work row (row r's 16-byte chunks
+              // XOR-swizzled by (r >> 1) & 3, the odd team's rows shifted by one); then lane t reads its row t
+              float* pw[4];
+#pragma unroll
+              for (int c4 = 0; c4 < 4; ++c4) pw[c4] = st + 16 * sh + ((((t >> 2) ^ c4) & 3) << 2) + (t & 3);
+              if (active) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) (k == 15 ? pw[3][sh ? -16 : 240] : pw[(k >> 1) & 3][16 * k]) = x[k];
+              }
+              __syncwarp(__activemask());
+              const float* rq = st + 16 * ((t + sh) & 15);
+#pragma unroll
+              for (int c4 = 0; c4 < 4; ++c4) {
+                const float4 v4 = *reinterpret_cast<const float4*>(rq + ((((t >> 1) ^ c4) & 3) << 2));
+                Tm[4 * c4] = v4.x; Tm[4 * c4 + 1] = v4.y; Tm[4 * c4 + 2] = v4.z; Tm[4 * c4 + 3] = v4.w;
+              }
             }
-            // Tm = raw in phase A: register k of lane t -> row k, position t of my work row (row r's 16-byte chunks
-            // XOR-swizzled by (r >> 1) & 3, the odd team's rows shifted by one); then lane t reads its row t
-            float* pw[4];
+            auto half_dots = [&](const float (&Pm)[16]) {
+              float2 acc[5];
 #pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) pw[c4] = st + 16 * sh + ((((t >> 2) ^ c4) & 3) << 2) + (t & 3);
-            if (active) {
+              for (int b = 0; b < 5; ++b) acc[b] = make_float2(0.0f, 0.0f);
 #pragma unroll
-              for (int k = 0; k < 16; ++k) (k == 15 ? pw[3][sh ? -16 : 240] : pw[(k >> 1) & 3][16 * k]) = x[k];
-            }
-            __syncwarp(__activemask());
-            const float* rq = st + 16 * ((t + sh) & 15);
+              for (int p2 = 0; p2 < 8; ++p2) {
+                const int k = 2 * p2;
+                const float2 pp = make_float2(Pm[k], Pm[k + 1]);
+                acc[0] = __ffma2_rn(pp, make_float2(Tm[k], Tm[k + 1]), acc[0]);
+                acc[1] = __ffma2_rn(pp, make_float2(Tm[k + 1], Tm[k]), acc[1]);
+                acc[2] = __ffma2_rn(pp, make_float2(Tm[k ^ 2], Tm[(k ^ 2) + 1]), acc[2]);
+                acc[3] = __ffma2_rn(pp, make_float2(Tm[k ^ 4], Tm[(k ^ 4) + 1]), acc[3]);
+                acc[4] = __ffma2_rn(pp, make_float2(Tm[k ^ 8], Tm[(k ^ 8) + 1]), acc[4]);
+              }
 #pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) {
-              const float4 v4 = *reinterpret_cast<const float4*>(rq + ((((t >> 1) ^ c4) & 3) << 2));
-              Tm[4 * c4] = v4.x; Tm[4 * c4 + 1] = v4.y; Tm[4 * c4 + 2] = v4.z; Tm[4 * c4 + 3] = v4.w;
+              for (int b = 0; b < 5; ++b) md5[b] = acc[b].x + acc[b].y;
+            };
+#ifdef NB_ABL_NODOTS
+            for (int b = 0; b < 5; ++b) md5[b] = Tm[b] + dA[b] + x[b];
+#else
+            if (ka) half_dots(x); else half_dots(dA);
+#endif
+            if (probe) {
+              float mdp[5];  // (the reduction works in place: my half's totals stay in md5 for split_finish)
+#pragma unroll
+              for (int b = 0; b < 5; ++b) mdp[b] = md5[b];
+              const uint32_t sbp = split_sign_bits(mdp, lane);
+              const uint32_t nibp = ((sbp >> 1) ^ ((sbp & 1u) ? 0xFu : 0u)) & 0xFu;
+              pnib |= ka ? nibp << 4 : nibp;
             }
           }
-          auto half_dots = [&](const float (&Pm)[16]) {
-            float2 acc[5];
-#pragma unroll
-            for (int b = 0; b < 5; ++b) acc[b] = make_float2(0.0f, 0.0f);
-#pragma unroll
-            for (int p2 = 0; p2 < 8; ++p2) {
-              const int k = 2 * p2;
-              const float2 pp = make_float2(Pm[k], Pm[k + 1]);
-              acc[0] = __ffma2_rn(pp, make_float2(Tm[k], Tm[k + 1]), acc[0]);
-              acc[1] = __ffma2_rn(pp, make_float2(Tm[k + 1], Tm[k]), acc[1]);
-              acc[2] = __ffma2_rn(pp, make_float2(Tm[k ^ 2], Tm[(k ^ 2) + 1]), acc[2]);
-              acc[3] = __ffma2_rn(pp, make_float2(Tm[k ^ 4], Tm[(k ^ 4) + 1]), acc[3]);
-              acc[4] = __ffma2_rn(pp, make_float2(Tm[k ^ 8], Tm[(k ^ 8) + 1]), acc[4]);
-            }
-#pragma unroll
-            for (int b = 0; b < 5; ++b) md5[b] = acc[b].x + acc[b].y;
-          };
-#ifdef NB_ABL_NODOTS
-          for (int b = 0; b < 5; ++b) md5[b] = Tm[b] + dA[b] + x[b];
-#else
-          if (kind_a) half_dots(x); else half_dots(dA);
-#endif
+          if (probe && in_check && t == 0) {  // h_e x_v of my edge, for the probe check's syndrome
+            uint32_t cb = 0;
+            if (active && pnib != 0) cb = GE[GL[rr.var_h & 0xFFu] + GL[pnib]];
+            sh_pc[team & 63] = (ptag << 8) | cb;
+          }
           if (!do_cn) split_finish();
         }
 
@@ -1756,10 +1821,26 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
               asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n}" ::"r"(smem_u32(&sh_cbar[grp]))
                            : "memory");
 #ifndef NB_ABL_NODEC
-            split_finish();
+            if (!skipc) split_finish();
 #endif
             mbar_wait(&sh_cbar[grp], cb_parity);
             cb_parity ^= 1u;
+            if (probe && cvalid && pck == 0) {
+              // the probe check's syndrome from its teams' words of this chunk; a word with another
+              // tag (a team that did not probe) voids the probe
+              uint32_t syn = 0;
+              bool valid = KT <= 64;
+              for (int jj = 0; jj < KT && jj < 64; ++jj) {
+                const uint32_t w = *reinterpret_cast<volatile uint32_t*>(&sh_pc[(team + jj) & 63]);
+                valid = valid && (w >> 8) == ptag;
+                syn ^= w & 0xFFu;
+              }
+              if (valid && syn != 0) {
+                *reinterpret_cast<volatile int*>(&sh_skip) = ps;
+                for (uint32_t r = 0; r < csz; ++r)
+                  if (r != rank) dsmem_st(dsmem_addr(&sh_skip, r), ps);
+              }
+            }
           } else {
             check_sync(lc, TPC);
           }
@@ -1978,8 +2059,15 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
       if (tid == 0) sh_bad = 0;
       __syncthreads();
       if (SPLITDEC_CT && split && ell >= 1) {
-        const int bad = split_pass_end(true);
-        if (__syncthreads_or(bad != 0) && tid == 0) dsmem_or((ell & 1) ? flag1 : flag0, 1);
+        // lazy decision: a pass with an unsatisfied probe check (or without a stopping rule) does not stop the frame;
+        // sh_skip is final here (local and remote writes precede the cluster barrier above)
+        const bool skipped = lazy && (lazy_all || *reinterpret_cast<volatile int*>(&sh_skip) == ps);
+        if (skipped) {
+          if (tid == 0) dsmem_or((ell & 1) ? flag1 : flag0, 1);
+        } else {
+          const int bad = split_pass_end(true);
+          if (__syncthreads_or(bad != 0) && tid == 0) dsmem_or((ell & 1) ? flag1 : flag0, 1);
+        }
       } else if (ell >= 1) {
         // my checks' syndromes s_c = XOR of the contribution bytes on their kpad edge slots
         int bad = 0;
