@@ -1292,7 +1292,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #endif
         if (do_dec && split && !skipc) {
           // (probe chunks run both halves: hp = 0 the other edge's half, hp = 1 mine, whose totals stay in md5)
-          uint32_t pnib = 0;
+          uint32_t pnib = 0, pweak = 0;
 #pragma unroll 1
           for (int hp = probe ? 0 : 1; hp < 2; ++hp) {
             const bool ka = (hp == 1) == kind_a;
@@ -1366,6 +1366,14 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
 #pragma unroll
               for (int b = 0; b < 5; ++b) mdp[b] = md5[b];
               const uint32_t sbp = split_sign_bits(mdp, lane);
+              // a probe must never contradict the whole decision, whose two halves come from the variable's two
+              // edges: a total that is not clearly away from zero (|M(alpha^i)| < 2^-6 |M(0)|, or M(0) zero or not
+              // finite -- the totals are left in mdp[0] of team lanes 0, 2, 4, 8, 10) voids the probe
+              {
+                const float t0 = fabsf(__shfl_sync(0xffffffffu, mdp[0], lane & 16));
+                const bool wk = !(fabsf(mdp[0]) >= 0.015625f * t0) || !(t0 > 0.0f) || !(t0 < 3.0e38f);
+                pweak |= (__ballot_sync(0xffffffffu, wk) >> (lane & 16)) & 0x0515u;
+              }
               const uint32_t nibp = ((sbp >> 1) ^ ((sbp & 1u) ? 0xFu : 0u)) & 0xFu;
               pnib |= ka ? nibp << 4 : nibp;
             }
@@ -1373,7 +1381,7 @@ __global__ void __launch_bounds__(NTHR, (NTHR <= 256 ? NB_CLUSTER_MINB : 1)) lf_
           if (probe && in_check && t == 0) {  // h_e x_v of my edge, for the probe check's syndrome
             uint32_t cb = 0;
             if (active && pnib != 0) cb = GE[GL[rr.var_h & 0xFFu] + GL[pnib]];
-            sh_pc[team & 63] = (ptag << 8) | cb;
+            sh_pc[team & 63] = ((pweak ? ptag ^ 0x800000u : ptag) << 8) | cb;
           }
           if (!do_cn) split_finish();
         }
