@@ -25,7 +25,10 @@ CASES = [  # name, point, GPU frames, oracle sample, kwargs
     ("C5", 4, 4096, 96, {"syndrome_mode": 1}),
 ]
 tot_stable_diff = 0
+only = sys.argv[1:]  # optional: config names to run
 for name, point, F, K, kw in CASES:
+    if only and name not in only:
+        continue
     c = synth.CONFIGS[name]
     _, llr, _ = config_inputs(name, 0, F, point=point)
     M, rows, cols, coeffs = synth.config_code(name)
